@@ -1,0 +1,125 @@
+/*
+ * sfsketch_cuda.h — C ABI of the B200-native SF sketch hot path.
+ *
+ * Every entry point replaces one numba kernel of the reference package
+ * (/root/reference/pkg/src/sfsketch/_kernels.py); the comment on each
+ * declaration cites the reference interface (file:line) it stands in for.
+ *
+ * Conventions (mirroring _kernels.py:1-16 and SURVEY.md §8(b)):
+ *   - Seeds (slim_seeds, fat_seeds, seeds) are HOST arrays of d uint64 values
+ *     (hashing.seed_array, hashing.py:132-137); they travel to the kernels by
+ *     value. Every other array argument is a DEVICE pointer owned by the
+ *     caller; state
+ *     arrays (counters, slim, fat, inc_counts) are mutated in place.
+ *   - Counters are uint32, row-major (d, w); the bucketed fat is (d, w, z)
+ *     C-order; tallies (inc_counts) are int64[d]; query estimates int64.
+ *   - Keys are described by (keys, key_kind, rec_len):
+ *       SFK_KEY_U64     uint64[n] (the reference's native key dtype)
+ *       SFK_KEY_U32     uint32[n], zero-extended to u64 (_ops.py:21)
+ *       SFK_KEY_RECORD  uint8[n * rec_len] packed byte records, hashed to a
+ *                       u64 key with FNV-1a-64 + finalize64, identical to
+ *                       hashing.key_from_string (hashing.py:124-129) for
+ *                       ASCII/UTF-8 bytes.
+ *   - ops are uint8[n], 0 = insert, 1 = delete (_kernels.py:28-29).
+ *   - Apply entry points never fail on sketch semantics: they write
+ *     {status, op_index, n_ins} into the device array `result` (int64[3])
+ *     with status codes OK=0 PHANTOM=1 SATURATED=2 UNSUPPORTED=3
+ *     (_kernels.py:21-24). A batch aborts at its first failing op: ops
+ *     before it are applied, the failing op leaves no trace.
+ *   - The int return value is a CUDA error code (0 = success), distinct
+ *     from the sketch status; sfk_last_error() describes it.
+ *   - Everything is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*). Apply calls need exclusive access to their state; queries on a
+ *     quiesced sketch may run concurrently on other streams or GPUs.
+ *   - Scratch memory is caller-provided: query sfk_*_workspace_size() and
+ *     pass a device buffer of at least that many bytes.
+ */
+#ifndef SFSKETCH_CUDA_H
+#define SFSKETCH_CUDA_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFK_KEY_U64 0
+#define SFK_KEY_U32 1
+#define SFK_KEY_RECORD 2
+
+#define SFK_OK 0
+#define SFK_PHANTOM 1
+#define SFK_SATURATED 2
+#define SFK_UNSUPPORTED 3
+
+/* SF variant codes: sf.py:57 (_FLAT_VARIANT_CODE) and sf.py:171-172 (mode) */
+#define SFK_VARIANT_SF1 1
+#define SFK_VARIANT_SF2 2
+#define SFK_VARIANT_SF3 3
+#define SFK_VARIANT_SF4 4
+#define SFK_VARIANT_SFF 6
+
+/* apply flags: SFK_FLAG_SEQUENTIAL forces the exact one-thread device engine
+ * (the reference loop replayed in order) instead of the parallel engine; the
+ * parity tests use it to cross-check the two on the GPU. */
+#define SFK_FLAG_SEQUENTIAL 1
+
+int sfk_abi_version(void);
+const char* sfk_last_error(void);
+
+/* Replaces _kernels.mix_batch (_kernels.py:56-59): out[t] = finalize64(keys[t]). */
+int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream);
+
+/* Key materialisation for any key kind (hashing.py:124-129 for records). */
+int sfk_load_keys(const void* keys, int key_kind, int rec_len, int64_t n, uint64_t* out, void* stream);
+
+/* Replaces _kernels.min_query (_kernels.py:229-241), called from
+ * SfSketch.query_many (sf.py:189-193), CmSketch/CuSketch.query_many
+ * (baselines.py:83-87, 167-171) and CollectorSketch.query_many
+ * (serialize.py:140-145). out[t] = min_i counters[i, h_i(key_t)]. */
+int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w,
+                  const void* keys, int key_kind, int rec_len, int64_t n, int64_t* out,
+                  void* stream);
+
+/* Replaces _kernels.cm_apply (_kernels.py:62-88), called from
+ * CmSketch.apply_ops (baselines.py:72-78). */
+size_t sfk_cm_workspace_size(int d, int64_t w, int64_t n);
+int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops,
+                 const void* keys, int key_kind, int rec_len, int64_t n, int64_t* inc_counts,
+                 int64_t* result, void* workspace, size_t workspace_bytes, int flags, void* stream);
+
+/* Replaces _kernels.cu_apply (_kernels.py:91-115), called from
+ * CuSketch.apply_ops (baselines.py:156-162). */
+size_t sfk_cu_workspace_size(int d, int64_t w, int64_t n);
+int sfk_cu_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops,
+                 const void* keys, int key_kind, int rec_len, int64_t n, int64_t* inc_counts,
+                 int64_t* result, void* workspace, size_t workspace_bytes, int flags, void* stream);
+
+/* Replaces _kernels.sf_flat_apply (_kernels.py:244-315; variants 1, 2, 3)
+ * and _kernels.sf_bucket_apply (_kernels.py:318-384; SF4 = mode 0,
+ * SFF = mode 1), called from SfSketch.apply_ops (sf.py:149-184).
+ *   variant  SFK_VARIANT_*; fat is (d, w_prime) for SF1/SF2/SF3 and
+ *            (d, w, z) for SF4/SFF; dsub is the (d, w) deletion sub-sketch
+ *            for SF2, else NULL.
+ *   slim_seeds = seed_array(master, 0, d); fat_seeds = seed_array(master, d, d)
+ *   (sf.py:115-116), except SF3 whose fat uses the slim seeds (sf.py:130). */
+size_t sfk_sf_workspace_size(int variant, int d, int64_t w, int64_t w_prime, int z, int64_t n);
+int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub,
+                 const uint64_t* slim_seeds, const uint64_t* fat_seeds, int d, int64_t w,
+                 int64_t w_prime, int z, const uint8_t* ops, const void* keys, int key_kind,
+                 int rec_len, int64_t n, int64_t* inc_counts, int64_t* result, void* workspace,
+                 size_t workspace_bytes, int flags, void* stream);
+
+/* Replaces _kernels.oracle_slim_apply (_kernels.py:387-411), called from
+ * SfSketch.oracle_assisted_apply (sf.py:199-229). */
+int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t w, const void* keys,
+                          int key_kind, int rec_len, const int64_t* true_counts, int64_t n,
+                          int64_t* inc_counts, int64_t* result, void* stream);
+
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFSKETCH_CUDA_H */

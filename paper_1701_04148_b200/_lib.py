@@ -1,0 +1,99 @@
+"""Loader for ``libsfsketch_cuda.so`` (the C ABI in ``include/sfsketch_cuda.h``).
+
+The library is built in-tree (``csrc/Makefile`` -> ``_lib/``). There is no
+CPU fallback: every sketch operation goes through this library, and using a
+sketch without a CUDA device or without the built library raises
+``RuntimeError`` naming what is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libsfsketch_cuda.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+KEY_U64, KEY_U32, KEY_RECORD = 0, 1, 2
+OK, PHANTOM, SATURATED, UNSUPPORTED = 0, 1, 2, 3
+VARIANT_CODE = {"sf1": 1, "sf2": 2, "sf3": 3, "sf4": 4, "sff": 6}
+FLAG_SEQUENTIAL = 1
+
+# every symbol the header declares; tests check the built library exports them
+EXPORTS = (
+    "sfk_abi_version",
+    "sfk_last_error",
+    "sfk_mix_batch",
+    "sfk_load_keys",
+    "sfk_min_query",
+    "sfk_cm_workspace_size",
+    "sfk_cm_apply",
+    "sfk_cu_workspace_size",
+    "sfk_cu_apply",
+    "sfk_sf_workspace_size",
+    "sfk_sf_apply",
+    "sfk_oracle_slim_apply",
+)
+
+_lib = None
+
+
+def build(jobs: int = 4) -> str:
+    """Compile the CUDA sources for sm_100a (nvcc cross-compiles; no GPU needed)."""
+    subprocess.run(["make", "-s", f"-j{jobs}", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def load_library() -> ctypes.CDLL:
+    """Load and type the library without touching a GPU."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"libsfsketch_cuda.so is not built ({LIB_PATH}); run `make -C {CSRC}` or __graft_entry__.build()"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+    L.sfk_abi_version.restype = I
+    L.sfk_last_error.restype = ctypes.c_char_p
+    L.sfk_mix_batch.argtypes = [P, I64, P, P]
+    L.sfk_load_keys.argtypes = [P, I, I, I64, P, P]
+    L.sfk_min_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
+    L.sfk_cm_workspace_size.argtypes = [I, I64, I64]
+    L.sfk_cm_workspace_size.restype = SZ
+    L.sfk_cu_workspace_size.argtypes = [I, I64, I64]
+    L.sfk_cu_workspace_size.restype = SZ
+    apply_args = [P, P, I, I64, P, P, I, I, I64, P, P, P, SZ, I, P]
+    L.sfk_cm_apply.argtypes = apply_args
+    L.sfk_cu_apply.argtypes = apply_args
+    L.sfk_sf_workspace_size.argtypes = [I, I, I64, I64, I, I64]
+    L.sfk_sf_workspace_size.restype = SZ
+    L.sfk_sf_apply.argtypes = [I, P, P, P, P, P, I, I64, I64, I, P, P, I, I, I64, P, P, P, SZ, I, P]
+    L.sfk_oracle_slim_apply.argtypes = [P, P, I, I64, P, I, I, P, I64, P, P, P]
+    _lib = L
+    return L
+
+
+def lib() -> ctypes.CDLL:
+    """The library, after checking that a CUDA device is usable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1701_04148_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return load_library()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load_library().sfk_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,156 @@
+"""Batch normalisation and status mapping (drop-in for ``sfsketch._ops``).
+
+The reference casts keys to contiguous uint64 and ops to uint8 in {0, 1}
+(``_ops.py:20-34``) and maps kernel status codes to exceptions
+(``_ops.py:44-59``). Here batches become CUDA tensors that the C ABI reads in
+place:
+
+* ``uint32`` keys stay 4 bytes wide and are zero-extended on the device
+  (bit-identical to the reference's cast, half the bytes to move);
+* signed or narrower integer keys are widened to int64 and reinterpreted as
+  uint64 exactly as numpy's cast does;
+* a 2-d ``uint8`` array of shape (n, rec_len) is a batch of fixed-size byte
+  records, hashed on the device with FNV-1a-64 + finalize64
+  (``hashing.key_from_string`` for the same bytes).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import (
+    ConfigurationError,
+    PhantomDeletionError,
+    SaturationError,
+    UnsupportedOperationError,
+)
+from .hashing import MASK64, key_from_bytes
+
+OP_INSERT = 0
+OP_DELETE = 1
+
+
+def device() -> torch.device:
+    _lib.lib()  # fail loudly without CUDA / the built library
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class KeyBatch:
+    tensor: torch.Tensor  # CUDA, contiguous
+    kind: int
+    rec_len: int
+    n: int
+
+    def ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+    def key_at(self, t: int) -> int:
+        v = self.tensor[t].cpu()
+        if self.kind == _lib.KEY_RECORD:
+            return key_from_bytes(bytes(v.numpy().tobytes()))
+        if self.kind == _lib.KEY_U32:
+            return int(v.item())
+        return int(v.view(torch.int64).item()) & MASK64
+
+    def slice(self, a: int, b: int) -> "KeyBatch":
+        return KeyBatch(self.tensor[a:b], self.kind, self.rec_len, b - a)
+
+
+def _to_device(t: torch.Tensor, dev: torch.device) -> torch.Tensor:
+    if t.device != dev:
+        t = t.to(dev, non_blocking=t.is_pinned())
+    return t.contiguous()
+
+
+def normalize_keys(keys) -> KeyBatch:
+    dev = device()
+    if isinstance(keys, KeyBatch):
+        return keys
+    if not isinstance(keys, torch.Tensor):
+        arr = np.asarray(keys)
+        if arr.dtype == object or arr.dtype.kind not in "iub":
+            arr = np.ascontiguousarray(keys, dtype=np.uint64)
+        if arr.dtype.kind == "b":
+            arr = arr.astype(np.uint64)
+        keys = torch.from_numpy(np.ascontiguousarray(arr))
+    t = keys
+    if t.dtype == torch.uint8 and t.dim() == 2:
+        t = _to_device(t, dev)
+        return KeyBatch(t, _lib.KEY_RECORD, int(t.shape[1]), int(t.shape[0]))
+    if t.dim() != 1:
+        raise ConfigurationError("keys must be a 1-d sequence")
+    if t.dtype == torch.uint32:
+        return KeyBatch(_to_device(t, dev), _lib.KEY_U32, 0, int(t.shape[0]))
+    if t.dtype == torch.uint64:
+        return KeyBatch(_to_device(t, dev), _lib.KEY_U64, 0, int(t.shape[0]))
+    if t.dtype == torch.int64:
+        return KeyBatch(_to_device(t, dev).view(torch.uint64), _lib.KEY_U64, 0, int(t.shape[0]))
+    if t.dtype in (torch.int32, torch.int16, torch.int8, torch.uint8, torch.uint16, torch.bool):
+        w = _to_device(t, dev).to(torch.int64)
+        return KeyBatch(w.view(torch.uint64), _lib.KEY_U64, 0, int(t.shape[0]))
+    raise ConfigurationError(f"keys must be integers, got {t.dtype}")
+
+
+def normalize_stream(ops, keys):
+    dev = device()
+    kb = normalize_keys(keys)
+    if isinstance(ops, torch.Tensor):
+        o = ops
+    else:
+        o = torch.from_numpy(np.ascontiguousarray(ops, dtype=np.uint8))
+    if o.dim() != 1 or int(o.shape[0]) != kb.n:
+        raise ConfigurationError("ops and keys must be 1-d sequences of equal length")
+    if o.dtype != torch.uint8:
+        o = o.to(torch.uint8) if o.device == dev else o.to(torch.uint8)
+    o = _to_device(o, dev)
+    if kb.n and bool((o > OP_DELETE).any()):
+        raise ConfigurationError("op codes must be 0 (insert) or 1 (delete)")
+    return o, kb
+
+
+def single_op(op_code: int, key: int):
+    return (
+        np.array([op_code], dtype=np.uint8),
+        np.array([int(key) & MASK64], dtype=np.uint64),
+    )
+
+
+def raise_for_status(status: int, op_index: int, keys: KeyBatch) -> None:
+    """``_ops.py:44-59``: the same exception types and messages."""
+    if status == _lib.OK:
+        return
+    key = keys.key_at(op_index)
+    if status == _lib.PHANTOM:
+        raise PhantomDeletionError(f"op {op_index}: deleting key {key} would drive a counter below zero")
+    if status == _lib.SATURATED:
+        raise SaturationError(f"op {op_index}: counter for key {key} is saturated")
+    if status == _lib.UNSUPPORTED:
+        raise UnsupportedOperationError(f"op {op_index}: this sketch does not support that operation")
+    raise AssertionError(f"unexpected kernel status {status}")
+
+
+class Scratch:
+    """Per-sketch device scratch: the result triple and a growable workspace."""
+
+    def __init__(self):
+        self.result = None
+        self.ws = None
+
+    def get(self, nbytes: int):
+        dev = device()
+        if self.result is None or self.result.device != dev:
+            self.result = torch.zeros(3, dtype=torch.int64, device=dev)
+            self.ws = None
+        if self.ws is None or self.ws.numel() < nbytes:
+            self.ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+        return self.result, self.ws
+
+    @staticmethod
+    def read(result: torch.Tensor):
+        s, i, n = (int(v) for v in result.tolist())
+        return s, i, n

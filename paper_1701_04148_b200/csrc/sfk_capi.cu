@@ -1,0 +1,257 @@
+// extern "C" entry points of libsfsketch_cuda.so (declared in
+// include/sfsketch_cuda.h). Each one validates its arguments, picks the
+// parallel engine or the exact sequential device engine, and splits very
+// large batches into chunks the 32-bit pair encoding can address.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+
+#include "sfk_common.cuh"
+
+namespace sfk {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+int sm_count() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!sms[dev]) {
+    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (sms[dev] < 1) sms[dev] = 1;
+  }
+  return sms[dev];
+}
+
+// implemented in sfk_query.cu / sfk_seq.cu / sfk_sf.cu
+int launch_min_query(const uint32_t*, const uint64_t*, int, int64_t, KeySrc, int64_t, int64_t*, cudaStream_t);
+int launch_mix_batch(const uint64_t*, int64_t, uint64_t*, cudaStream_t);
+int launch_load_keys(KeySrc, int64_t, uint64_t*, cudaStream_t);
+int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* s_seeds,
+                     const uint64_t* f_seeds, int d, int64_t w, int64_t wp, int64_t z, const uint8_t* ops, KeySrc ks,
+                     const int64_t* true_counts, int64_t n, int64_t* inc, int64_t* result, cudaStream_t st);
+size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n);
+int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
+                   int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
+                   int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st);
+int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64_t cells, void* ws, size_t ws_bytes,
+                  Stats* host, cudaStream_t st);
+int cm_fast(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
+            cudaStream_t st);
+
+__global__ void set_result_k(int64_t* result, int64_t status, int64_t idx, int64_t n_ins, int64_t* inc, int d,
+                             int64_t inc_add) {
+  result[0] = status;
+  result[1] = idx;
+  result[2] = n_ins;
+  if (inc)
+    for (int i = 0; i < d; ++i) inc[i] += inc_add;
+}
+
+// parallel kinds (sfk_sf.cu): 0 SFF, 1 SF1, 2 CU, 3 CM exact
+static int64_t chunk_ops(int d, int z) {
+  // t << (kb + 1) must fit 32 bits and d * n must fit a signed int
+  int kb = 0;
+  while ((1 << kb) < std::max(z, 1)) ++kb;
+  int64_t lim_t = (int64_t)1 << (31 - kb);
+  int64_t lim_n = ((int64_t)1 << 30) / std::max(d, 1);
+  return std::min(lim_t, lim_n);
+}
+
+static const char* key_ptr(const void* keys, int key_kind, int rec_len, int64_t t0) {
+  const char* p = static_cast<const char*>(keys);
+  int64_t sz = key_kind == SFK_KEY_U64 ? 8 : key_kind == SFK_KEY_U32 ? 4 : rec_len;
+  return p + t0 * sz;
+}
+
+static int check_common(int d, int64_t w, int key_kind, int rec_len) {
+  if (d < 1 || d > MAXSEEDS) { set_error("d must lie in [1, %d], got %d", MAXSEEDS, d); return 1; }
+  if (w < 1 || (uint64_t)d * (uint64_t)w >= (1ull << 32)) { set_error("bad width w=%lld", (long long)w); return 1; }
+  if (key_kind != SFK_KEY_U64 && key_kind != SFK_KEY_U32 && key_kind != SFK_KEY_RECORD) {
+    set_error("unknown key kind %d", key_kind);
+    return 1;
+  }
+  if (key_kind == SFK_KEY_RECORD && rec_len < 1) { set_error("record keys need rec_len >= 1"); return 1; }
+  return 0;
+}
+
+// Run `body(t0, cnt, result)` over chunks; accumulate {status, op_index, n_ins}.
+template <typename F>
+static int chunked(int64_t n, int64_t chunk, int64_t* result, cudaStream_t st, F body) {
+  if (n <= 0) {
+    set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, 0, nullptr, 0, 0);
+    return check_launch("set_result");
+  }
+  if (n <= chunk) return body((int64_t)0, n);
+  int64_t total_ins = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += chunk) {
+    const int64_t cnt = std::min(chunk, n - t0);
+    if (int r = body(t0, cnt)) return r;
+    int64_t h[3];
+    cudaMemcpyAsync(h, result, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { set_error("chunk sync: %s", cudaGetErrorString(e)); return (int)e; }
+    total_ins += h[2];
+    if (h[0] != SFK_OK) {
+      set_result_k<<<1, 1, 0, st>>>(result, h[0], t0 + h[1], total_ins, nullptr, 0, 0);
+      return check_launch("set_result");
+    }
+  }
+  set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, total_ins, nullptr, 0, 0);
+  return check_launch("set_result");
+}
+
+}  // namespace sfk
+
+using namespace sfk;
+
+extern "C" {
+
+int sfk_abi_version(void) { return 1; }
+
+const char* sfk_last_error(void) { return g_err; }
+
+int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream) {
+  return launch_mix_batch(keys, n, out, (cudaStream_t)stream);
+}
+
+int sfk_load_keys(const void* keys, int key_kind, int rec_len, int64_t n, uint64_t* out, void* stream) {
+  if (check_common(1, 1, key_kind, rec_len)) return 1;
+  return launch_load_keys(KeySrc{keys, key_kind, rec_len}, n, out, (cudaStream_t)stream);
+}
+
+int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind,
+                  int rec_len, int64_t n, int64_t* out, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  return launch_min_query(counters, seeds, d, w, KeySrc{keys, key_kind, rec_len}, n, out, (cudaStream_t)stream);
+}
+
+size_t sfk_cm_workspace_size(int d, int64_t w, int64_t n) {
+  if (d > MAXD) return 256;
+  return parallel_workspace_size(3, d, w, 0, 1, std::min<int64_t>(n, chunk_ops(d, 1)));
+}
+
+int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, const void* keys,
+                 int key_kind, int rec_len, int64_t n, int64_t* inc_counts, int64_t* result, void* workspace,
+                 size_t workspace_bytes, int flags, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+    return launch_seq_apply(0, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops,
+                            KeySrc{keys, key_kind, rec_len}, nullptr, n, inc_counts, result, st);
+  return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    Stats s;
+    if (int r = collect_stats(ops + t0, cnt, counters, (int64_t)d * w, workspace, workspace_bytes, &s, st)) return r;
+    // no insert can meet a saturated counter and no delete a zero one
+    const bool safe = ((uint64_t)s.cmax + s.n_ins <= 0xFFFFFFFFull) && (s.n_del == 0 || (uint64_t)s.cmin >= s.n_del);
+    if (safe) {
+      if (int r = cm_fast(counters, seeds, d, w, ops + t0, ks, cnt, st)) return r;
+      set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, (int64_t)s.n_ins, inc_counts, d, (int64_t)s.n_ins);
+      return check_launch("set_result");
+    }
+    return parallel_apply(3, counters, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,
+                          workspace, workspace_bytes, st);
+  });
+}
+
+size_t sfk_cu_workspace_size(int d, int64_t w, int64_t n) {
+  if (d > MAXD) return 256;
+  return parallel_workspace_size(2, d, w, 0, 1, std::min<int64_t>(n, chunk_ops(d, 1)));
+}
+
+int sfk_cu_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, const void* keys,
+                 int key_kind, int rec_len, int64_t n, int64_t* inc_counts, int64_t* result, void* workspace,
+                 size_t workspace_bytes, int flags, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  KeySrc all{keys, key_kind, rec_len};
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+    return launch_seq_apply(1, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops, all, nullptr, n,
+                            inc_counts, result, st);
+  return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    Stats s;
+    if (int r = collect_stats(ops + t0, cnt, counters, (int64_t)d * w, workspace, workspace_bytes, &s, st)) return r;
+    // the CU min can reach 0xFFFFFFFF only if some counter climbs that far:
+    // counters grow by at most one per insert
+    if ((uint64_t)s.cmax + s.ins_before_first_del < 0xFFFFFFFFull)
+      return parallel_apply(2, counters, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,
+                            workspace, workspace_bytes, st);
+    return launch_seq_apply(1, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, nullptr, cnt,
+                            inc_counts, result, st);
+  });
+}
+
+static int sf_parallel_kind(int variant, int d, int z) {
+  if (d > MAXD) return -1;
+  if (variant == SFK_VARIANT_SF1) return 1;
+  if (variant == SFK_VARIANT_SFF && z >= 1 && z <= 8) return 0;
+  return -1;
+}
+
+size_t sfk_sf_workspace_size(int variant, int d, int64_t w, int64_t w_prime, int z, int64_t n) {
+  const int kind = sf_parallel_kind(variant, d, z);
+  if (kind < 0) return 256;
+  return parallel_workspace_size(kind, d, w, w_prime, z, std::min<int64_t>(n, chunk_ops(d, kind == 0 ? z : 1)));
+}
+
+int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
+                 const uint64_t* fat_seeds, int d, int64_t w, int64_t w_prime, int z, const uint8_t* ops,
+                 const void* keys, int key_kind, int rec_len, int64_t n, int64_t* inc_counts, int64_t* result,
+                 void* workspace, size_t workspace_bytes, int flags, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool flat = variant == SFK_VARIANT_SF1 || variant == SFK_VARIANT_SF2 || variant == SFK_VARIANT_SF3;
+  const bool bucketed = variant == SFK_VARIANT_SF4 || variant == SFK_VARIANT_SFF;
+  if (!flat && !bucketed) { set_error("unknown SF variant %d", variant); return 1; }
+  if (z < 1) { set_error("z must be >= 1"); return 1; }
+  if (flat && (w_prime < w || (uint64_t)d * (uint64_t)w_prime >= (1ull << 32))) {
+    set_error("bad w_prime=%lld", (long long)w_prime);
+    return 1;
+  }
+  if (bucketed && (uint64_t)d * (uint64_t)w * (uint64_t)z >= (1ull << 32)) { set_error("fat too large"); return 1; }
+  if (variant == SFK_VARIANT_SF2 && dsub == nullptr) { set_error("SF2 needs the deletion sub-sketch"); return 1; }
+  const int kind = sf_parallel_kind(variant, d, z);
+  KeySrc all{keys, key_kind, rec_len};
+  if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0) {
+    if (flat)
+      return launch_seq_apply(2, variant, slim, fat, dsub, slim_seeds, fat_seeds, d, w, w_prime, w_prime / w, ops, all,
+                              nullptr, n, inc_counts, result, st);
+    return launch_seq_apply(3, variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, nullptr, slim_seeds, fat_seeds, d, w, 0,
+                            z, ops, all, nullptr, n, inc_counts, result, st);
+  }
+  return chunked(n, chunk_ops(d, kind == 0 ? z : 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    return parallel_apply(kind, slim, fat, slim_seeds, fat_seeds, d, w, w_prime, z, ops + t0, ks, cnt, inc_counts,
+                          result, workspace, workspace_bytes, st);
+  });
+}
+
+int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind,
+                          int rec_len, const int64_t* true_counts, int64_t n, int64_t* inc_counts, int64_t* result,
+                          void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  return launch_seq_apply(4, 0, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr,
+                          KeySrc{keys, key_kind, rec_len}, true_counts, n, inc_counts, result, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// Exact sequential device engine: one thread replays a batch in stream order
+// with the reference's per-op rules (_kernels.py:62-115, 244-411).
+//
+// It is the GPU path for the configurations the parallel engines do not
+// cover (SF2/SF3/SF4 variants, d > 8, CU batches that could saturate, the
+// oracle-assisted mode) and the cross-check the parity tests run against the
+// parallel engines (flag SFK_FLAG_SEQUENTIAL). It is slow (one L2 round trip
+// per counter touch) but bit-exact by construction.
+#include "sfk_common.cuh"
+
+namespace sfk {
+
+struct SeqArgs {
+  uint32_t* slim;  // counters for CM/CU
+  uint32_t* fat;
+  uint32_t* dsub;
+  Seeds<MAXSEEDS> s_seeds;  // slim / bucket / CM seeds
+  Seeds<MAXSEEDS> f_seeds;  // fat / slot seeds
+  int d;
+  int64_t w, wp, z;
+  Mod wm, wpm, zm;
+  const uint8_t* ops;
+  KeySrc keys;
+  const int64_t* true_counts;
+  int64_t n;
+  int64_t* inc;
+  int64_t* result;
+};
+
+// kind: 0 CM, 1 CU, 2 SF flat (variant 1/2/3), 3 SF bucketed (mode 0/1/2), 4 oracle-assisted slim
+__global__ void seq_apply_k(SeqArgs a, int kind, int variant) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int d = a.d;
+  int64_t idx[MAXSEEDS], idx2[MAXSEEDS];
+  int64_t n_ins = 0;
+  int64_t status = SFK_OK, bad = -1;
+  const int64_t w = a.w, wp = a.wp, z = a.z;
+  for (int64_t t = 0; t < a.n; ++t) {
+    const uint64_t key = load_key(a.keys, t);
+    const int op = a.ops ? a.ops[t] : 0;
+    if (kind == 0) {  // cm_apply, _kernels.py:62-88
+      bool fail = false;
+      for (int i = 0; i < d; ++i) {
+        idx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        uint32_t v = a.slim[i * w + idx[i]];
+        if (op == 0 ? v == U32MAX : v == 0u) fail = true;
+      }
+      if (fail) { status = op == 0 ? SFK_SATURATED : SFK_PHANTOM; bad = t; break; }
+      for (int i = 0; i < d; ++i) {
+        if (op == 0) { a.slim[i * w + idx[i]] += 1u; a.inc[i] += 1; }
+        else a.slim[i * w + idx[i]] -= 1u;
+      }
+      if (op == 0) ++n_ins;
+    } else if (kind == 1 || kind == 4) {  // cu_apply 91-115, oracle_slim_apply 387-411
+      if (kind == 1 && op != 0) { status = SFK_UNSUPPORTED; bad = t; break; }
+      uint64_t m = U64MAX;
+      for (int i = 0; i < d; ++i) {
+        idx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        uint64_t v = a.slim[i * w + idx[i]];
+        if (v < m) m = v;
+      }
+      bool raise = true;
+      if (kind == 4) raise = m < (uint64_t)a.true_counts[t];
+      if (raise) {
+        if (m >= 0xFFFFFFFFull) { status = SFK_SATURATED; bad = t; break; }
+        for (int i = 0; i < d; ++i)
+          if ((uint64_t)a.slim[i * w + idx[i]] == m) { a.slim[i * w + idx[i]] += 1u; a.inc[i] += 1; }
+      }
+      ++n_ins;
+    } else if (kind == 2) {  // sf_flat_apply 244-315
+      int64_t* sidx = idx;
+      int64_t* fidx = idx2;
+      for (int i = 0; i < d; ++i) {
+        if (variant == 3) {
+          uint64_t g = bucket(key, a.f_seeds.s[i], a.wpm);
+          fidx[i] = (int64_t)g;
+          sidx[i] = (int64_t)fmod64(g, a.wm);
+        } else {
+          fidx[i] = (int64_t)bucket(key, a.f_seeds.s[i], a.wpm);
+          sidx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        }
+      }
+      if (op == 0) {
+        bool fail = false;
+        for (int i = 0; i < d; ++i) {
+          if (a.fat[i * wp + fidx[i]] == U32MAX) fail = true;
+          if (variant == 2 && a.dsub[i * w + sidx[i]] == U32MAX) fail = true;
+        }
+        if (fail) { status = SFK_SATURATED; bad = t; break; }
+        uint64_t bmin = U64MAX;
+        for (int i = 0; i < d; ++i) {
+          a.fat[i * wp + fidx[i]] += 1u;
+          uint64_t v = a.fat[i * wp + fidx[i]];
+          if (v < bmin) bmin = v;
+          if (variant == 2) a.dsub[i * w + sidx[i]] += 1u;
+        }
+        uint64_t m = U64MAX;
+        for (int i = 0; i < d; ++i) {
+          uint64_t v = a.slim[i * w + sidx[i]];
+          if (v < m) m = v;
+        }
+        if (m < bmin)
+          for (int i = 0; i < d; ++i)
+            if ((uint64_t)a.slim[i * w + sidx[i]] == m) { a.slim[i * w + sidx[i]] += 1u; a.inc[i] += 1; }
+        ++n_ins;
+      } else {
+        if (variant == 1) { status = SFK_UNSUPPORTED; bad = t; break; }
+        bool fail = false;
+        for (int i = 0; i < d; ++i) {
+          if (a.fat[i * wp + fidx[i]] == 0u) fail = true;
+          if (variant == 2 && a.dsub[i * w + sidx[i]] == 0u) fail = true;
+        }
+        if (fail) { status = SFK_PHANTOM; bad = t; break; }
+        for (int i = 0; i < d; ++i) {
+          a.fat[i * wp + fidx[i]] -= 1u;
+          uint32_t* sc = &a.slim[i * w + sidx[i]];
+          if (variant == 2) {
+            a.dsub[i * w + sidx[i]] -= 1u;
+            if (*sc > a.dsub[i * w + sidx[i]]) *sc -= 1u;
+          } else {
+            uint64_t total = 0;
+            for (int64_t m2 = 0; m2 < z; ++m2) total += a.fat[i * wp + sidx[i] + m2 * w];
+            if ((uint64_t)*sc > total) *sc -= 1u;
+          }
+        }
+      }
+    } else {  // kind 3: sf_bucket_apply 318-384
+      int64_t* jidx = idx;
+      int64_t* kidx = idx2;
+      for (int i = 0; i < d; ++i) {
+        jidx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        kidx[i] = (int64_t)bucket(key, a.f_seeds.s[i], a.zm);
+      }
+#define FATC(i, j, k) a.fat[((int64_t)(i) * w + (j)) * z + (k)]
+      if (op == 0) {
+        bool fail = false;
+        for (int i = 0; i < d; ++i)
+          if (FATC(i, jidx[i], kidx[i]) == U32MAX) fail = true;
+        if (fail) { status = SFK_SATURATED; bad = t; break; }
+        uint64_t bmin = U64MAX;
+        for (int i = 0; i < d; ++i) {
+          FATC(i, jidx[i], kidx[i]) += 1u;
+          uint64_t v = FATC(i, jidx[i], kidx[i]);
+          if (v < bmin) bmin = v;
+        }
+        uint64_t m = U64MAX;
+        for (int i = 0; i < d; ++i) {
+          uint64_t v = a.slim[i * w + jidx[i]];
+          if (v < m) m = v;
+        }
+        if (m < bmin)
+          for (int i = 0; i < d; ++i)
+            if ((uint64_t)a.slim[i * w + jidx[i]] == m) { a.slim[i * w + jidx[i]] += 1u; a.inc[i] += 1; }
+        ++n_ins;
+      } else {
+        bool fail = false;
+        for (int i = 0; i < d; ++i)
+          if (FATC(i, jidx[i], kidx[i]) == 0u) fail = true;
+        if (fail) { status = SFK_PHANTOM; bad = t; break; }
+        for (int i = 0; i < d; ++i) {
+          const int64_t j = jidx[i];
+          uint32_t pre = 0;
+          if (variant == 2)
+            for (int64_t k = 0; k < z; ++k) pre = max(pre, FATC(i, j, k));
+          FATC(i, j, kidx[i]) -= 1u;
+          uint32_t* sc = &a.slim[i * w + j];
+          if (variant == 0) {
+            uint64_t total = 0;
+            for (int64_t k = 0; k < z; ++k) total += FATC(i, j, k);
+            if ((uint64_t)*sc > total) *sc -= 1u;
+          } else {
+            uint32_t mx = 0;
+            for (int64_t k = 0; k < z; ++k) mx = max(mx, FATC(i, j, k));
+            if (variant == 1) {
+              if (*sc > mx) *sc = mx;
+            } else if (mx != pre && *sc > mx) {
+              *sc = mx;
+            }
+          }
+        }
+      }
+#undef FATC
+    }
+  }
+  a.result[0] = status;
+  a.result[1] = bad;
+  a.result[2] = n_ins;
+}
+
+int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub,
+                     const uint64_t* s_seeds, const uint64_t* f_seeds, int d, int64_t w, int64_t wp, int64_t z,
+                     const uint8_t* ops, KeySrc ks, const int64_t* true_counts, int64_t n, int64_t* inc,
+                     int64_t* result, cudaStream_t st) {
+  SeqArgs a;
+  a.slim = slim;
+  a.fat = fat;
+  a.dsub = dsub;
+  for (int i = 0; i < d; ++i) {
+    a.s_seeds.s[i] = s_seeds ? s_seeds[i] : 0;
+    a.f_seeds.s[i] = f_seeds ? f_seeds[i] : 0;
+  }
+  a.d = d;
+  a.w = w;
+  a.wp = wp > 0 ? wp : 1;
+  a.z = z > 0 ? z : 1;
+  a.wm = make_mod((uint64_t)w);
+  a.wpm = make_mod((uint64_t)a.wp);
+  a.zm = make_mod((uint64_t)a.z);
+  a.ops = ops;
+  a.keys = ks;
+  a.true_counts = true_counts;
+  a.n = n;
+  a.inc = inc;
+  a.result = result;
+  seq_apply_k<<<1, 32, 0, st>>>(a, kind, variant);
+  return check_launch("seq_apply");
+}
+
+}  // namespace sfk

@@ -1,0 +1,1011 @@
+// Parallel, bit-exact batch update engine for the SF sketch (SF1, SFF), the
+// CU baseline and the exact-validation path of the CM baseline.
+//
+// The reference applies ops one at a time (_kernels.py:244-384, 62-115).
+// This file computes the same final state with a fixed pipeline of
+// data-parallel passes:
+//
+//   1. hash_emit     fused key load + hash: for every op t and row i emit the
+//                    counter cell it touches as a (cell, t|op|slot) pair.
+//   2. radix sort    stable by cell (CUB onesweep), so every cell's ops sit
+//                    contiguously in stream order.
+//   3. segscan       a segmented prefix scan over the sorted pairs. Fat
+//                    counts commute, so the fat value right after op t is
+//                    initial + (#inserts - #deletes at that cell up to t):
+//                    per-op observations (post-insert own count -> b_min,
+//                    bucket max after a delete -> clamp), exact
+//                    saturation/phantom detection (first failing op t* =
+//                    atomicMin), the final fat, and for the slim cells each
+//                    op's rank in its cell and its predecessor op.
+//   4. runs_mark     consecutive same-key ops whose d slim cells were last
+//                    touched by that same key form a "run"; a run is
+//                    contiguous in the row-0 sorted order and is replayed
+//                    by one thread in registers.
+//   5. slim_engine   ordered dataflow engine over runs: each slim cell is a
+//                    64-bit word (seq << 32 | value); a run whose head has
+//                    rank r_i in cell i waits until seq_i == r_i for all its
+//                    cells, replays its ops, and publishes (r_i + L, value)
+//                    with one store per cell. Runs are claimed in stream
+//                    order of their heads, so the earliest unfinished run is
+//                    always ready and the engine cannot deadlock.
+//
+// Insert-only runs collapse in closed form (b_min strictly increases along
+// a same-key insert run, so once a raise happens every later op raises):
+// s raises give c_i' = max(c_i, m0 + s).
+#include <cub/cub.cuh>
+
+#include "sfk_common.cuh"
+
+namespace sfk {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- shared state
+struct Ctl {
+  uint32_t fail_t;     // first failing op (NONE32 if none)
+  uint32_t ticket;     // engine run ticket
+  unsigned long long n_ins;  // inserts applied (t < t*)
+  uint32_t n_runs;
+  uint32_t pad;
+};
+
+// ---------------------------------------------------------------- 1. hash_emit
+// kind: 0 bucketed (SFF: cell = bucket, slot in the low bits of val)
+//       1 flat fat (cell = fat index), 2 slim-only (cell = slim index)
+template <int D>
+struct HashArgs {
+  KeySrc keys;
+  const uint8_t* ops;
+  int64_t n;
+  Seeds<D> cell_seeds;
+  Seeds<D> slot_seeds;
+  Mod cm;  // cell range per row
+  Mod zm;  // slot range
+  uint32_t row_cells;  // cells per row
+  int kb;              // slot bits
+  uint32_t* key_out;
+  uint32_t* val_out;
+  int unsupported_deletes;  // SF1 / CU: a delete is the failing op
+  Ctl* ctl;
+};
+
+template <int D, int KIND>
+__global__ void __launch_bounds__(256) hash_emit_k(HashArgs<D> a) {
+  uint32_t local_fail = NONE32;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = load_key(a.keys, t);
+    const uint32_t op = a.ops[t];
+    if (a.unsupported_deletes && op != 0 && local_fail == NONE32) local_fail = (uint32_t)t;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      uint32_t cell = (uint32_t)i * a.row_cells + (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
+      uint32_t v = ((uint32_t)t << (a.kb + 1)) | (op << a.kb);
+      if (KIND == 0) v |= (uint32_t)bucket(key, a.slot_seeds.s[i], a.zm);
+      a.key_out[(int64_t)i * a.n + t] = cell;
+      a.val_out[(int64_t)i * a.n + t] = v;
+    }
+  }
+  // grid-stride order means a thread's first delete is its smallest
+  if (local_fail != NONE32) atomicMin(&a.ctl->fail_t, local_fail);
+}
+
+// ---------------------------------------------------------------- 3. segscan
+template <int Z>
+struct SegState {
+  uint32_t flag;  // a segment head lies inside this span
+  uint32_t head;  // position of the last head inside the span (if flag)
+  int32_t v[Z];   // net count deltas since that head (or over the span)
+};
+
+template <int Z>
+__device__ __forceinline__ SegState<Z> seg_combine(const SegState<Z>& a, const SegState<Z>& b) {
+  if (b.flag) return b;
+  SegState<Z> r;
+  r.flag = a.flag;
+  r.head = a.head;
+#pragma unroll
+  for (int k = 0; k < Z; ++k) r.v[k] = a.v[k] + b.v[k];
+  return r;
+}
+
+template <int Z>
+__device__ __forceinline__ SegState<Z> seg_identity() {
+  SegState<Z> r;
+  r.flag = 0;
+  r.head = 0;
+#pragma unroll
+  for (int k = 0; k < Z; ++k) r.v[k] = 0;
+  return r;
+}
+
+template <int Z>
+__device__ __forceinline__ SegState<Z> shfl_state(const SegState<Z>& s, int src_delta, bool up) {
+  SegState<Z> r;
+  if (up) {
+    r.flag = __shfl_up_sync(0xffffffffu, s.flag, src_delta);
+    r.head = __shfl_up_sync(0xffffffffu, s.head, src_delta);
+#pragma unroll
+    for (int k = 0; k < Z; ++k) r.v[k] = __shfl_up_sync(0xffffffffu, s.v[k], src_delta);
+  } else {
+    r.flag = __shfl_down_sync(0xffffffffu, s.flag, src_delta);
+    r.head = __shfl_down_sync(0xffffffffu, s.head, src_delta);
+#pragma unroll
+    for (int k = 0; k < Z; ++k) r.v[k] = __shfl_down_sync(0xffffffffu, s.v[k], src_delta);
+  }
+  return r;
+}
+
+// element e as a one-element span
+template <int Z, bool HAS_FAT>
+__device__ __forceinline__ SegState<Z> elem_state(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                  uint32_t e, int kb) {
+  SegState<Z> s = seg_identity<Z>();
+  const uint32_t c = keys[e];
+  s.flag = (e == 0) || (keys[e - 1] != c);
+  s.head = e;
+  if (HAS_FAT) {
+    const uint32_t v = vals[e];
+    const uint32_t k = v & ((1u << kb) - 1u);
+    const int32_t dl = ((v >> kb) & 1u) ? -1 : 1;
+#pragma unroll
+    for (int q = 0; q < Z; ++q) s.v[q] = (q == (int)k) ? dl : 0;
+  }
+  return s;
+}
+
+// exclusive block scan of per-thread aggregates (ordered, non-commutative)
+template <int Z>
+__device__ __forceinline__ SegState<Z> block_exclusive(SegState<Z> agg, SegState<Z>* warp_tot, SegState<Z>* block_tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  SegState<Z> inc = agg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    SegState<Z> o = shfl_state<Z>(inc, off, true);
+    if (lane >= off) inc = seg_combine<Z>(o, inc);
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SegState<Z> run = seg_identity<Z>();
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+      SegState<Z> t = warp_tot[w];
+      warp_tot[w] = run;  // exclusive prefix of warp w
+      run = seg_combine<Z>(run, t);
+    }
+    *block_tot = run;
+  }
+  __syncthreads();
+  SegState<Z> excl_in_warp = shfl_state<Z>(inc, 1, true);
+  if (lane == 0) excl_in_warp = seg_identity<Z>();
+  return seg_combine<Z>(warp_tot[wid], excl_in_warp);
+}
+
+template <int Z, bool HAS_FAT>
+__global__ void __launch_bounds__(SCAN_THREADS) segscan_reduce_k(const uint32_t* __restrict__ keys,
+                                                                 const uint32_t* __restrict__ vals, uint32_t N, int kb,
+                                                                 SegState<Z>* __restrict__ tile_agg) {
+  __shared__ SegState<Z> warp_tot[SCAN_THREADS / 32];
+  __shared__ SegState<Z> block_tot;
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  SegState<Z> agg = seg_identity<Z>();
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    uint32_t e = base + q;
+    if (e < N) agg = seg_combine<Z>(agg, elem_state<Z, HAS_FAT>(keys, vals, e, kb));
+  }
+  (void)block_exclusive<Z>(agg, warp_tot, &block_tot);
+  if (threadIdx.x == 0) tile_agg[blockIdx.x] = block_tot;
+}
+
+// single block: exclusive scan of tile aggregates -> carry-in per tile
+template <int Z>
+__global__ void __launch_bounds__(1024) segscan_tiles_k(SegState<Z>* __restrict__ tile_agg, uint32_t ntiles) {
+  __shared__ SegState<Z> warp_tot[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(ntiles, threadIdx.x * per), hi = min(ntiles, lo + per);
+  SegState<Z> agg = seg_identity<Z>();
+  for (uint32_t k = lo; k < hi; ++k) agg = seg_combine<Z>(agg, tile_agg[k]);
+  SegState<Z> inc = agg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    SegState<Z> o = shfl_state<Z>(inc, off, true);
+    if (lane >= off) inc = seg_combine<Z>(o, inc);
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SegState<Z> run = seg_identity<Z>();
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      SegState<Z> t = warp_tot[w];
+      warp_tot[w] = run;
+      run = seg_combine<Z>(run, t);
+    }
+  }
+  __syncthreads();
+  SegState<Z> ex = shfl_state<Z>(inc, 1, true);
+  if (lane == 0) ex = seg_identity<Z>();
+  SegState<Z> run = seg_combine<Z>(warp_tot[wid], ex);
+  for (uint32_t k = lo; k < hi; ++k) {
+    SegState<Z> t = tile_agg[k];
+    tile_agg[k] = run;  // exclusive
+    run = seg_combine<Z>(run, t);
+  }
+}
+
+struct ScanOut {
+  const uint32_t* fat_init;  // snapshot of the fat (cell-major, Z per cell)
+  uint32_t* fat_out;         // final fat (written at segment ends)
+  uint32_t* obs;             // [t*D + row]: post own count (insert) / bucket max (delete)
+  uint2* links;              // [t*D + row]: {rank in cell, previous op or NONE}
+  uint32_t n;                // ops
+  uint32_t D;
+  uint32_t row_cells;
+  Ctl* ctl;
+};
+
+template <int Z, bool HAS_FAT, bool WRITE_OBS, bool WRITE_LINKS>
+__global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* __restrict__ keys,
+                                                                const uint32_t* __restrict__ vals, uint32_t N, int kb,
+                                                                const SegState<Z>* __restrict__ carry, ScanOut o) {
+  __shared__ SegState<Z> warp_tot[SCAN_THREADS / 32];
+  __shared__ SegState<Z> block_tot;
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  SegState<Z> agg = seg_identity<Z>();
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    uint32_t e = base + q;
+    if (e < N) agg = seg_combine<Z>(agg, elem_state<Z, HAS_FAT>(keys, vals, e, kb));
+  }
+  SegState<Z> run = block_exclusive<Z>(agg, warp_tot, &block_tot);
+  run = seg_combine<Z>(carry[blockIdx.x], run);
+  uint32_t local_fail = NONE32;
+  uint32_t prev_t = (base > 0 && base < N) ? (vals[base - 1] >> (kb + 1)) : NONE32;
+#pragma unroll 1
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e >= N) break;
+    const SegState<Z> s = elem_state<Z, HAS_FAT>(keys, vals, e, kb);
+    run = seg_combine<Z>(run, s);
+    const uint32_t c = keys[e];
+    const uint32_t v = vals[e];
+    const uint32_t t = v >> (kb + 1);
+    const uint32_t op = (v >> kb) & 1u;
+    const uint32_t row = c / o.row_cells;
+    if (HAS_FAT) {
+      const uint32_t k = v & ((1u << kb) - 1u);
+      uint32_t init[Z];
+#pragma unroll
+      for (int q2 = 0; q2 < Z; ++q2) init[q2] = __ldg(o.fat_init + (size_t)c * Z + q2);
+      const int64_t post_own = (int64_t)init[k] + (int64_t)run.v[k];
+      const int64_t pre_own = post_own + (op ? 1 : -1);
+      if (op == 0 ? (pre_own == (int64_t)U32MAX) : (pre_own == 0)) local_fail = min(local_fail, t);
+      if (WRITE_OBS) {
+        uint32_t ob;
+        if (op == 0) {
+          ob = (uint32_t)post_own;
+        } else {
+          ob = 0;
+#pragma unroll
+          for (int q2 = 0; q2 < Z; ++q2) ob = max(ob, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+        }
+        o.obs[(size_t)t * o.D + row] = ob;
+      }
+      const bool last = (e + 1 == N) || (keys[e + 1] != c);
+      if (last) {
+#pragma unroll
+        for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
+      }
+    }
+    if (WRITE_LINKS) {
+      const uint32_t rank = e - run.head;
+      const uint32_t prev = (e > run.head) ? prev_t : NONE32;
+      o.links[(size_t)t * o.D + row] = make_uint2(rank, prev);
+    }
+    prev_t = t;
+  }
+  if (HAS_FAT && local_fail != NONE32) atomicMin(&o.ctl->fail_t, local_fail);
+}
+
+// ---------------------------------------------------------------- 4. runs
+template <int D>
+struct RunArgs {
+  const uint32_t* vals0;  // row-0 sorted vals (slim cells)
+  int kb;
+  uint32_t n;
+  const uint2* links;
+  const uint32_t* obs;     // may be null (CU)
+  KeySrc keys;
+  uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
+  uint32_t* opdata;        // [e*DW + ...]
+  int DW;
+  uint32_t* headflag;      // [t]
+  uint32_t* head_e0;       // [t]
+  Ctl* ctl;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
+  const uint32_t tstar = a.ctl->fail_t;
+  uint32_t ins = 0;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.n; e += gridDim.x * blockDim.x) {
+    const uint32_t v = a.vals0[e];
+    const uint32_t t = v >> (a.kb + 1);
+    const uint32_t op = (v >> a.kb) & 1u;
+    const bool valid = t < tstar;
+    uint2 lk[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) lk[i] = a.links[(size_t)t * D + i];
+    bool cont = valid && lk[0].y != NONE32;
+#pragma unroll
+    for (int i = 1; i < D; ++i) cont = cont && (lk[i].y == lk[0].y);
+    // same cells is not enough for the closed forms: require the same key
+    if (cont) cont = load_key(a.keys, lk[0].y) == load_key(a.keys, t);
+    a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
+    if (a.obs) {
+      if (op == 0 || a.DW < D) {
+        uint32_t b = U32MAX;
+#pragma unroll
+        for (int i = 0; i < D; ++i) b = min(b, a.obs[(size_t)t * D + i]);
+        a.opdata[(size_t)e * a.DW] = b;
+      } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i) a.opdata[(size_t)e * a.DW + i] = a.obs[(size_t)t * D + i];
+      }
+    }
+    const bool head = valid && !cont;
+    a.headflag[t] = head ? 1u : 0u;
+    a.head_e0[t] = e;
+    if (valid && op == 0) ++ins;
+  }
+  // n_ins: warp reduce then one atomic per warp
+  for (int off = 16; off > 0; off >>= 1) ins += __shfl_down_sync(0xffffffffu, ins, off);
+  if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&a.ctl->n_ins, (unsigned long long)ins);
+}
+
+__global__ void runs_build_k(const uint32_t* __restrict__ headflag, const uint32_t* __restrict__ ridx,
+                             const uint32_t* __restrict__ head_e0, const uint8_t* __restrict__ opflags, uint32_t n,
+                             uint32_t* __restrict__ run_e0, uint32_t* __restrict__ run_info,
+                             uint32_t* __restrict__ run_t, Ctl* ctl) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    if (t == n - 1) ctl->n_runs = ridx[t] + headflag[t];
+    if (!headflag[t]) continue;
+    const uint32_t r = ridx[t];
+    const uint32_t e0 = head_e0[t];
+    uint32_t hasdel = opflags[e0] & 1u;
+    uint32_t L = 1;
+    for (uint32_t e = e0 + 1; e < n; ++e) {
+      const uint8_t f = opflags[e];
+      if ((f & 6u) != 6u) break;
+      hasdel |= f & 1u;
+      ++L;
+    }
+    run_e0[r] = e0;
+    run_info[r] = L | (hasdel << 31);
+    run_t[r] = t;
+  }
+}
+
+// ---------------------------------------------------------------- 5. engine
+template <int D>
+struct EngineArgs {
+  unsigned long long* slim64;
+  uint32_t w;  // slim row width
+  Seeds<D> seeds;
+  Mod wm;
+  KeySrc keys;
+  const uint32_t* run_e0;
+  const uint32_t* run_info;
+  const uint32_t* run_t;
+  const uint2* links;
+  const uint8_t* opflags;
+  const uint32_t* opdata;
+  int DW;
+  Ctl* ctl;
+  unsigned long long* inc;  // int64[d] tallies (two's complement add)
+};
+
+// MODE 0: SF (raise gated by b_min, deletes clamp to the bucket max)
+// MODE 1: CU (raise always; saturation ruled out by the host precheck)
+template <int D, int MODE>
+__global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t R = a.ctl->n_runs;
+  bool has = false, exhausted = false;
+  uint32_t cells[D], rank[D], raised[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0;
+  uint32_t e0 = 0, info = 0;
+  uint32_t backoff = 32;
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, !has && !exhausted);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&a.ctl->ticket, (uint32_t)__popc(need));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!has && !exhausted) {
+        const uint32_t r = base + __popc(need & lanemask_lt());
+        if (r < R) {
+          e0 = a.run_e0[r];
+          info = a.run_info[r];
+          const uint32_t t = a.run_t[r];
+          const uint64_t key = load_key(a.keys, t);
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            cells[i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+            rank[i] = a.links[(size_t)t * D + i].x;
+          }
+          has = true;
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, !has)) break;  // no lane holds a run and none can get one
+    bool progressed = false;
+    if (has) {
+      unsigned long long wv[D];
+      bool ready = true;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        wv[i] = ld_relaxed_u64(a.slim64 + cells[i]);
+        ready = ready && ((uint32_t)(wv[i] >> 32) == rank[i]);
+      }
+      if (ready) {
+        uint32_t c[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) c[i] = (uint32_t)wv[i];
+        const uint32_t L = info & 0x7fffffffu;
+        const bool hasdel = info >> 31;
+        uint32_t m0 = c[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) m0 = min(m0, c[i]);
+        if (MODE == 1) {
+          // every insert raises: s = L
+          const uint64_t tgt = (uint64_t)m0 + L;
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+        } else if (!hasdel) {
+          // closed form: first k with b_k > m0, then every later op raises
+          uint32_t k = 0;
+          while (k < L && a.opdata[(size_t)(e0 + k) * a.DW] <= m0) ++k;
+          const uint32_t s = L - k;
+          if (s) {
+            const uint64_t tgt = (uint64_t)m0 + s;
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+              if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+          }
+        } else {
+          for (uint32_t k = 0; k < L; ++k) {
+            const size_t e = (size_t)e0 + k;
+            const uint8_t f = a.opflags[e];
+            if (!(f & 1u)) {
+              const uint32_t b = a.opdata[e * a.DW];
+              uint32_t m = c[0];
+#pragma unroll
+              for (int i = 1; i < D; ++i) m = min(m, c[i]);
+              if (m < b) {
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+                  if (c[i] == m) { c[i] += 1u; raised[i] += 1u; }
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < D; ++i) c[i] = min(c[i], a.opdata[e * a.DW + i]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
+        has = false;
+        progressed = true;
+        backoff = 32;
+      }
+    }
+    if (!__any_sync(0xffffffffu, progressed)) {
+      __nanosleep(backoff);
+      backoff = min(backoff * 2, 1024u);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    unsigned long long r = raised[i];
+    for (int off = 16; off > 0; off >>= 1) r += __shfl_down_sync(0xffffffffu, r, off);
+    if (lane == 0 && r) atomicAdd(a.inc + i, r);
+  }
+}
+
+__global__ void pack_slim_k(const uint32_t* __restrict__ slim, unsigned long long* __restrict__ s64, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) s64[c] = slim[c];
+}
+__global__ void unpack_slim_k(const unsigned long long* __restrict__ s64, uint32_t* __restrict__ slim, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
+    slim[c] = (uint32_t)s64[c];
+}
+
+__global__ void ctl_init_k(Ctl* ctl) {
+  ctl->fail_t = NONE32;
+  ctl->ticket = 0;
+  ctl->n_ins = 0;
+  ctl->n_runs = 0;
+}
+
+// undo the fat deltas of ops t >= t* (the fat was written for the whole
+// batch; u32 arithmetic is modular so the correction is exact)
+template <int D, int KIND>
+__global__ void fat_undo_k(HashArgs<D> a, uint32_t* __restrict__ fat, uint32_t zstride) {
+  const uint32_t tstar = a.ctl->fail_t;
+  if (tstar == NONE32) return;
+  for (int64_t t = (int64_t)tstar + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = load_key(a.keys, t);
+    const uint32_t undo = a.ops[t] ? 1u : 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      uint32_t cell = (uint32_t)i * a.row_cells + (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
+      uint32_t k = (KIND == 0) ? (uint32_t)bucket(key, a.slot_seeds.s[i], a.zm) : 0u;
+      atomicAdd(fat + (size_t)cell * zstride + k, undo);
+    }
+  }
+}
+
+// result = {status, op_index, n_ins}; CM tallies (+n_ins per row)
+__global__ void finalize_k(const Ctl* ctl, const uint8_t* __restrict__ ops, int variant_kind, int64_t* result,
+                           unsigned long long* inc, int d, int cm_tallies) {
+  const uint32_t ts = ctl->fail_t;
+  int64_t status = SFK_OK;
+  if (ts != NONE32) {
+    const int op = ops[ts];
+    // variant_kind: 0 SF1 / CU (delete unsupported), 1 SFF / CM (delete phantom)
+    status = op == 0 ? SFK_SATURATED : (variant_kind == 0 ? SFK_UNSUPPORTED : SFK_PHANTOM);
+  }
+  result[0] = status;
+  result[1] = ts == NONE32 ? -1 : (int64_t)ts;
+  result[2] = (int64_t)ctl->n_ins;
+  if (cm_tallies)
+    for (int i = 0; i < d; ++i) inc[i] += ctl->n_ins;
+}
+
+// inserts applied before the first failing op (CM exact path)
+__global__ void count_ins_k(const uint8_t* __restrict__ ops, int64_t n, Ctl* ctl) {
+  const uint32_t ts = ctl->fail_t;
+  const int64_t lim = ts == NONE32 ? n : (int64_t)ts;
+  unsigned long long ins = 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < lim; t += (int64_t)gridDim.x * blockDim.x)
+    ins += ops[t] == 0;
+  for (int off = 16; off > 0; off >>= 1) ins += __shfl_down_sync(0xffffffffu, ins, off);
+  if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&ctl->n_ins, ins);
+}
+
+// ---------------------------------------------------------------- CM fast path
+// warp-aggregated atomics: lanes hitting the same cell merge their net delta
+// (__match_any_sync) and the group leader issues one atomicAdd.
+template <int D>
+__global__ void __launch_bounds__(256) cm_atomic_k(uint32_t* __restrict__ counters, Seeds<D> seeds, Mod wm, uint32_t w,
+                                                   const uint8_t* __restrict__ ops, KeySrc keys, int64_t n,
+                                                   const Ctl* ctl) {
+  const int64_t limit = ctl ? (ctl->fail_t == NONE32 ? n : (int64_t)ctl->fail_t) : n;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp_id * 32; base < limit; base += nwarps * 32) {
+    const int64_t t = base + lane;
+    const bool active = t < limit;
+    const unsigned amask = __ballot_sync(0xffffffffu, active);
+    if (!active) continue;
+    const uint64_t key = load_key(keys, t);
+    const uint32_t op = ops[t];
+    const unsigned del = __ballot_sync(amask, op != 0);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint32_t cell = (uint32_t)i * w + (uint32_t)bucket(key, seeds.s[i], wm);
+      const unsigned g = __match_any_sync(amask, cell);
+      if (lane == __ffs(g) - 1) {
+        const int net = __popc(g & ~del) - __popc(g & del);
+        if (net) atomicAdd(counters + cell, (uint32_t)net);
+      }
+    }
+  }
+}
+
+
+__global__ void stats_ops_k(const uint8_t* __restrict__ ops, int64_t n, Stats* st) {
+  unsigned long long ins = 0, del = 0, fd = 0xFFFFFFFFFFFFFFFFull;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (ops[t]) { ++del; if ((unsigned long long)t < fd) fd = t; }
+    else ++ins;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    ins += __shfl_down_sync(0xffffffffu, ins, off);
+    del += __shfl_down_sync(0xffffffffu, del, off);
+    fd = min(fd, __shfl_down_sync(0xffffffffu, fd, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ins) atomicAdd(&st->n_ins, ins);
+    if (del) atomicAdd(&st->n_del, del);
+    if (fd != 0xFFFFFFFFFFFFFFFFull) atomicMin(&st->first_del, fd);
+  }
+}
+__global__ void stats_ins_before_k(const uint8_t* __restrict__ ops, Stats* st) {
+  const unsigned long long lim = st->first_del;
+  unsigned long long ins = 0;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < lim;
+       t += (unsigned long long)gridDim.x * blockDim.x)
+    ins += ops[t] == 0;
+  for (int off = 16; off > 0; off >>= 1) ins += __shfl_down_sync(0xffffffffu, ins, off);
+  if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&st->ins_before_first_del, ins);
+}
+__global__ void stats_counters_k(const uint32_t* __restrict__ c, int64_t cells, Stats* st) {
+  uint32_t mx = 0, mn = U32MAX;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cells; k += (int64_t)gridDim.x * blockDim.x) {
+    mx = max(mx, c[k]);
+    mn = min(mn, c[k]);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
+    mn = min(mn, __shfl_down_sync(0xffffffffu, mn, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->cmax, mx);
+    atomicMin(&st->cmin, mn);
+  }
+}
+
+// ================================================================ host side
+struct Plan {
+  // sizes
+  uint32_t n, N;  // ops, pairs (D*n)
+  int D, kb;
+  size_t cub_sort_bytes, cub_scan_bytes;
+  uint32_t ntiles;
+};
+
+static size_t sort_temp_bytes(uint32_t N) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)N, 0, 32);
+  return bytes;
+}
+static size_t scan_temp_bytes(uint32_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+  return bytes;
+}
+
+static int bits_for(uint64_t v) {  // bits needed to represent values < v
+  int b = 0;
+  while (b < 64 && (1ull << b) < v) ++b;
+  return b;
+}
+
+// Workspace layout shared by every parallel apply. Sizes are upper bounds
+// for the given (kind, dims, n); a null base only measures.
+struct Layout {
+  uint32_t *k_in, *v_in, *k_out, *v_out;
+  void* cub_tmp;
+  size_t cub_tmp_bytes;
+  void* tiles;        // SegState<Z> per tile
+  uint32_t* fat_snap;
+  uint32_t* obs;
+  uint2* links;
+  uint8_t* opflags;
+  uint32_t* opdata;
+  uint32_t* headflag;
+  uint32_t* head_e0;
+  uint32_t* ridx;
+  uint32_t *run_e0, *run_info, *run_t;
+  unsigned long long* slim64;
+  Ctl* ctl;
+  Stats* stats;
+  size_t total;
+  bool ok;
+};
+
+// kind: 0 SFF (bucketed), 1 SF1 (flat), 2 CU, 3 CM exact
+static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
+  Carver cv(base, cap);
+  Layout L{};
+  const uint64_t N = (uint64_t)d * (uint64_t)n;
+  L.ctl = cv.take<Ctl>(1);
+  L.stats = cv.take<Stats>(1);
+  L.k_in = cv.take<uint32_t>(N);
+  L.v_in = cv.take<uint32_t>(N);
+  L.k_out = cv.take<uint32_t>(N);
+  L.v_out = cv.take<uint32_t>(N);
+  L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n));
+  L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
+  const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
+  uint64_t fat_cells = 0;
+  if (kind == 0) fat_cells = (uint64_t)d * w * z;
+  if (kind == 1) fat_cells = (uint64_t)d * wp;
+  if (kind == 3) fat_cells = (uint64_t)d * w;
+  L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
+  const bool need_obs = kind == 0 || kind == 1;
+  L.obs = cv.take<uint32_t>(need_obs ? N : 1);
+  const bool engine = kind != 3;
+  L.links = cv.take<uint2>(engine ? N : 1);
+  L.opflags = cv.take<uint8_t>(engine ? n : 1);
+  const int DW = kind == 0 ? d : 1;
+  L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n * DW : 1);
+  L.headflag = cv.take<uint32_t>(engine ? n : 1);
+  L.head_e0 = cv.take<uint32_t>(engine ? n : 1);
+  L.ridx = cv.take<uint32_t>(engine ? n : 1);
+  L.run_e0 = cv.take<uint32_t>(engine ? n : 1);
+  L.run_info = cv.take<uint32_t>(engine ? n : 1);
+  L.run_t = cv.take<uint32_t>(engine ? n : 1);
+  L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
+  L.total = cv.off + 256;
+  L.ok = cv.ok;
+  return L;
+}
+
+size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
+  if (n <= 0) return 256;
+  Layout L = carve(nullptr, ~size_t(0), kind, d, w, wp, z, n);
+  return L.total;
+}
+
+template <int Z, bool HAS_FAT, bool OBS, bool LINKS>
+static int run_scan(const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
+                    cudaStream_t st) {
+  const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  SegState<Z>* ta = static_cast<SegState<Z>*>(tiles);
+  segscan_reduce_k<Z, HAS_FAT><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta);
+  segscan_tiles_k<Z><<<1, 1024, 0, st>>>(ta, ntiles);
+  segscan_apply_k<Z, HAS_FAT, OBS, LINKS><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta, so);
+  return check_launch("segscan");
+}
+
+template <bool HAS_FAT, bool OBS, bool LINKS>
+static int run_scan_z(int z, const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
+                      cudaStream_t st) {
+  switch (z) {
+    case 1: return run_scan<1, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 2: return run_scan<2, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 3: return run_scan<3, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 4: return run_scan<4, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 5: return run_scan<5, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 6: return run_scan<6, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 7: return run_scan<7, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+    case 8: return run_scan<8, HAS_FAT, OBS, LINKS>(keys, vals, N, kb, tiles, so, st);
+  }
+  set_error("segscan: unsupported z=%d", z);
+  return 1;
+}
+
+static int sort_pairs(Layout& L, uint32_t N, int end_bit, cudaStream_t st) {
+  size_t bytes = L.cub_tmp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N, 0,
+                                                  std::max(end_bit, 1), st);
+  if (e != cudaSuccess) {
+    set_error("radix sort: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+template <int D>
+static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uint64_t* cell_seeds,
+                             const uint64_t* slot_seeds, uint64_t row_cells, int z, int kb, Layout& L,
+                             int unsupported_deletes) {
+  HashArgs<D> h;
+  h.keys = ks;
+  h.ops = ops;
+  h.n = n;
+  for (int i = 0; i < D; ++i) {
+    h.cell_seeds.s[i] = cell_seeds[i];
+    h.slot_seeds.s[i] = slot_seeds ? slot_seeds[i] : 0;
+  }
+  h.cm = make_mod(row_cells);
+  h.zm = make_mod((uint64_t)std::max(z, 1));
+  h.row_cells = (uint32_t)row_cells;
+  h.kb = kb;
+  h.key_out = L.k_in;
+  h.val_out = L.v_in;
+  h.unsupported_deletes = unsupported_deletes;
+  h.ctl = L.ctl;
+  return h;
+}
+
+// The run/engine tail shared by SFF, SF1 and CU once the row-0 sorted slim
+// pairs (k_out/v_out) and links (+ obs) exist.
+template <int D, int MODE>
+static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int64_t w, KeySrc ks, uint32_t n, int kb,
+                      bool with_obs, int DW, int64_t* inc, cudaStream_t st) {
+  const int sms = sm_count();
+  RunArgs<D> ra;
+  ra.vals0 = L.v_out;
+  ra.kb = kb;
+  ra.n = n;
+  ra.links = L.links;
+  ra.obs = with_obs ? L.obs : nullptr;
+  ra.keys = ks;
+  ra.opflags = L.opflags;
+  ra.opdata = L.opdata;
+  ra.DW = DW;
+  ra.headflag = L.headflag;
+  ra.head_e0 = L.head_e0;
+  ra.ctl = L.ctl;
+  runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra);
+  size_t bytes = L.cub_tmp_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.headflag, L.ridx, (int)n, st);
+  if (e != cudaSuccess) {
+    set_error("run scan: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  runs_build_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.headflag, L.ridx, L.head_e0, L.opflags, n, L.run_e0,
+                                                          L.run_info, L.run_t, L.ctl);
+  const uint32_t cells = (uint32_t)(D * w);
+  pack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(slim, L.slim64, cells);
+  EngineArgs<D> ea;
+  ea.slim64 = L.slim64;
+  ea.w = (uint32_t)w;
+  for (int i = 0; i < D; ++i) ea.seeds.s[i] = slim_seeds[i];
+  ea.wm = make_mod((uint64_t)w);
+  ea.keys = ks;
+  ea.run_e0 = L.run_e0;
+  ea.run_info = L.run_info;
+  ea.run_t = L.run_t;
+  ea.links = L.links;
+  ea.opflags = L.opflags;
+  ea.opdata = L.opdata;
+  ea.DW = DW;
+  ea.ctl = L.ctl;
+  ea.inc = reinterpret_cast<unsigned long long*>(inc);
+  // persistent: every warp resident (the deadlock-freedom argument needs the
+  // ticket holders to be running, which any launch satisfies; residency
+  // just keeps the window of in-flight runs wide)
+  static int occ = -1;
+  if (occ < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slim_engine_k<D, MODE>, 256, 0);
+    if (occ < 1) occ = 1;
+  }
+  slim_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea);
+  unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells);
+  return check_launch("slim_engine");
+}
+
+template <int D>
+static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
+                         int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n64, int64_t* inc,
+                         int64_t* result, Layout& L, cudaStream_t st) {
+  const int sms = sm_count();
+  const uint32_t n = (uint32_t)n64;
+  const uint32_t N = (uint32_t)(D * n64);
+  ctl_init_k<<<1, 1, 0, st>>>(L.ctl);
+  if (kind == 0) {  // ------------------------------------------------ SFF
+    const int kb = bits_for((uint64_t)z);
+    HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, fat_seeds, (uint64_t)w, z, kb, L, 0);
+    hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h);
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    const size_t fat_bytes = (size_t)D * w * z * 4;
+    cudaMemcpyAsync(L.fat_snap, fat, fat_bytes, cudaMemcpyDeviceToDevice, st);
+    ScanOut so{L.fat_snap, fat, L.obs, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, true, true>(z, L.k_out, L.v_out, N, kb, L.tiles, so, st)) return r;
+    fat_undo_k<D, 0><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, fat, (uint32_t)z);
+    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, kb, true, D, inc, st)) return r;
+    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0);
+  } else if (kind == 1) {  // ------------------------------------------ SF1
+    HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
+    hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf);
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
+    cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
+    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
+    if (int r = run_scan_z<true, true, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u);
+    HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
+    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs);
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    ScanOut ss{nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<false, false, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, true, 1, inc, st)) return r;
+    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0);
+  } else if (kind == 2) {  // ------------------------------------------ CU
+    HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
+    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs);
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    ScanOut ss{nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<false, false, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, false, 1, inc, st)) return r;
+    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0);
+  } else {  // ------------------------------------------------------- CM exact
+    HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
+    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h);
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    cudaMemcpyAsync(L.fat_snap, slim, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
+    ScanOut so{L.fat_snap, slim, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, false, false>(1, L.k_out, L.v_out, N, 0, L.tiles, so, st)) return r;
+    fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, slim, 1u);
+    count_ins_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ops, n64, L.ctl);
+    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, reinterpret_cast<unsigned long long*>(inc), D, 1);
+  }
+  return check_launch("sf_parallel");
+}
+
+int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds, int d,
+                   int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
+                   int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Layout L = carve(ws, ws_bytes, kind, d, w, wp, z, n);
+  if (!L.ok || ws == nullptr) {
+    set_error("workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
+    return 1;
+  }
+  switch (d) {
+    case 1: return sf_parallel_d<1>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 2: return sf_parallel_d<2>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 3: return sf_parallel_d<3>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 4: return sf_parallel_d<4>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 5: return sf_parallel_d<5>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 6: return sf_parallel_d<6>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 7: return sf_parallel_d<7>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 8: return sf_parallel_d<8>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+  }
+  set_error("parallel engine: unsupported d=%d", d);
+  return 1;
+}
+
+// CM/CU precheck statistics (host reads them back: one small sync)
+int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64_t cells, void* ws, size_t ws_bytes,
+                  Stats* host, cudaStream_t st) {
+  Carver cv(ws, ws_bytes);
+  cv.take<Ctl>(1);
+  Stats* s = cv.take<Stats>(1);
+  Stats init{};
+  init.first_del = (unsigned long long)n;
+  init.cmax = 0;
+  init.cmin = U32MAX;
+  cudaMemcpyAsync(s, &init, sizeof(Stats), cudaMemcpyHostToDevice, st);
+  const int sms = sm_count();
+  if (n > 0) stats_ops_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, n, s);
+  if (n > 0) stats_ins_before_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, s);
+  stats_counters_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(counters, cells, s);
+  cudaMemcpyAsync(host, s, sizeof(Stats), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    set_error("stats: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+template <int D>
+static int cm_fast_d(uint32_t* counters, const uint64_t* seeds, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
+                     cudaStream_t st) {
+  Seeds<D> sd;
+  for (int i = 0; i < D; ++i) sd.s[i] = seeds[i];
+  const int sms = sm_count();
+  cm_atomic_k<D><<<grid_for((n + 31) / 32 * 32, 256, sms * 16), 256, 0, st>>>(counters, sd, make_mod((uint64_t)w),
+                                                                              (uint32_t)w, ops, ks, n, nullptr);
+  return check_launch("cm_atomic");
+}
+
+int cm_fast(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
+            cudaStream_t st) {
+  switch (d) {
+    case 1: return cm_fast_d<1>(counters, seeds, w, ops, ks, n, st);
+    case 2: return cm_fast_d<2>(counters, seeds, w, ops, ks, n, st);
+    case 3: return cm_fast_d<3>(counters, seeds, w, ops, ks, n, st);
+    case 4: return cm_fast_d<4>(counters, seeds, w, ops, ks, n, st);
+    case 5: return cm_fast_d<5>(counters, seeds, w, ops, ks, n, st);
+    case 6: return cm_fast_d<6>(counters, seeds, w, ops, ks, n, st);
+    case 7: return cm_fast_d<7>(counters, seeds, w, ops, ks, n, st);
+    case 8: return cm_fast_d<8>(counters, seeds, w, ops, ks, n, st);
+  }
+  set_error("cm fast path: unsupported d=%d", d);
+  return 1;
+}
+
+}  // namespace sfk

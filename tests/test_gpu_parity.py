@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (parallel engine and the exact sequential device
+engine) against the reference's golden fixtures and against the CPU oracle on
+the BASELINE configurations. Bit-exact on every counter, tally and estimate."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import fixture_names, load_fixture, load_hashing
+from gpu_util import apply_batches, assert_state_equal, counters_of, host, make_sketch, set_state
+
+pytestmark = pytest.mark.gpu
+
+import paper_1701_04148_b200 as P  # noqa: E402
+from paper_1701_04148_b200 import device as D  # noqa: E402
+from paper_1701_04148_b200 import workloads as W  # noqa: E402
+
+
+def test_device_hash_goldens():
+    h = load_hashing()
+    ins = np.array([int(x) for x in h["mix_batch_in"]], dtype=np.uint64)
+    got = host(D.mix_batch(ins))
+    assert [str(int(v)) for v in got] == h["mix_batch_out"]
+    fin = np.array([int(k) for k in h["finalize"]], dtype=np.uint64)
+    assert [int(v) for v in host(D.mix_batch(fin))] == [int(v) for v in h["finalize"].values()]
+    for s, want in h["key_from_string"].items():
+        b = s.encode("utf-8")
+        if not b:
+            continue
+        rec = np.frombuffer(b, dtype=np.uint8).reshape(1, -1)
+        assert int(host(D.load_keys(rec))[0]) == int(want)
+
+
+@pytest.mark.parametrize("sequential", [False, True])
+@pytest.mark.parametrize("name", fixture_names())
+def test_fixture_parity(name, sequential):
+    fx = load_fixture(name)
+    kind = str(fx["kind"])
+    sk = make_sketch(kind, int(fx["d"]), int(fx["w"]), int(fx["z"]), int(fx["w_prime"]), int(fx["master_seed"]))
+    set_state(sk, fx)
+    status, idx = apply_batches(sk, fx["ops"], fx["keys"], int(fx["batches"]), sequential)
+    assert (status, idx) == (int(fx["status"]), int(fx["op_index"]))
+    assert_state_equal(sk, fx["slim"], fx["inc"], fx["seen"], fx.get("fat"), fx.get("dsub"))
+    np.testing.assert_array_equal(host(sk.query_many(fx["query_keys"])), fx["query"])
+    assert P.export_slim(sk) == fx["export"].tobytes()
+
+
+def oracle_run(oracle, kind, d, w, z, wp, seed, ops, keys_u64):
+    o = oracle.OracleSketch(kind, d, w, z, wp, seed)
+    r = o.apply_ops(ops, keys_u64)
+    return o, r
+
+
+def compare_cfg(oracle, kind, d, w, z, wp, seed, ops, keys, keys_u64, qkeys, qkeys_u64=None):
+    o, (st, oi, _) = oracle_run(oracle, kind, d, w, z, wp, seed, ops, keys_u64)
+    sk = make_sketch(kind, d, w, z, wp, seed)
+    dev_ops = torch.from_numpy(ops).cuda()
+    dev_keys = torch.from_numpy(keys).cuda() if isinstance(keys, np.ndarray) else keys
+    status, idx = apply_batches(sk, dev_ops, dev_keys)
+    assert (status, idx) == (st, oi)
+    assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat, o.dsub)
+    if qkeys_u64 is None:
+        qkeys_u64 = np.asarray(qkeys).astype(np.uint64)
+    np.testing.assert_array_equal(host(sk.query_many(qkeys)), o.query_many(qkeys_u64))
+    return sk
+
+
+def test_cfg1_sf1_full(oracle):
+    c = W.cfg1(seed=2017)
+    compare_cfg(oracle, "sf1", 4, 16384, 4, 65536, 2017, c["ops"], c["keys"], c["keys"].astype(np.uint64),
+                c["distinct"])
+
+
+@pytest.mark.parametrize("kind", ["cm", "cu"])
+def test_cfg2_full(oracle, kind):
+    c = W.cfg2(seed=2017)
+    compare_cfg(oracle, kind, 4, 65536, 1, None, 2017, c["ops"], c["keys"], c["keys"].astype(np.uint64),
+                c["distinct"][:200000])
+
+
+@pytest.mark.parametrize("alpha", [0.5, 1.0, 1.5])
+def test_cfg3_sff_full(oracle, alpha):
+    c = W.cfg3(seed=2017, alpha=alpha)
+    sk = compare_cfg(oracle, "sff", 4, 65536, 4, None, 2017, c["ops"], c["keys"], c["keys"].astype(np.uint64),
+                     c["distinct"])
+    sk.check_invariants()
+
+
+def test_cfg4_sf1_records(oracle):
+    c = W.cfg4(seed=2017, n=20_000_000, v=2_000_000)
+    keys_u64 = oracle.keys_from_records(c["records"])
+    q = c["distinct"][:100000]
+    compare_cfg(oracle, "sf1", 4, 12800, 1, 4194304, 2017, c["ops"], c["records"], keys_u64, q,
+                oracle.keys_from_records(q))
+
+
+def test_chunked_batches_equal_one_batch(oracle):
+    c = W.cfg3(seed=7, n_ins=400_000, v=20_000, alpha=1.2)
+    o, _ = oracle_run(oracle, "sff", 4, 4096, 4, None, 7, c["ops"], c["keys"].astype(np.uint64))
+    sk = make_sketch("sff", 4, 4096, 4, None, 7)
+    apply_batches(sk, c["ops"], c["keys"], batches=7)
+    assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+
+
+@pytest.mark.parametrize("kind", ["sff", "sf1", "cm", "cu"])
+def test_prefix_semantics_at_scale(oracle, kind):
+    """A failing op deep inside a large batch: the prefix is applied, the
+    failing op leaves no trace (_kernels.py:4-8)."""
+    c = W.cfg3(seed=3, n_ins=200_000, v=5000, alpha=1.0)
+    ops, keys = c["ops"].copy(), c["keys"].copy()
+    if kind in ("sf1", "cu"):
+        ops = np.zeros_like(ops)
+        ops[150_000] = 1  # unsupported delete
+    else:
+        keys[150_000] = np.uint32(0xDEADBEEF)  # never inserted
+        ops[150_000] = 1  # phantom
+    compare_cfg(oracle, kind, 4, 1024, 4, None, 3, ops, keys, keys.astype(np.uint64), c["distinct"])
+
+
+def test_saturation_prefix_at_scale(oracle):
+    c = W.cfg1(seed=4, n=100_000, v=300)
+    for kind, z in (("sff", 4), ("sf1", 4)):
+        o = oracle.OracleSketch(kind, 4, 64, z, None, 4)
+        o.fat[...] = np.uint32(0xFFFFFFFF - 2000)
+        st = o.apply_ops(c["ops"], c["keys"].astype(np.uint64))
+        assert st[0] == 2
+        sk = make_sketch(kind, 4, 64, z, None, 4)
+        sk.fat.counters.fill_(0xFFFFFFFF - 2000)
+        status, idx = apply_batches(sk, c["ops"], c["keys"])
+        assert (status, idx) == st[:2]
+        assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
