@@ -1,0 +1,374 @@
+"""Headline benchmark: SF insert & query throughput on B200 (BASELINE.json).
+
+One step = the SF sketch hot path over one synthetic batch:
+  1. build: a fresh SFF sketch (d=4, w=65536, z=4) applies the cfg-3 stream
+     (10M inserts Zipf(1.0) over 1M distinct uint32 keys + 2M occurrence-level
+     deletes, 12M ops) through ``SfSketch.apply_ops`` on rank 0 (SF updates
+     are order-dependent: single GPU);
+  2. replicate: with N > 1 the slim is broadcast from rank 0 (NCCL/NVLink);
+  3. query: the cfg-5 batch of Q point queries (default 1B uint32 keys, half
+     present with Zipf(1.0) rank skew, half absent) sharded contiguously over
+     the N GPUs, each answering its slice with the fused hash+gather+min kernel.
+value = (ops applied + queries answered) / step time (max over ranks),
+Mitems/s. Inputs are device-resident for ``value``; ``e2e`` repeats the step
+through the same public API from pinned HOST buffers (H2D of ops/keys and
+query keys, D2H of the estimates inside the timed region).
+
+``--impl reference`` times the CPU oracle (a C port of the reference's numba
+kernels, tests pin it bit-exact to the reference) on the host cores for the
+same workload: the build single-threaded (single-writer contract), the
+queries on all host threads, extrapolated from a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SF insert & query Mitems/s"
+SEED = 2017
+D, W, Z = 4, 65536, 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--queries", type=int, default=1_000_000_000)
+    ap.add_argument("--alpha", type=float, default=1.0, help="build stream skew (cfg 3)")
+    ap.add_argument("--alpha-q", type=float, default=1.0, help="query rank skew (cfg 5)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(args, world):
+    return {
+        "workload": "cfg3 SFF build (10M inserts Zipf(%.1f)/1M + 2M interleaved deletes) + cfg5 %d point queries "
+                    "(50%% present Zipf(%.1f), 50%% absent) on the built slim" % (args.alpha, args.queries, args.alpha_q),
+        "d": D, "w": W, "z": Z, "ops": 12_000_000, "queries": args.queries,
+        "parallelism": "build on rank 0 (order-dependent), slim broadcast, queries sharded over %d GPU(s)" % world,
+        "l2": "query keys (4 B x Q) exceed L2; L2 flushed (256 MiB write) between steps",
+        "seed": SEED,
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(p):
+        with open(p) as fh:
+            hbm, src = float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    gather = None
+    gp = os.path.join(ROOT, "profiles", "gather_peaks.json")
+    if os.path.exists(gp):
+        with open(gp) as fh:
+            gather = json.load(fh)
+    return hbm, src, gather
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_measure(args, stream, present_sample_keys, threads):
+    """Oracle (C port of the reference kernels): build single-threaded over the
+    full 12M-op stream, queries with `threads` threads over a sample."""
+    from oracle import oracle as orc
+
+    orc.lib()
+    o = orc.OracleSketch("sff", D, W, Z, None, SEED)
+    keys64 = stream["keys"].astype(np.uint64)
+    t0 = time.perf_counter()
+    st = o.apply_ops(stream["ops"], keys64)
+    t_build = time.perf_counter() - t0
+    assert st[0] == 0
+    qs = present_sample_keys
+    t0 = time.perf_counter()
+    o.query_many(qs, threads=threads)
+    t_q = time.perf_counter() - t0
+    n_ops = stream["ops"].shape[0]
+    t_total = t_build + t_q * (args.queries / qs.shape[0])
+    value = (n_ops + args.queries) / t_total / 1e6
+    sample = (f"full 12M-op cfg-3 build on 1 thread ({t_build:.2f} s) + {qs.shape[0]:,} cfg-5 queries on "
+              f"{threads} threads ({t_q:.2f} s), query time extrapolated to {args.queries:,}")
+    return value, t_build, t_q, sample, o
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1701_04148_b200 import workloads as Wl
+
+    stream = Wl.cfg3(seed=SEED, alpha=args.alpha)
+    sample_n = 50_000_000
+    qs = Wl.query_keys(SEED + 5, stream["distinct"], args.alpha_q, 0, sample_n)
+    from oracle import oracle as orc
+
+    threads = orc.max_threads()
+    times = []
+    for k in range(args.warmup + args.steps):
+        value, tb, tq, sample, _ = cpu_measure(args, stream, qs, threads)
+        if k >= args.warmup:
+            times.append((value, tb, tq))
+    value = statistics.median([t[0] for t in times])
+    n_items = 12_000_000 + args.queries
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mitems/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(n_items / (value * 1e6) * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mitems/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mitems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1701_04148_b200 as P
+    from paper_1701_04148_b200 import _lib, workloads as Wl
+    from paper_1701_04148_b200.sf import query_min, query_min_host
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+
+    stream = Wl.cfg3(seed=SEED, alpha=args.alpha)
+    n_ops = int(stream["ops"].shape[0])
+    ops_d = torch.from_numpy(stream["ops"]).to(dev)
+    keys_d = torch.from_numpy(stream["keys"]).to(dev)
+    per = args.queries // world
+    q0 = rank * per
+    qn = per if rank < world - 1 else args.queries - q0
+    gen = Wl.DeviceQueryStream(SEED + 5, stream["distinct"], args.alpha_q)
+    qkeys = gen.keys(q0, qn)
+    qout = torch.empty(qn, dtype=torch.int64, device=dev)
+    params = P.SketchParams(d=D, w=W, z=Z, master_seed=SEED)
+    sk = P.SfSketch(params, "sff")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def reset():
+        sk.slim.counters.zero_()
+        sk.fat.counters.zero_()
+        sk.slim.increment_counts.zero_()
+        sk.slim.insertions_seen = 0
+        sk._used_normal = False
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def step():
+        ev[0].record()
+        if rank == 0:
+            reset()
+            sk.apply_ops(ops_d, keys_d)
+        ev[1].record()
+        if world > 1:
+            sk.broadcast_slim_(src=0)
+        ev[2].record()
+        rc = L.sfk_min_query(sk.slim.counters.data_ptr(), sk._slim_seeds.ctypes.data, D, W, qkeys.data_ptr(),
+                             _lib.KEY_U32, 0, qn, qout.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "sfk_min_query")
+        ev[3].record()
+        torch.cuda.synchronize()
+        return [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+
+    for _ in range(args.warmup):
+        step()
+        flush.fill_(1)
+    # correctness gate for the measured state (rank 0 vs its own last build)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = L.sfk_launch_count()
+    phases = []
+    for _ in range(args.steps):
+        phases.append(step())
+        flush.fill_(1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = L.sfk_launch_count() - launches0
+    clk = clocks.stop()
+    tot = np.array(phases).sum(axis=0)  # build, bcast, query (ms over K steps)
+    step_ms_local = float(tot.sum()) / args.steps
+    t = torch.tensor([step_ms_local, tot[0] / args.steps, tot[1] / args.steps, tot[2] / args.steps],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, build_ms, bcast_ms, query_ms = (float(x) for x in t.tolist())
+    items = n_ops + args.queries
+    value = items / (step_ms * 1e-3) / 1e6
+
+    hbm, hbm_src, gather = measured_peaks()
+    # dominant kernel: the query kernel on this rank (CUDA events on its stream)
+    q_s = float(tot[2]) / args.steps * 1e-3
+    achieved_gbs = qn * 12 / q_s / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved_gbs / hbm, 4), "traffic": None,
+                "kernel": "min_query (fused key load + 4x hash + 4 gathers + min + int64 store)",
+                "algorithmic_bytes_per_query": 12, "peak_source": hbm_src}
+    if gather:
+        gpk = float(gather.get("gather_1MiB_Gps", 0.0))
+        gachieved = qn * 4 / q_s / 1e9
+        roofline["gather"] = {"achieved_Gps": round(gachieved, 1), "peak_Gps": gpk,
+                              "frac": round(gachieved / gpk, 4) if gpk else None,
+                              "peak_source": "profiles/gather_peaks.json (random 4-B loads, 1 MiB table, L2)"}
+
+    breakdown = {"build_ms": round(build_ms, 3), "bcast_ms": round(bcast_ms, 3), "query_ms": round(query_ms, 3),
+                 "insert_Mitems_s": round(n_ops / (build_ms * 1e-3) / 1e6, 2) if build_ms else None,
+                 "query_Mitems_s": round(args.queries / (query_ms * 1e-3) / 1e6, 2) if query_ms else None}
+
+    # ------------------------------------------------ e2e through the API from host buffers
+    e2e = None
+    if not args.no_e2e:
+        ops_h = torch.from_numpy(stream["ops"]).pin_memory()
+        keys_h = torch.from_numpy(stream["keys"]).pin_memory()
+        qk_h = torch.empty(qn, dtype=torch.uint32).pin_memory()
+        qk_h.copy_(qkeys)
+        qo_h = torch.empty(qn, dtype=torch.int64).pin_memory()
+        e_times = []
+        for k in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if rank == 0:
+                reset()
+                sk.apply_ops(ops_h, keys_h)  # H2D inside the API call
+            if world > 1:
+                sk.broadcast_slim_(src=0)
+            query_min_host(sk.slim.counters, sk._slim_seeds, qk_h, qo_h)
+            torch.cuda.synchronize()
+            e = time.perf_counter() - t0
+            if k >= args.warmup:
+                e_times.append(e)
+            flush.fill_(1)
+        et = torch.tensor([sum(e_times) / len(e_times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(items / float(et.item()) / 1e6, 3), "unit": "Mitems/s",
+               "h2d_bytes_per_step": int(n_ops * 5 + args.queries * 4) if rank == 0 else int(qn * 4),
+               "d2h_bytes_per_step": int(args.queries * 8 + 24),
+               "note": "apply_ops from pinned host ops/keys; queries through query_min_host (3-stream "
+                       "H2D/kernel/D2H pipeline); wall clock, max over ranks"}
+        # the estimates must equal the device-resident run's
+        assert torch.equal(qo_h.to(dev), qout), "e2e estimates differ from device-resident run"
+
+    # ------------------------------------------------ parity gate + CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0:
+        from oracle import oracle as orc
+
+        sample_n = 20_000_000
+        qs = qkeys[:sample_n].cpu().numpy()
+        threads = orc.max_threads()
+        if not args.no_cpu_baseline and world == 1:
+            v, tb, tq, sample, o = cpu_measure(args, stream, qs, threads)
+            cpu = {"value": round(v, 3), "unit": "Mitems/s", "cores": threads, "kind": "port", "sample": sample,
+                   "build_s": round(tb, 3)}
+            ok = (np.array_equal(sk.slim.counters.cpu().numpy(), o.slim)
+                  and np.array_equal(sk.fat.counters.cpu().numpy(), o.fat)
+                  and np.array_equal(qout[:sample_n].cpu().numpy(), o.query_many(qs, threads=threads)))
+            assert ok, "GPU state differs from the oracle"
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mitems/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": workload_config(args, world), "breakdown": breakdown, "roofline": roofline,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "gpu_launches_note": "own kernels only (sfk_launch_count); CUB radix-sort/scan launches not counted",
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,6 +68,18 @@ extern "C" {
 int sfk_abi_version(void);
 const char* sfk_last_error(void);
 
+/* Diagnostics: number of kernels this library has launched in the process
+ * (its own kernels; CUB's internal radix-sort/scan launches excluded). */
+unsigned long long sfk_launch_count(void);
+
+/* Workload utility (no reference counterpart; SURVEY.md §8(d) cfg 5): keys
+ * t0 .. t0+n-1 of the counter-based query stream of
+ * paper_1701_04148_b200.workloads.query_keys, generated on the device.
+ * present: uint32[v] keys in draw order; sorted_present: the same sorted;
+ * cdf: float64[v] Zipf CDF or NULL for uniform ranks. */
+int sfk_gen_query_keys(uint64_t seed, const uint32_t* present, const uint32_t* sorted_present, uint32_t v,
+                       const double* cdf, int64_t t0, int64_t n, uint32_t* out, void* stream);
+
 /* Replaces _kernels.mix_batch (_kernels.py:56-59): out[t] = finalize64(keys[t]). */
 int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream);
 

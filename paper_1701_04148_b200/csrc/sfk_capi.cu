@@ -12,6 +12,9 @@
 namespace sfk {
 
 static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void note_launch() { __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -45,6 +48,8 @@ int sm_count() {
 int launch_min_query(const uint32_t*, const uint64_t*, int, int64_t, KeySrc, int64_t, int64_t*, cudaStream_t);
 int launch_mix_batch(const uint64_t*, int64_t, uint64_t*, cudaStream_t);
 int launch_load_keys(KeySrc, int64_t, uint64_t*, cudaStream_t);
+int launch_gen_query_keys(uint64_t, const uint32_t*, const uint32_t*, uint32_t, const double*, int64_t, int64_t,
+                          uint32_t*, cudaStream_t);
 int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* s_seeds,
                      const uint64_t* f_seeds, int d, int64_t w, int64_t wp, int64_t z, const uint8_t* ops, KeySrc ks,
                      const int64_t* true_counts, int64_t n, int64_t* inc, int64_t* result, cudaStream_t st);
@@ -97,7 +102,7 @@ static int check_common(int d, int64_t w, int key_kind, int rec_len) {
 template <typename F>
 static int chunked(int64_t n, int64_t chunk, int64_t* result, cudaStream_t st, F body) {
   if (n <= 0) {
-    set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, 0, nullptr, 0, 0);
+    { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, 0, nullptr, 0, 0); }
     return check_launch("set_result");
   }
   if (n <= chunk) return body((int64_t)0, n);
@@ -111,11 +116,11 @@ static int chunked(int64_t n, int64_t chunk, int64_t* result, cudaStream_t st, F
     if (e != cudaSuccess) { set_error("chunk sync: %s", cudaGetErrorString(e)); return (int)e; }
     total_ins += h[2];
     if (h[0] != SFK_OK) {
-      set_result_k<<<1, 1, 0, st>>>(result, h[0], t0 + h[1], total_ins, nullptr, 0, 0);
+      { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, h[0], t0 + h[1], total_ins, nullptr, 0, 0); }
       return check_launch("set_result");
     }
   }
-  set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, total_ins, nullptr, 0, 0);
+  { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, total_ins, nullptr, 0, 0); }
   return check_launch("set_result");
 }
 
@@ -126,6 +131,13 @@ using namespace sfk;
 extern "C" {
 
 int sfk_abi_version(void) { return 1; }
+
+unsigned long long sfk_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int sfk_gen_query_keys(uint64_t seed, const uint32_t* present, const uint32_t* sorted_present, uint32_t v,
+                       const double* cdf, int64_t t0, int64_t n, uint32_t* out, void* stream) {
+  return launch_gen_query_keys(seed, present, sorted_present, v, cdf, t0, n, out, (cudaStream_t)stream);
+}
 
 const char* sfk_last_error(void) { return g_err; }
 
@@ -165,7 +177,7 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
     const bool safe = ((uint64_t)s.cmax + s.n_ins <= 0xFFFFFFFFull) && (s.n_del == 0 || (uint64_t)s.cmin >= s.n_del);
     if (safe) {
       if (int r = cm_fast(counters, seeds, d, w, ops + t0, ks, cnt, st)) return r;
-      set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, (int64_t)s.n_ins, inc_counts, d, (int64_t)s.n_ins);
+      { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, (int64_t)s.n_ins, inc_counts, d, (int64_t)s.n_ins); }
       return check_launch("set_result");
     }
     return parallel_apply(3, counters, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,

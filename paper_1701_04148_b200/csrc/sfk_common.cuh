@@ -118,6 +118,10 @@ struct Stats {
   uint32_t cmax, cmin;
 };
 
+// counts every kernel this library launches itself (CUB's internal sort/scan
+// launches are not included); read through sfk_launch_count()
+void note_launch();
+
 void set_error(const char* fmt, ...);
 int check_launch(const char* where);
 

@@ -128,11 +128,11 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
       cudaFuncSetAttribute(min_query_smem<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
       attr_set = true;
     }
-    min_query_smem<D, 4><<<sms, 1024, tab_bytes, st>>>(counters, sd, wm, w, ks, n, out);
+    { note_launch(); min_query_smem<D, 4><<<sms, 1024, tab_bytes, st>>>(counters, sd, wm, w, ks, n, out); }
     return check_launch("min_query_smem");
   }
   int blocks = grid_for(n, 256 * 4, sms * 8);
-  min_query_l2<D, 4><<<blocks, 256, 0, st>>>(counters, sd, wm, w, ks, n, out);
+  { note_launch(); min_query_l2<D, 4><<<blocks, 256, 0, st>>>(counters, sd, wm, w, ks, n, out); }
   return check_launch("min_query_l2");
 }
 
@@ -152,7 +152,7 @@ int launch_min_query(const uint32_t* counters, const uint64_t* seeds_host, int d
       Mod wm = make_mod((uint64_t)w);
       Seeds<MAXSEEDS> sd;
       for (int i = 0; i < d && i < MAXSEEDS; ++i) sd.s[i] = seeds_host[i];
-      min_query_generic<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(counters, sd, d, wm, w, ks, n, out);
+      { note_launch(); min_query_generic<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(counters, sd, d, wm, w, ks, n, out); }
       return check_launch("min_query_generic");
     }
   }
@@ -160,13 +160,13 @@ int launch_min_query(const uint32_t* counters, const uint64_t* seeds_host, int d
 
 int launch_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, cudaStream_t st) {
   if (n <= 0) return 0;
-  mix_batch_k<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(keys, n, out);
+  { note_launch(); mix_batch_k<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(keys, n, out); }
   return check_launch("mix_batch");
 }
 
 int launch_load_keys(KeySrc ks, int64_t n, uint64_t* out, cudaStream_t st) {
   if (n <= 0) return 0;
-  load_keys_k<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(ks, n, out);
+  { note_launch(); load_keys_k<<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(ks, n, out); }
   return check_launch("load_keys");
 }
 

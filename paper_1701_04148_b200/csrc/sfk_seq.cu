@@ -212,7 +212,7 @@ int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint3
   a.n = n;
   a.inc = inc;
   a.result = result;
-  seq_apply_k<<<1, 32, 0, st>>>(a, kind, variant);
+  { note_launch(); seq_apply_k<<<1, 32, 0, st>>>(a, kind, variant); }
   return check_launch("seq_apply");
 }
 

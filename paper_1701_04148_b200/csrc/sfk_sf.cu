@@ -245,6 +245,7 @@ struct ScanOut {
   const uint32_t* fat_init;  // snapshot of the fat (cell-major, Z per cell)
   uint32_t* fat_out;         // final fat (written at segment ends)
   uint32_t* obs;             // [t*D + row]: post own count (insert) / bucket max (delete)
+  uint2* obs2;               // [t*D + row]: {own slot count after the op, max of the other slots}
   uint2* links;              // [t*D + row]: {rank in cell, previous op or NONE}
   uint32_t n;                // ops
   uint32_t D;
@@ -252,7 +253,8 @@ struct ScanOut {
   Ctl* ctl;
 };
 
-template <int Z, bool HAS_FAT, bool WRITE_OBS, bool WRITE_LINKS>
+// WRITE_OBS: 0 none, 1 obs (b_min / bucket max), 2 obs2 (own count, max of the others)
+template <int Z, bool HAS_FAT, int WRITE_OBS, bool WRITE_LINKS>
 __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ vals, uint32_t N, int kb,
                                                                 const SegState<Z>* __restrict__ carry, ScanOut o) {
@@ -288,7 +290,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
       const int64_t post_own = (int64_t)init[k] + (int64_t)run.v[k];
       const int64_t pre_own = post_own + (op ? 1 : -1);
       if (op == 0 ? (pre_own == (int64_t)U32MAX) : (pre_own == 0)) local_fail = min(local_fail, t);
-      if (WRITE_OBS) {
+      if (WRITE_OBS == 2) {
+        uint32_t others = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < Z; ++q2)
+          if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+        o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
+      }
+      if (WRITE_OBS == 1) {
         uint32_t ob;
         if (op == 0) {
           ob = (uint32_t)post_own;
@@ -329,6 +338,7 @@ struct RunArgs {
   int DW;
   uint32_t* headflag;      // [t]
   uint32_t* head_e0;       // [t]
+  uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   Ctl* ctl;
 };
 
@@ -360,6 +370,11 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
 #pragma unroll
         for (int i = 0; i < D; ++i) a.opdata[(size_t)e * a.DW + i] = a.obs[(size_t)t * D + i];
       }
+    }
+    if (a.delbits) {
+      // e advances in warp-aligned strides, so the ballot covers one word
+      const unsigned bits = __ballot_sync(__activemask(), op != 0);
+      if ((threadIdx.x & 31) == 0) a.delbits[e >> 5] = bits;
     }
     const bool head = valid && !cont;
     a.headflag[t] = head ? 1u : 0u;
@@ -409,12 +424,21 @@ struct EngineArgs {
   const uint8_t* opflags;
   const uint32_t* opdata;
   int DW;
+  const uint2* obs2;        // SFF: {own count after the op, max of the other slots} per (t, row)
+  const uint32_t* delbits;  // SFF: delete flags in row-0 order, one bit per op
   Ctl* ctl;
   unsigned long long* inc;  // int64[d] tallies (two's complement add)
 };
 
-// MODE 0: SF (raise gated by b_min, deletes clamp to the bucket max)
+// MODE 0: SF1 (raise gated by b_min; runs are insert-only)
 // MODE 1: CU (raise always; saturation ruled out by the host precheck)
+// MODE 2: SFF. Within a run no other op touches the key's d buckets, so in
+//         row i the key's own slot count is A_i + x (x = the run's net
+//         inserts so far) and the other slots keep their maximum O_i. Every
+//         per-op observation follows from (A_i, O_i, x): an insert's b_min is
+//         min_i A_i + x, a delete clamps row i to max(A_i + x, O_i). The run
+//         replays from one delete-bit per op; insert stretches collapse in
+//         closed form (b_min rises by exactly one per insert).
 template <int D, int MODE>
 __global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
   const int lane = threadIdx.x & 31;
@@ -423,7 +447,7 @@ __global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
   uint32_t cells[D], rank[D], raised[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0;
-  uint32_t e0 = 0, info = 0;
+  uint32_t e0 = 0, info = 0, th = 0;
   uint32_t backoff = 32;
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !has && !exhausted);
@@ -438,6 +462,7 @@ __global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
           e0 = a.run_e0[r];
           info = a.run_info[r];
           const uint32_t t = a.run_t[r];
+          th = t;
           const uint64_t key = load_key(a.keys, t);
 #pragma unroll
           for (int i = 0; i < D; ++i) {
@@ -475,6 +500,55 @@ __global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
 #pragma unroll
           for (int i = 0; i < D; ++i)
             if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+        } else if (MODE == 2) {
+          const bool head_del = (a.delbits[e0 >> 5] >> (e0 & 31)) & 1u;
+          uint32_t A[D], O[D];
+          uint32_t A0 = U32MAX;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const uint2 ob = a.obs2[(size_t)th * D + i];
+            A[i] = head_del ? ob.x + 1u : ob.x - 1u;
+            O[i] = ob.y;
+            A0 = min(A0, A[i]);
+          }
+          uint32_t m = m0, x = 0;  // x: net inserts (mod 2^32; every A_i + x is a true count)
+          uint32_t e = e0, rem = L;
+          while (rem) {
+            const uint32_t off = e & 31u;
+            const uint32_t avail = min(32u - off, rem);
+            const uint32_t bits = (a.delbits[e >> 5] >> off) & (avail == 32u ? 0xffffffffu : ((1u << avail) - 1u));
+            uint32_t pos = 0;
+            while (pos < avail) {
+              const uint32_t rest = bits >> pos;
+              const uint32_t s = min(rest ? (uint32_t)(__ffs(rest) - 1) : 32u, avail - pos);
+              if (s) {
+                // k-th insert of the stretch raises iff m < A0 + x + k; once one
+                // raises, all later ones do
+                const int64_t diff = (int64_t)m - (int64_t)(uint32_t)(A0 + x);
+                const int64_t kstar = diff + 1 > 1 ? diff + 1 : 1;
+                if (kstar <= (int64_t)s) {
+                  m += (uint32_t)((int64_t)s - kstar + 1);
+#pragma unroll
+                  for (int i = 0; i < D; ++i)
+                    if (c[i] < m) { raised[i] += m - c[i]; c[i] = m; }
+                }
+                x += s;
+                pos += s;
+              }
+              if (pos < avail) {  // a delete
+                x -= 1u;
+                m = U32MAX;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                  c[i] = min(c[i], max(A[i] + x, O[i]));
+                  m = min(m, c[i]);
+                }
+                pos += 1;
+              }
+            }
+            e += avail;
+            rem -= avail;
+          }
         } else if (!hasdel) {
           // closed form: first k with b_k > m0, then every later op raises
           uint32_t k = 0;
@@ -699,6 +773,8 @@ struct Layout {
   void* tiles;        // SegState<Z> per tile
   uint32_t* fat_snap;
   uint32_t* obs;
+  uint2* obs2;
+  uint32_t* delbits;
   uint2* links;
   uint8_t* opflags;
   uint32_t* opdata;
@@ -733,13 +809,14 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   if (kind == 1) fat_cells = (uint64_t)d * wp;
   if (kind == 3) fat_cells = (uint64_t)d * w;
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
-  const bool need_obs = kind == 0 || kind == 1;
+  const bool need_obs = kind == 1;
   L.obs = cv.take<uint32_t>(need_obs ? N : 1);
+  L.obs2 = cv.take<uint2>(kind == 0 ? N : 1);
+  L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 2 : 1);
   const bool engine = kind != 3;
   L.links = cv.take<uint2>(engine ? N : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
-  const int DW = kind == 0 ? d : 1;
-  L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n * DW : 1);
+  L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);
   L.headflag = cv.take<uint32_t>(engine ? n : 1);
   L.head_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
@@ -758,18 +835,18 @@ size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, in
   return L.total;
 }
 
-template <int Z, bool HAS_FAT, bool OBS, bool LINKS>
+template <int Z, bool HAS_FAT, int OBS, bool LINKS>
 static int run_scan(const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
                     cudaStream_t st) {
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   SegState<Z>* ta = static_cast<SegState<Z>*>(tiles);
-  segscan_reduce_k<Z, HAS_FAT><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta);
-  segscan_tiles_k<Z><<<1, 1024, 0, st>>>(ta, ntiles);
-  segscan_apply_k<Z, HAS_FAT, OBS, LINKS><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta, so);
+  { note_launch(); segscan_reduce_k<Z, HAS_FAT><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta); }
+  { note_launch(); segscan_tiles_k<Z><<<1, 1024, 0, st>>>(ta, ntiles); }
+  { note_launch(); segscan_apply_k<Z, HAS_FAT, OBS, LINKS><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta, so); }
   return check_launch("segscan");
 }
 
-template <bool HAS_FAT, bool OBS, bool LINKS>
+template <bool HAS_FAT, int OBS, bool LINKS>
 static int run_scan_z(int z, const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
                       cudaStream_t st) {
   switch (z) {
@@ -838,18 +915,19 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.DW = DW;
   ra.headflag = L.headflag;
   ra.head_e0 = L.head_e0;
+  ra.delbits = MODE == 2 ? L.delbits : nullptr;
   ra.ctl = L.ctl;
-  runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra);
+  { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.headflag, L.ridx, (int)n, st);
   if (e != cudaSuccess) {
     set_error("run scan: %s", cudaGetErrorString(e));
     return (int)e;
   }
-  runs_build_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.headflag, L.ridx, L.head_e0, L.opflags, n, L.run_e0,
-                                                          L.run_info, L.run_t, L.ctl);
+  { note_launch(); runs_build_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.headflag, L.ridx, L.head_e0, L.opflags, n, L.run_e0,
+                                                          L.run_info, L.run_t, L.ctl); }
   const uint32_t cells = (uint32_t)(D * w);
-  pack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(slim, L.slim64, cells);
+  { note_launch(); pack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(slim, L.slim64, cells); }
   EngineArgs<D> ea;
   ea.slim64 = L.slim64;
   ea.w = (uint32_t)w;
@@ -863,6 +941,8 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.opflags = L.opflags;
   ea.opdata = L.opdata;
   ea.DW = DW;
+  ea.obs2 = L.obs2;
+  ea.delbits = L.delbits;
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
   // persistent: every warp resident (the deadlock-freedom argument needs the
@@ -873,8 +953,8 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slim_engine_k<D, MODE>, 256, 0);
     if (occ < 1) occ = 1;
   }
-  slim_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea);
-  unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells);
+  { note_launch(); slim_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea); }
+  { note_launch(); unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells); }
   return check_launch("slim_engine");
 }
 
@@ -885,52 +965,52 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
   const int sms = sm_count();
   const uint32_t n = (uint32_t)n64;
   const uint32_t N = (uint32_t)(D * n64);
-  ctl_init_k<<<1, 1, 0, st>>>(L.ctl);
+  { note_launch(); ctl_init_k<<<1, 1, 0, st>>>(L.ctl); }
   if (kind == 0) {  // ------------------------------------------------ SFF
     const int kb = bits_for((uint64_t)z);
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, fat_seeds, (uint64_t)w, z, kb, L, 0);
-    hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h);
+    { note_launch(); hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
     const size_t fat_bytes = (size_t)D * w * z * 4;
     cudaMemcpyAsync(L.fat_snap, fat, fat_bytes, cudaMemcpyDeviceToDevice, st);
-    ScanOut so{L.fat_snap, fat, L.obs, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<true, true, true>(z, L.k_out, L.v_out, N, kb, L.tiles, so, st)) return r;
-    fat_undo_k<D, 0><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, fat, (uint32_t)z);
-    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, kb, true, D, inc, st)) return r;
-    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0);
+    ScanOut so{L.fat_snap, fat, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, 2, true>(z, L.k_out, L.v_out, N, kb, L.tiles, so, st)) return r;
+    { note_launch(); fat_undo_k<D, 0><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, fat, (uint32_t)z); }
+    if (int r = run_engine<D, 2>(L, slim, slim_seeds, w, ks, n, kb, false, 0, inc, st)) return r;
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
   } else if (kind == 1) {  // ------------------------------------------ SF1
     HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
-    hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf);
+    { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
-    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
-    if (int r = run_scan_z<true, true, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
-    fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u);
+    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
+    if (int r = run_scan_z<true, 1, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
-    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs);
+    { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
-    ScanOut ss{nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<false, false, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, true, 1, inc, st)) return r;
-    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0);
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
-    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs);
+    { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
-    ScanOut ss{nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<false, false, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, false, 1, inc, st)) return r;
-    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0);
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else {  // ------------------------------------------------------- CM exact
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
-    hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h);
+    { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
     cudaMemcpyAsync(L.fat_snap, slim, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
-    ScanOut so{L.fat_snap, slim, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<true, false, false>(1, L.k_out, L.v_out, N, 0, L.tiles, so, st)) return r;
-    fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, slim, 1u);
-    count_ins_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ops, n64, L.ctl);
-    finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, reinterpret_cast<unsigned long long*>(inc), D, 1);
+    ScanOut so{L.fat_snap, slim, nullptr, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, 0, false>(1, L.k_out, L.v_out, N, 0, L.tiles, so, st)) return r;
+    { note_launch(); fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, slim, 1u); }
+    { note_launch(); count_ins_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ops, n64, L.ctl); }
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, reinterpret_cast<unsigned long long*>(inc), D, 1); }
   }
   return check_launch("sf_parallel");
 }
@@ -969,9 +1049,9 @@ int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64
   init.cmin = U32MAX;
   cudaMemcpyAsync(s, &init, sizeof(Stats), cudaMemcpyHostToDevice, st);
   const int sms = sm_count();
-  if (n > 0) stats_ops_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, n, s);
-  if (n > 0) stats_ins_before_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, s);
-  stats_counters_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(counters, cells, s);
+  if (n > 0) { note_launch(); stats_ops_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, n, s); }
+  if (n > 0) { note_launch(); stats_ins_before_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, s); }
+  { note_launch(); stats_counters_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(counters, cells, s); }
   cudaMemcpyAsync(host, s, sizeof(Stats), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
@@ -987,8 +1067,8 @@ static int cm_fast_d(uint32_t* counters, const uint64_t* seeds, int64_t w, const
   Seeds<D> sd;
   for (int i = 0; i < D; ++i) sd.s[i] = seeds[i];
   const int sms = sm_count();
-  cm_atomic_k<D><<<grid_for((n + 31) / 32 * 32, 256, sms * 16), 256, 0, st>>>(counters, sd, make_mod((uint64_t)w),
-                                                                              (uint32_t)w, ops, ks, n, nullptr);
+  { note_launch(); cm_atomic_k<D><<<grid_for((n + 31) / 32 * 32, 256, sms * 16), 256, 0, st>>>(counters, sd, make_mod((uint64_t)w),
+                                                                              (uint32_t)w, ops, ks, n, nullptr); }
   return check_launch("cm_atomic");
 }
 

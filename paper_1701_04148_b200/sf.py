@@ -97,6 +97,43 @@ def query_min(counters: torch.Tensor, seeds: np.ndarray, keys) -> torch.Tensor:
     return out
 
 
+def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host: torch.Tensor, out_host: torch.Tensor,
+                   chunk: int = 1 << 25, streams: int = 3) -> torch.Tensor:
+    """Point queries for a batch that lives in (pinned) HOST memory.
+
+    The batch is cut into chunks that flow through a multi-stream pipeline
+    (H2D copy -> fused hash/gather/min kernel -> D2H copy), so PCIe transfers
+    overlap the kernel as in the paper's GPU query design.
+    ``out_host`` (int64, same length) receives the estimates; returns it after
+    the last copy completed."""
+    L = _lib.lib()
+    dev = counters.device
+    n = int(keys_host.shape[0])
+    d, w = counters.shape
+    kind = _lib.KEY_U32 if keys_host.dtype == torch.uint32 else _lib.KEY_U64
+    esz = 4 if kind == _lib.KEY_U32 else 8
+    cur = torch.cuda.current_stream(dev)
+    ss = [torch.cuda.Stream(dev) for _ in range(streams)]
+    kbuf = [torch.empty(chunk * esz, dtype=torch.uint8, device=dev) for _ in range(streams)]
+    obuf = [torch.empty(chunk, dtype=torch.int64, device=dev) for _ in range(streams)]
+    for s in ss:
+        s.wait_stream(cur)
+    for c, a in enumerate(range(0, n, chunk)):
+        b = min(n, a + chunk)
+        s = ss[c % streams]
+        with torch.cuda.stream(s):
+            kd = kbuf[c % streams][: (b - a) * esz].view(keys_host.dtype)
+            kd.copy_(keys_host[a:b], non_blocking=True)
+            od = obuf[c % streams][: b - a]
+            rc = L.sfk_min_query(counters.data_ptr(), seeds.ctypes.data, d, w, kd.data_ptr(), kind, 0, b - a,
+                                 od.data_ptr(), int(s.cuda_stream))
+            _lib.check(rc, "sfk_min_query")
+            out_host[a:b].copy_(od, non_blocking=True)
+    for s in ss:
+        cur.wait_stream(s)
+    return out_host
+
+
 class SfSketch:
     """One of the five slim-fat variants over a shared interface."""
 

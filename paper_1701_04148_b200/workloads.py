@@ -106,6 +106,36 @@ def _mix_np(x: np.ndarray) -> np.ndarray:
     return x ^ (x >> np.uint64(31))
 
 
+class DeviceQueryStream:
+    """The cfg-5 query stream generated on the GPU (``sfk_gen_query_keys``):
+    ``keys(t0, n)`` equals ``query_keys(seed, present, alpha_q, t0, t0 + n)``."""
+
+    def __init__(self, seed: int, present: np.ndarray, alpha_q: float):
+        import torch
+
+        from . import _lib
+
+        self._lib = _lib
+        self.seed = int(seed) & MASK64
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.present = torch.from_numpy(np.ascontiguousarray(present, dtype=np.uint32)).to(dev)
+        self.sorted = torch.from_numpy(np.sort(present).astype(np.uint32)).to(dev)
+        self.v = int(present.shape[0])
+        self.cdf = None if alpha_q == 0.0 else torch.from_numpy(zipf_cdf(self.v, alpha_q)).to(dev)
+
+    def keys(self, t0: int, n: int, out=None):
+        import torch
+
+        if out is None:
+            out = torch.empty(n, dtype=torch.uint32, device=self.present.device)
+        L = self._lib.lib()
+        rc = L.sfk_gen_query_keys(self.seed, self.present.data_ptr(), self.sorted.data_ptr(), self.v,
+                                  self.cdf.data_ptr() if self.cdf is not None else None, int(t0), int(n),
+                                  out.data_ptr(), self._lib.stream_ptr())
+        self._lib.check(rc, "sfk_gen_query_keys")
+        return out
+
+
 def query_keys(seed: int, present: np.ndarray, alpha_q: float, t0: int, t1: int) -> np.ndarray:
     """Keys t0..t1-1 of the cfg-5 query stream (counter-based, so any slice
     is reproducible). Draw t: h = finalize64(seed + (t+1)*GOLDEN); bit 0 picks
