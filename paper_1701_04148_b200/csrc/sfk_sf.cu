@@ -50,10 +50,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // ---------------------------------------------------------------- shared state
 struct Ctl {
-  uint32_t fail_t;     // first failing op (NONE32 if none)
-  uint32_t ticket;     // engine run ticket
+  uint32_t fail_t;           // first failing op (NONE32 if none)
+  uint32_t n_runs;           // runs of the slim engine
   unsigned long long n_ins;  // inserts applied (t < t*)
-  uint32_t n_runs;
+  uint32_t qhead, qtail;     // engine ready queue
+  uint32_t executed;         // engine runs finished
   uint32_t pad;
 };
 
@@ -246,7 +247,7 @@ struct ScanOut {
   uint32_t* fat_out;         // final fat (written at segment ends)
   uint32_t* obs;             // [t*D + row]: post own count (insert) / bucket max (delete)
   uint2* obs2;               // [t*D + row]: {own slot count after the op, max of the other slots}
-  uint2* links;              // [t*D + row]: {rank in cell, previous op or NONE}
+  uint2* links;              // [t*D + row]: {previous op on the cell, next op on the cell} (NONE if absent)
   uint32_t n;                // ops
   uint32_t D;
   uint32_t row_cells;
@@ -315,9 +316,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
       }
     }
     if (WRITE_LINKS) {
-      const uint32_t rank = e - run.head;
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
-      o.links[(size_t)t * o.D + row] = make_uint2(rank, prev);
+      const uint32_t next = (e + 1 < N && keys[e + 1] == c) ? (vals[e + 1] >> (kb + 1)) : NONE32;
+      o.links[(size_t)t * o.D + row] = make_uint2(prev, next);
     }
     prev_t = t;
   }
@@ -330,12 +331,11 @@ struct RunArgs {
   const uint32_t* vals0;  // row-0 sorted vals (slim cells)
   int kb;
   uint32_t n;
-  const uint2* links;
-  const uint32_t* obs;     // may be null (CU)
+  const uint2* links;      // {prev op, next op} per (t, row)
+  const uint32_t* obs;     // SF1: post-insert own fat count per (t, row); null otherwise
   KeySrc keys;
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
-  uint32_t* opdata;        // [e*DW + ...]
-  int DW;
+  uint32_t* opdata;        // SF1: b_min per op, row-0 order
   uint32_t* headflag;      // [t]
   uint32_t* head_e0;       // [t]
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
@@ -351,25 +351,20 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const uint32_t t = v >> (a.kb + 1);
     const uint32_t op = (v >> a.kb) & 1u;
     const bool valid = t < tstar;
-    uint2 lk[D];
+    uint32_t prev[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) lk[i] = a.links[(size_t)t * D + i];
-    bool cont = valid && lk[0].y != NONE32;
+    for (int i = 0; i < D; ++i) prev[i] = a.links[(size_t)t * D + i].x;
+    bool cont = valid && prev[0] != NONE32;
 #pragma unroll
-    for (int i = 1; i < D; ++i) cont = cont && (lk[i].y == lk[0].y);
-    // same cells is not enough for the closed forms: require the same key
-    if (cont) cont = load_key(a.keys, lk[0].y) == load_key(a.keys, t);
+    for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
+    // the same d cells is not enough for the closed forms: require the same key
+    if (cont) cont = load_key(a.keys, prev[0]) == load_key(a.keys, t);
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
     if (a.obs) {
-      if (op == 0 || a.DW < D) {
-        uint32_t b = U32MAX;
+      uint32_t b = U32MAX;
 #pragma unroll
-        for (int i = 0; i < D; ++i) b = min(b, a.obs[(size_t)t * D + i]);
-        a.opdata[(size_t)e * a.DW] = b;
-      } else {
-#pragma unroll
-        for (int i = 0; i < D; ++i) a.opdata[(size_t)e * a.DW + i] = a.obs[(size_t)t * D + i];
-      }
+      for (int i = 0; i < D; ++i) b = min(b, a.obs[(size_t)t * D + i]);
+      a.opdata[e] = b;
     }
     if (a.delbits) {
       // e advances in warp-aligned strides, so the ballot covers one word
@@ -386,52 +381,125 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
   if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&a.ctl->n_ins, (unsigned long long)ins);
 }
 
-__global__ void runs_build_k(const uint32_t* __restrict__ headflag, const uint32_t* __restrict__ ridx,
-                             const uint32_t* __restrict__ head_e0, const uint8_t* __restrict__ opflags, uint32_t n,
-                             uint32_t* __restrict__ run_e0, uint32_t* __restrict__ run_info,
-                             uint32_t* __restrict__ run_t, Ctl* ctl) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    if (t == n - 1) ctl->n_runs = ridx[t] + headflag[t];
-    if (!headflag[t]) continue;
-    const uint32_t r = ridx[t];
-    const uint32_t e0 = head_e0[t];
-    uint32_t hasdel = opflags[e0] & 1u;
-    uint32_t L = 1;
-    for (uint32_t e = e0 + 1; e < n; ++e) {
-      const uint8_t f = opflags[e];
-      if ((f & 6u) != 6u) break;
-      hasdel |= f & 1u;
-      ++L;
+// Run records, indexed by run id (= rank of the head in stream order):
+// e0/info/t, the d slim cells, the successor run on each cell (the run that
+// holds the next op on that cell), and the dependency count (cells whose
+// head op has a predecessor). Runs with no dependency are queued.
+template <int D>
+struct BuildArgs {
+  const uint32_t* headflag;
+  const uint32_t* ridx;
+  const uint32_t* head_e0;
+  const uint8_t* opflags;
+  const uint32_t* vals0;
+  const uint2* links;
+  int kb;
+  uint32_t n;
+  KeySrc keys;
+  Seeds<D> seeds;
+  Mod wm;
+  uint32_t w;
+  uint32_t* run_e0;
+  uint32_t* run_info;
+  uint32_t* run_t;
+  uint32_t* run_cells;
+  uint32_t* run_succ;
+  uint32_t* run_dep;
+  uint32_t* queue;
+  Ctl* ctl;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
+  const uint32_t tstar = a.ctl->fail_t;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
+    if (t == a.n - 1) a.ctl->n_runs = a.ridx[t] + a.headflag[t];
+    bool ready = false;
+    uint32_t r = 0;
+    if (a.headflag[t]) {
+      r = a.ridx[t];
+      const uint32_t e0 = a.head_e0[t];
+      uint32_t hasdel = a.opflags[e0] & 1u;
+      uint32_t L = 1;
+      for (uint32_t e = e0 + 1; e < a.n; ++e) {
+        const uint8_t f = a.opflags[e];
+        if ((f & 6u) != 6u) break;
+        hasdel |= f & 1u;
+        ++L;
+      }
+      const uint32_t t_last = a.vals0[e0 + L - 1] >> (a.kb + 1);
+      const uint64_t key = load_key(a.keys, t);
+      uint32_t dep = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        a.run_cells[(size_t)r * D + i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+        dep += a.links[(size_t)t * D + i].x != NONE32;
+        const uint32_t s = a.links[(size_t)t_last * D + i].y;
+        a.run_succ[(size_t)r * D + i] = (s != NONE32 && s < tstar) ? a.ridx[s] : NONE32;
+      }
+      a.run_e0[r] = e0;
+      a.run_info[r] = L | (hasdel << 31);
+      a.run_t[r] = t;
+      a.run_dep[r] = dep;
+      ready = dep == 0;
     }
-    run_e0[r] = e0;
-    run_info[r] = L | (hasdel << 31);
-    run_t[r] = t;
+    // queue the runs that are ready from the start (warp-aggregated push)
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, ready);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&a.ctl->qtail, (uint32_t)__popc(m));
+      base = __shfl_sync(am, base, leader);
+      if (ready) a.queue[base + __popc(m & lanemask_lt())] = r;
+    }
   }
 }
 
 // ---------------------------------------------------------------- 5. engine
+__device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int D>
 struct EngineArgs {
-  unsigned long long* slim64;
-  uint32_t w;  // slim row width
-  Seeds<D> seeds;
-  Mod wm;
-  KeySrc keys;
+  uint32_t* slim;
   const uint32_t* run_e0;
   const uint32_t* run_info;
   const uint32_t* run_t;
-  const uint2* links;
-  const uint8_t* opflags;
-  const uint32_t* opdata;
-  int DW;
+  const uint32_t* run_cells;
+  const uint32_t* run_succ;
+  uint32_t* run_dep;
+  uint32_t* queue;
+  const uint32_t* opdata;   // SF1: b_min per op (row-0 order)
   const uint2* obs2;        // SFF: {own count after the op, max of the other slots} per (t, row)
   const uint32_t* delbits;  // SFF: delete flags in row-0 order, one bit per op
   Ctl* ctl;
   unsigned long long* inc;  // int64[d] tallies (two's complement add)
 };
 
+// Replay one run on its d slim cells (registers c[], tallies raised[]).
 // MODE 0: SF1 (raise gated by b_min; runs are insert-only)
-// MODE 1: CU (raise always; saturation ruled out by the host precheck)
+// MODE 1: CU (every insert raises; saturation ruled out by the host precheck)
 // MODE 2: SFF. Within a run no other op touches the key's d buckets, so in
 //         row i the key's own slot count is A_i + x (x = the run's net
 //         inserts so far) and the other slots keep their maximum O_i. Every
@@ -440,157 +508,176 @@ struct EngineArgs {
 //         replays from one delete-bit per op; insert stretches collapse in
 //         closed form (b_min rises by exactly one per insert).
 template <int D, int MODE>
-__global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t R = a.ctl->n_runs;
-  bool has = false, exhausted = false;
-  uint32_t cells[D], rank[D], raised[D];
+__device__ __forceinline__ void replay_run(const EngineArgs<D>& a, uint32_t e0, uint32_t info, uint32_t th,
+                                           uint32_t (&c)[D], uint32_t (&raised)[D]) {
+  const uint32_t L = info & 0x7fffffffu;
+  uint32_t m0 = c[0];
 #pragma unroll
-  for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0;
-  uint32_t e0 = 0, info = 0, th = 0;
-  uint32_t backoff = 32;
+  for (int i = 1; i < D; ++i) m0 = min(m0, c[i]);
+  if (MODE == 1) {
+    const uint64_t tgt = (uint64_t)m0 + L;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+      if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+  } else if (MODE == 0) {
+    // b_min strictly increases along a same-key insert run: the first k
+    // with b_k > m0 raises, and so does every later op
+    uint32_t k = 0;
+    while (k < L && a.opdata[e0 + k] <= m0) ++k;
+    const uint32_t s = L - k;
+    if (s) {
+      const uint64_t tgt = (uint64_t)m0 + s;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+        if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+    }
+  } else {
+    const bool head_del = (a.delbits[e0 >> 5] >> (e0 & 31)) & 1u;
+    uint32_t A[D], O[D];
+    uint32_t A0 = U32MAX;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint2 ob = a.obs2[(size_t)th * D + i];
+      A[i] = head_del ? ob.x + 1u : ob.x - 1u;
+      O[i] = ob.y;
+      A0 = min(A0, A[i]);
+    }
+    uint32_t m = m0, x = 0;  // x: net inserts (mod 2^32; every A_i + x is a true count)
+    uint32_t e = e0, rem = L;
+    uint32_t word = a.delbits[e >> 5];
+    while (rem) {
+      const uint32_t off = e & 31u;
+      const uint32_t avail = min(32u - off, rem);
+      const uint32_t bits = (word >> off) & (avail == 32u ? 0xffffffffu : ((1u << avail) - 1u));
+      if (avail < rem) word = a.delbits[(e >> 5) + 1];  // prefetch the next word
+      uint32_t pos = 0;
+      while (pos < avail) {
+        const uint32_t rest = bits >> pos;
+        const uint32_t s = min(rest ? (uint32_t)(__ffs(rest) - 1) : 32u, avail - pos);
+        if (s) {
+          // k-th insert of the stretch raises iff m < A0 + x + k; once one
+          // raises, all later ones do
+          const int64_t diff = (int64_t)m - (int64_t)(uint32_t)(A0 + x);
+          const int64_t kstar = diff + 1 > 1 ? diff + 1 : 1;
+          if (kstar <= (int64_t)s) {
+            m += (uint32_t)((int64_t)s - kstar + 1);
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+              if (c[i] < m) { raised[i] += m - c[i]; c[i] = m; }
+          }
+          x += s;
+          pos += s;
+        }
+        if (pos < avail) {  // a delete
+          x -= 1u;
+          m = U32MAX;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            c[i] = min(c[i], max(A[i] + x, O[i]));
+            m = min(m, c[i]);
+          }
+          pos += 1;
+        }
+      }
+      e += avail;
+      rem -= avail;
+    }
+  }
+}
+
+// Dataflow engine over the run DAG. A run executes exactly once, after every
+// run holding an earlier op on one of its cells finished: each finishing run
+// decrements its successors' dependency counters (acq_rel) and the lane that
+// releases the last dependency runs that successor directly (further newly
+// ready runs go to a global queue that idle lanes pop). No lane ever waits
+// while holding a run, so the engine cannot deadlock; it ends when every run
+// has executed.
+template <int D, int MODE>
+__global__ void __launch_bounds__(256) dag_engine_k(EngineArgs<D> a) {
+  __shared__ uint32_t blk_pending;  // completions not yet published to ctl->executed
+  __shared__ volatile int blk_exit;
+  if (threadIdx.x == 0) {
+    blk_pending = 0;
+    blk_exit = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t R = a.ctl->n_runs;
+  uint32_t cur = NONE32, slot = NONE32, done_local = 0, backoff = 0, idle_iters = 0;
+  uint32_t raised[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) raised[i] = 0;
   while (true) {
-    const unsigned need = __ballot_sync(0xffffffffu, !has && !exhausted);
+    const unsigned need = __ballot_sync(0xffffffffu, cur == NONE32 && slot == NONE32);
     if (need) {
       const int leader = __ffs(need) - 1;
       uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&a.ctl->ticket, (uint32_t)__popc(need));
+      if (lane == leader) base = atomicAdd(&a.ctl->qhead, (uint32_t)__popc(need));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (!has && !exhausted) {
-        const uint32_t r = base + __popc(need & lanemask_lt());
-        if (r < R) {
-          e0 = a.run_e0[r];
-          info = a.run_info[r];
-          const uint32_t t = a.run_t[r];
-          th = t;
-          const uint64_t key = load_key(a.keys, t);
-#pragma unroll
-          for (int i = 0; i < D; ++i) {
-            cells[i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
-            rank[i] = a.links[(size_t)t * D + i].x;
-          }
-          has = true;
-        } else {
-          exhausted = true;
-        }
+      if (cur == NONE32 && slot == NONE32) slot = base + __popc(need & lanemask_lt());
+    }
+    if (cur == NONE32 && slot < R) {
+      const uint32_t v = ld_relaxed_u32(a.queue + slot);
+      if (v != NONE32) {
+        fence_acq_rel_gpu();  // acquire: the pusher's release pattern covers the run's inputs
+        cur = v;
+        slot = NONE32;
       }
     }
-    if (__all_sync(0xffffffffu, !has)) break;  // no lane holds a run and none can get one
-    bool progressed = false;
-    if (has) {
-      unsigned long long wv[D];
-      bool ready = true;
+    const bool busy = cur != NONE32;
+    if (busy) {
+      const uint32_t r = cur;
+      const uint32_t e0 = a.run_e0[r], info = a.run_info[r], th = a.run_t[r];
+      uint32_t cells[D], succ[D], c[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        wv[i] = ld_relaxed_u64(a.slim64 + cells[i]);
-        ready = ready && ((uint32_t)(wv[i] >> 32) == rank[i]);
+        cells[i] = a.run_cells[(size_t)r * D + i];
+        succ[i] = a.run_succ[(size_t)r * D + i];
       }
-      if (ready) {
-        uint32_t c[D];
 #pragma unroll
-        for (int i = 0; i < D; ++i) c[i] = (uint32_t)wv[i];
-        const uint32_t L = info & 0x7fffffffu;
-        const bool hasdel = info >> 31;
-        uint32_t m0 = c[0];
+      for (int i = 0; i < D; ++i) c[i] = ld_relaxed_u32(a.slim + cells[i]);
+      replay_run<D, MODE>(a, e0, info, th, c, raised);
 #pragma unroll
-        for (int i = 1; i < D; ++i) m0 = min(m0, c[i]);
-        if (MODE == 1) {
-          // every insert raises: s = L
-          const uint64_t tgt = (uint64_t)m0 + L;
+      for (int i = 0; i < D; ++i) st_relaxed_u32(a.slim + cells[i], c[i]);
+      fence_acq_rel_gpu();  // release the cell values before the dependency decrements
+      uint32_t ready[D];
+      int nready = 0;
 #pragma unroll
-          for (int i = 0; i < D; ++i)
-            if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
-        } else if (MODE == 2) {
-          const bool head_del = (a.delbits[e0 >> 5] >> (e0 & 31)) & 1u;
-          uint32_t A[D], O[D];
-          uint32_t A0 = U32MAX;
-#pragma unroll
-          for (int i = 0; i < D; ++i) {
-            const uint2 ob = a.obs2[(size_t)th * D + i];
-            A[i] = head_del ? ob.x + 1u : ob.x - 1u;
-            O[i] = ob.y;
-            A0 = min(A0, A[i]);
-          }
-          uint32_t m = m0, x = 0;  // x: net inserts (mod 2^32; every A_i + x is a true count)
-          uint32_t e = e0, rem = L;
-          while (rem) {
-            const uint32_t off = e & 31u;
-            const uint32_t avail = min(32u - off, rem);
-            const uint32_t bits = (a.delbits[e >> 5] >> off) & (avail == 32u ? 0xffffffffu : ((1u << avail) - 1u));
-            uint32_t pos = 0;
-            while (pos < avail) {
-              const uint32_t rest = bits >> pos;
-              const uint32_t s = min(rest ? (uint32_t)(__ffs(rest) - 1) : 32u, avail - pos);
-              if (s) {
-                // k-th insert of the stretch raises iff m < A0 + x + k; once one
-                // raises, all later ones do
-                const int64_t diff = (int64_t)m - (int64_t)(uint32_t)(A0 + x);
-                const int64_t kstar = diff + 1 > 1 ? diff + 1 : 1;
-                if (kstar <= (int64_t)s) {
-                  m += (uint32_t)((int64_t)s - kstar + 1);
-#pragma unroll
-                  for (int i = 0; i < D; ++i)
-                    if (c[i] < m) { raised[i] += m - c[i]; c[i] = m; }
-                }
-                x += s;
-                pos += s;
-              }
-              if (pos < avail) {  // a delete
-                x -= 1u;
-                m = U32MAX;
-#pragma unroll
-                for (int i = 0; i < D; ++i) {
-                  c[i] = min(c[i], max(A[i] + x, O[i]));
-                  m = min(m, c[i]);
-                }
-                pos += 1;
-              }
-            }
-            e += avail;
-            rem -= avail;
-          }
-        } else if (!hasdel) {
-          // closed form: first k with b_k > m0, then every later op raises
-          uint32_t k = 0;
-          while (k < L && a.opdata[(size_t)(e0 + k) * a.DW] <= m0) ++k;
-          const uint32_t s = L - k;
-          if (s) {
-            const uint64_t tgt = (uint64_t)m0 + s;
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-              if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
-          }
-        } else {
-          for (uint32_t k = 0; k < L; ++k) {
-            const size_t e = (size_t)e0 + k;
-            const uint8_t f = a.opflags[e];
-            if (!(f & 1u)) {
-              const uint32_t b = a.opdata[e * a.DW];
-              uint32_t m = c[0];
-#pragma unroll
-              for (int i = 1; i < D; ++i) m = min(m, c[i]);
-              if (m < b) {
-#pragma unroll
-                for (int i = 0; i < D; ++i)
-                  if (c[i] == m) { c[i] += 1u; raised[i] += 1u; }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < D; ++i) c[i] = min(c[i], a.opdata[e * a.DW + i]);
-            }
-          }
+      for (int i = 0; i < D; ++i)
+        if (succ[i] != NONE32 && atom_add_relaxed(a.run_dep + succ[i], 0xFFFFFFFFu) == 1u) ready[nready++] = succ[i];
+      uint32_t next = NONE32;
+      if (nready) {
+        fence_acq_rel_gpu();  // acquire the other producers' cells; release for the pushes
+        next = ready[0];
+        for (int k = 1; k < nready; ++k) {
+          const uint32_t q = atomicAdd(&a.ctl->qtail, 1u);
+          st_relaxed_u32(a.queue + q, ready[k]);
         }
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-          st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
-        has = false;
-        progressed = true;
-        backoff = 32;
       }
+      ++done_local;
+      cur = next;
     }
-    if (!__any_sync(0xffffffffu, progressed)) {
-      __nanosleep(backoff);
-      backoff = min(backoff * 2, 1024u);
+    if (!__any_sync(0xffffffffu, busy)) {
+      // idle warp: publish completions to the block, warp 0 moves them to the
+      // global count now and then and raises the block's exit flag at the end
+      uint32_t dsum = done_local;
+      for (int off = 16; off > 0; off >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, off);
+      done_local = 0;
+      if (lane == 0 && dsum) atomicAdd(&blk_pending, dsum);
+      if (wid == 0 && (++idle_iters & 7u) == 0) {
+        uint32_t ex = 0;
+        if (lane == 0) {
+          const uint32_t p = atomicExch(&blk_pending, 0u);
+          ex = p ? atomicAdd(&a.ctl->executed, p) + p : ld_relaxed_u32(&a.ctl->executed);
+          if (ex >= R) blk_exit = 1;
+        }
+      }
+      __syncwarp();
+      if (blk_exit) break;
+      if (backoff) __nanosleep(backoff);
+      backoff = min(backoff * 2 + 16, 256u);
+    } else {
+      backoff = 0;
     }
   }
 #pragma unroll
@@ -601,19 +688,13 @@ __global__ void __launch_bounds__(256) slim_engine_k(EngineArgs<D> a) {
   }
 }
 
-__global__ void pack_slim_k(const uint32_t* __restrict__ slim, unsigned long long* __restrict__ s64, uint32_t cells) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) s64[c] = slim[c];
-}
-__global__ void unpack_slim_k(const unsigned long long* __restrict__ s64, uint32_t* __restrict__ slim, uint32_t cells) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
-    slim[c] = (uint32_t)s64[c];
-}
-
 __global__ void ctl_init_k(Ctl* ctl) {
   ctl->fail_t = NONE32;
-  ctl->ticket = 0;
-  ctl->n_ins = 0;
   ctl->n_runs = 0;
+  ctl->n_ins = 0;
+  ctl->qhead = 0;
+  ctl->qtail = 0;
+  ctl->executed = 0;
 }
 
 // undo the fat deltas of ops t >= t* (the fat was written for the whole
@@ -782,7 +863,7 @@ struct Layout {
   uint32_t* head_e0;
   uint32_t* ridx;
   uint32_t *run_e0, *run_info, *run_t;
-  unsigned long long* slim64;
+  uint32_t *run_cells, *run_succ, *run_dep, *queue;
   Ctl* ctl;
   Stats* stats;
   size_t total;
@@ -823,7 +904,10 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.run_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.run_info = cv.take<uint32_t>(engine ? n : 1);
   L.run_t = cv.take<uint32_t>(engine ? n : 1);
-  L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
+  L.run_cells = cv.take<uint32_t>(engine ? N : 1);
+  L.run_succ = cv.take<uint32_t>(engine ? N : 1);
+  L.run_dep = cv.take<uint32_t>(engine ? n : 1);
+  L.queue = cv.take<uint32_t>(engine ? n : 1);
   L.total = cv.off + 256;
   L.ok = cv.ok;
   return L;
@@ -898,21 +982,20 @@ static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uin
 }
 
 // The run/engine tail shared by SFF, SF1 and CU once the row-0 sorted slim
-// pairs (k_out/v_out) and links (+ obs) exist.
+// pairs (k_out/v_out), the links and the observations exist.
 template <int D, int MODE>
 static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int64_t w, KeySrc ks, uint32_t n, int kb,
-                      bool with_obs, int DW, int64_t* inc, cudaStream_t st) {
+                      int64_t* inc, cudaStream_t st) {
   const int sms = sm_count();
   RunArgs<D> ra;
   ra.vals0 = L.v_out;
   ra.kb = kb;
   ra.n = n;
   ra.links = L.links;
-  ra.obs = with_obs ? L.obs : nullptr;
+  ra.obs = MODE == 0 ? L.obs : nullptr;
   ra.keys = ks;
   ra.opflags = L.opflags;
   ra.opdata = L.opdata;
-  ra.DW = DW;
   ra.headflag = L.headflag;
   ra.head_e0 = L.head_e0;
   ra.delbits = MODE == 2 ? L.delbits : nullptr;
@@ -924,38 +1007,50 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
     set_error("run scan: %s", cudaGetErrorString(e));
     return (int)e;
   }
-  { note_launch(); runs_build_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.headflag, L.ridx, L.head_e0, L.opflags, n, L.run_e0,
-                                                          L.run_info, L.run_t, L.ctl); }
-  const uint32_t cells = (uint32_t)(D * w);
-  { note_launch(); pack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(slim, L.slim64, cells); }
+  cudaMemsetAsync(L.queue, 0xFF, (size_t)n * 4, st);
+  BuildArgs<D> ba;
+  ba.headflag = L.headflag;
+  ba.ridx = L.ridx;
+  ba.head_e0 = L.head_e0;
+  ba.opflags = L.opflags;
+  ba.vals0 = L.v_out;
+  ba.links = L.links;
+  ba.kb = kb;
+  ba.n = n;
+  ba.keys = ks;
+  for (int i = 0; i < D; ++i) ba.seeds.s[i] = slim_seeds[i];
+  ba.wm = make_mod((uint64_t)w);
+  ba.w = (uint32_t)w;
+  ba.run_e0 = L.run_e0;
+  ba.run_info = L.run_info;
+  ba.run_t = L.run_t;
+  ba.run_cells = L.run_cells;
+  ba.run_succ = L.run_succ;
+  ba.run_dep = L.run_dep;
+  ba.queue = L.queue;
+  ba.ctl = L.ctl;
+  { note_launch(); runs_build_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ba); }
   EngineArgs<D> ea;
-  ea.slim64 = L.slim64;
-  ea.w = (uint32_t)w;
-  for (int i = 0; i < D; ++i) ea.seeds.s[i] = slim_seeds[i];
-  ea.wm = make_mod((uint64_t)w);
-  ea.keys = ks;
+  ea.slim = slim;
   ea.run_e0 = L.run_e0;
   ea.run_info = L.run_info;
   ea.run_t = L.run_t;
-  ea.links = L.links;
-  ea.opflags = L.opflags;
+  ea.run_cells = L.run_cells;
+  ea.run_succ = L.run_succ;
+  ea.run_dep = L.run_dep;
+  ea.queue = L.queue;
   ea.opdata = L.opdata;
-  ea.DW = DW;
   ea.obs2 = L.obs2;
   ea.delbits = L.delbits;
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
-  // persistent: every warp resident (the deadlock-freedom argument needs the
-  // ticket holders to be running, which any launch satisfies; residency
-  // just keeps the window of in-flight runs wide)
   static int occ = -1;
   if (occ < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slim_engine_k<D, MODE>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dag_engine_k<D, MODE>, 256, 0);
     if (occ < 1) occ = 1;
   }
-  { note_launch(); slim_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea); }
-  { note_launch(); unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells); }
-  return check_launch("slim_engine");
+  { note_launch(); dag_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea); }
+  return check_launch("dag_engine");
 }
 
 template <int D>
@@ -976,7 +1071,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
     ScanOut so{L.fat_snap, fat, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<true, 2, true>(z, L.k_out, L.v_out, N, kb, L.tiles, so, st)) return r;
     { note_launch(); fat_undo_k<D, 0><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, fat, (uint32_t)z); }
-    if (int r = run_engine<D, 2>(L, slim, slim_seeds, w, ks, n, kb, false, 0, inc, st)) return r;
+    if (int r = run_engine<D, 2>(L, slim, slim_seeds, w, ks, n, kb, inc, st)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
   } else if (kind == 1) {  // ------------------------------------------ SF1
     HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
@@ -991,7 +1086,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
     ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
-    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, true, 1, inc, st)) return r;
+    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
@@ -999,7 +1094,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
     ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
-    if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, false, 1, inc, st)) return r;
+    if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else {  // ------------------------------------------------------- CM exact
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
