@@ -72,6 +72,11 @@ const char* sfk_last_error(void);
  * (its own kernels; CUB's internal radix-sort/scan launches excluded). */
 unsigned long long sfk_launch_count(void);
 
+/* Diagnostics of the ordered slim engine, summed over launches since the last
+ * reset: out8 = {words on the gap path, words on the steady path, words
+ * replayed op by op, replay cycles, runs executed, warp iterations, 0, 0}. */
+int sfk_engine_stats(unsigned long long* out8, int reset);
+
 /* Workload utility (no reference counterpart; SURVEY.md §8(d) cfg 5): keys
  * t0 .. t0+n-1 of the counter-based query stream of
  * paper_1701_04148_b200.workloads.query_keys, generated on the device.

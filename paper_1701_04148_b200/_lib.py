@@ -37,6 +37,7 @@ EXPORTS = (
     "sfk_oracle_slim_apply",
     "sfk_launch_count",
     "sfk_gen_query_keys",
+    "sfk_engine_stats",
 )
 
 _lib = None
@@ -76,6 +77,7 @@ def load_library() -> ctypes.CDLL:
     L.sfk_sf_apply.argtypes = [I, P, P, P, P, P, I, I64, I64, I, P, P, I, I, I64, P, P, P, SZ, I, P]
     L.sfk_oracle_slim_apply.argtypes = [P, P, I, I64, P, I, I, P, I64, P, P, P]
     L.sfk_launch_count.restype = ctypes.c_ulonglong
+    L.sfk_engine_stats.argtypes = [P, I]
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]
     _lib = L
     return L

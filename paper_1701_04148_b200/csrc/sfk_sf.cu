@@ -41,6 +41,17 @@ namespace sfk {
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int ENGINE_BLOCKS_PER_SM = 1;
+
+static int engine_blocks_per_sm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SFK_ENGINE_BLOCKS_PER_SM");  // tuning knob
+    v = s ? atoi(s) : ENGINE_BLOCKS_PER_SM;
+    if (v < 1 || v > 8) v = ENGINE_BLOCKS_PER_SM;
+  }
+  return v;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -247,7 +258,7 @@ struct ScanOut {
   uint32_t* fat_out;         // final fat (written at segment ends)
   uint32_t* obs;             // [t*D + row]: post own count (insert) / bucket max (delete)
   uint2* obs2;               // [t*D + row]: {own slot count after the op, max of the other slots}
-  uint2* links;              // [t*D + row]: {previous op on the cell, next op on the cell} (NONE if absent)
+  uint2* links;              // [t*D + row]: {rank of the op in its cell, previous op on the cell or NONE}
   uint32_t n;                // ops
   uint32_t D;
   uint32_t row_cells;
@@ -317,8 +328,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
     }
     if (WRITE_LINKS) {
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
-      const uint32_t next = (e + 1 < N && keys[e + 1] == c) ? (vals[e + 1] >> (kb + 1)) : NONE32;
-      o.links[(size_t)t * o.D + row] = make_uint2(prev, next);
+      o.links[(size_t)t * o.D + row] = make_uint2(e - run.head, prev);
     }
     prev_t = t;
   }
@@ -331,7 +341,7 @@ struct RunArgs {
   const uint32_t* vals0;  // row-0 sorted vals (slim cells)
   int kb;
   uint32_t n;
-  const uint2* links;      // {prev op, next op} per (t, row)
+  const uint2* links;      // {rank in cell, prev op} per (t, row)
   const uint32_t* obs;     // SF1: post-insert own fat count per (t, row); null otherwise
   KeySrc keys;
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
@@ -339,6 +349,8 @@ struct RunArgs {
   uint32_t* headflag;      // [t]
   uint32_t* head_e0;       // [t]
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
+  uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
+  uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
   Ctl* ctl;
 };
 
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const bool valid = t < tstar;
     uint32_t prev[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) prev[i] = a.links[(size_t)t * D + i].x;
+    for (int i = 0; i < D; ++i) prev[i] = a.links[(size_t)t * D + i].y;
     bool cont = valid && prev[0] != NONE32;
 #pragma unroll
     for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
@@ -372,6 +384,8 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
       if ((threadIdx.x & 31) == 0) a.delbits[e >> 5] = bits;
     }
     const bool head = valid && !cont;
+    a.bnd[e] = (valid && cont) ? 0u : 1u;
+    a.isdel[e] = op;
     a.headflag[t] = head ? 1u : 0u;
     a.head_e0[t] = e;
     if (valid && op == 0) ++ins;
@@ -381,303 +395,380 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
   if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&a.ctl->n_ins, (unsigned long long)ins);
 }
 
-// Run records, indexed by run id (= rank of the head in stream order):
-// e0/info/t, the d slim cells, the successor run on each cell (the run that
-// holds the next op on that cell), and the dependency count (cells whose
-// head op has a predecessor). Runs with no dependency are queued.
+// Run records, indexed by run id (= rank of the head in stream order): where
+// the run starts in row-0 order, its length (+ a has-delete bit), its d slim
+// cells, the head's rank in each cell (the cell's sequence number the run
+// must wait for) and, for SFF, the key's own slot count before the run (A)
+// and the maximum of the other slots of the bucket (O) in every row.
+template <int D>
+struct RunRec {
+  uint32_t e0, info;
+  uint32_t bits0;  // SFF: delete flags of the run's first 32 ops
+  uint32_t cells[D];
+  uint32_t rank[D];
+  uint32_t A[D];
+  uint32_t O[D];
+};
+
 template <int D>
 struct BuildArgs {
   const uint32_t* headflag;
   const uint32_t* ridx;
   const uint32_t* head_e0;
   const uint8_t* opflags;
-  const uint32_t* vals0;
+  const uint32_t* bidx;     // exclusive prefix count of boundaries (row-0 order)
+  const uint32_t* bpos;     // position of the k-th boundary; bpos[K] = n
+  const uint32_t* delpre;   // exclusive prefix count of deletes, n + 1 entries
+  const uint32_t* delbits;  // SFF
+  const uint2* obs2;        // SFF
   const uint2* links;
-  int kb;
   uint32_t n;
   KeySrc keys;
   Seeds<D> seeds;
   Mod wm;
   uint32_t w;
-  uint32_t* run_e0;
-  uint32_t* run_info;
-  uint32_t* run_t;
-  uint32_t* run_cells;
-  uint32_t* run_succ;
-  uint32_t* run_dep;
-  uint32_t* queue;
+  RunRec<D>* recs;
   Ctl* ctl;
 };
 
+__global__ void boundary_pos_k(const uint32_t* __restrict__ bnd, const uint32_t* __restrict__ bidx, uint32_t n,
+                               uint32_t* __restrict__ bpos) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    if (bnd[e]) bpos[bidx[e]] = e;
+    if (e == n - 1) bpos[bidx[e] + bnd[e]] = n;
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
-  const uint32_t tstar = a.ctl->fail_t;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
     if (t == a.n - 1) a.ctl->n_runs = a.ridx[t] + a.headflag[t];
-    bool ready = false;
-    uint32_t r = 0;
-    if (a.headflag[t]) {
-      r = a.ridx[t];
-      const uint32_t e0 = a.head_e0[t];
-      uint32_t hasdel = a.opflags[e0] & 1u;
-      uint32_t L = 1;
-      for (uint32_t e = e0 + 1; e < a.n; ++e) {
-        const uint8_t f = a.opflags[e];
-        if ((f & 6u) != 6u) break;
-        hasdel |= f & 1u;
-        ++L;
-      }
-      const uint32_t t_last = a.vals0[e0 + L - 1] >> (a.kb + 1);
-      const uint64_t key = load_key(a.keys, t);
-      uint32_t dep = 0;
+    if (!a.headflag[t]) continue;
+    const uint32_t r = a.ridx[t];
+    const uint32_t e0 = a.head_e0[t];
+    // the run ends at the next boundary (row-0 order)
+    const uint32_t e_end = a.bpos[a.bidx[e0] + 1];
+    const uint32_t L = e_end - e0;
+    const uint32_t hasdel = a.delpre[e_end] != a.delpre[e0];
+    RunRec<D> rec;
+    rec.e0 = e0;
+    rec.info = L | (hasdel << 31);
+    rec.bits0 = 0;
+    if (a.delbits && hasdel) {
+      const uint32_t sh = e0 & 31u;
+      uint32_t b = a.delbits[e0 >> 5] >> sh;
+      if (sh) b |= a.delbits[(e0 >> 5) + 1] << (32u - sh);
+      rec.bits0 = L >= 32 ? b : (b & ((1u << L) - 1u));
+    }
+    const uint64_t key = load_key(a.keys, t);
+    const bool head_del = a.opflags[e0] & 1u;
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        a.run_cells[(size_t)r * D + i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
-        dep += a.links[(size_t)t * D + i].x != NONE32;
-        const uint32_t s = a.links[(size_t)t_last * D + i].y;
-        a.run_succ[(size_t)r * D + i] = (s != NONE32 && s < tstar) ? a.ridx[s] : NONE32;
+    for (int i = 0; i < D; ++i) {
+      rec.cells[i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+      rec.rank[i] = a.links[(size_t)t * D + i].x;
+      if (a.obs2) {
+        const uint2 ob = a.obs2[(size_t)t * D + i];
+        rec.A[i] = head_del ? ob.x + 1u : ob.x - 1u;
+        rec.O[i] = ob.y;
+      } else {
+        rec.A[i] = 0;
+        rec.O[i] = 0;
       }
-      a.run_e0[r] = e0;
-      a.run_info[r] = L | (hasdel << 31);
-      a.run_t[r] = t;
-      a.run_dep[r] = dep;
-      ready = dep == 0;
     }
-    // queue the runs that are ready from the start (warp-aggregated push)
-    const unsigned am = __activemask();
-    const unsigned m = __ballot_sync(am, ready);
-    if (m) {
-      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&a.ctl->qtail, (uint32_t)__popc(m));
-      base = __shfl_sync(am, base, leader);
-      if (ready) a.queue[base + __popc(m & lanemask_lt())] = r;
-    }
+    a.recs[r] = rec;
   }
 }
 
 // ---------------------------------------------------------------- 5. engine
-__device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
+__device__ unsigned long long g_engine_stats[8];
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 template <int D>
 struct EngineArgs {
-  uint32_t* slim;
-  const uint32_t* run_e0;
-  const uint32_t* run_info;
-  const uint32_t* run_t;
-  const uint32_t* run_cells;
-  const uint32_t* run_succ;
-  uint32_t* run_dep;
-  uint32_t* queue;
-  const uint32_t* opdata;   // SF1: b_min per op (row-0 order)
-  const uint2* obs2;        // SFF: {own count after the op, max of the other slots} per (t, row)
-  const uint32_t* delbits;  // SFF: delete flags in row-0 order, one bit per op
+  unsigned long long* slim64;  // (seq << 32 | value) per slim cell
+  const RunRec<D>* recs;
+  const uint32_t* opdata;      // SF1: b_min per op (row-0 order)
+  const uint32_t* delbits;     // SFF: delete flags in row-0 order, one bit per op
   Ctl* ctl;
-  unsigned long long* inc;  // int64[d] tallies (two's complement add)
+  unsigned long long* inc;     // int64[d] tallies (two's complement add)
 };
 
-// Replay one run on its d slim cells (registers c[], tallies raised[]).
-// MODE 0: SF1 (raise gated by b_min; runs are insert-only)
-// MODE 1: CU (every insert raises; saturation ruled out by the host precheck)
-// MODE 2: SFF. Within a run no other op touches the key's d buckets, so in
-//         row i the key's own slot count is A_i + x (x = the run's net
-//         inserts so far) and the other slots keep their maximum O_i. Every
-//         per-op observation follows from (A_i, O_i, x): an insert's b_min is
-//         min_i A_i + x, a delete clamps row i to max(A_i + x, O_i). The run
-//         replays from one delete-bit per op; insert stretches collapse in
-//         closed form (b_min rises by exactly one per insert).
-template <int D, int MODE>
-__device__ __forceinline__ void replay_run(const EngineArgs<D>& a, uint32_t e0, uint32_t info, uint32_t th,
-                                           uint32_t (&c)[D], uint32_t (&raised)[D]) {
-  const uint32_t L = info & 0x7fffffffu;
-  uint32_t m0 = c[0];
+// ops one lane replays per engine iteration before it yields, so a long run
+// never stalls the other lanes of its warp
+constexpr uint32_t REPLAY_BUDGET = 1024;
+
+// Replay position inside the run a lane executes (SFF runs may span several
+// engine iterations).
+struct Cursor {
+  uint32_t m, x, e, rem, A0;
+  uint32_t wi, w0, w1, w2, w3;  // delete-bit prefetch ring for the word-aligned part
+  bool ring;
+};
+
+template <int D>
+__device__ __forceinline__ void raise_to(uint32_t tgt, uint32_t (&c)[D], uint32_t (&raised)[D]) {
 #pragma unroll
-  for (int i = 1; i < D; ++i) m0 = min(m0, c[i]);
-  if (MODE == 1) {
-    const uint64_t tgt = (uint64_t)m0 + L;
+  for (int i = 0; i < D; ++i)
+    if (c[i] < tgt) { raised[i] += tgt - c[i]; c[i] = tgt; }
+}
+
+// SFF: replay `avail` ops of a run whose delete flags are the low bits of
+// `bits`. Within a run no other op touches the key's d buckets, so in row i
+// the key's own slot count is A_i + x (x = the run's net inserts so far) and
+// the other slots keep their maximum O_i: an insert's b_min is min_i A_i + x
+// and a delete clamps row i to max(A_i + x, O_i).
+template <int D>
+__device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const uint32_t (&A)[D],
+                                            const uint32_t (&O)[D], uint32_t A0, uint32_t& m, uint32_t& x,
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3]) {
+  const uint32_t nd = __popc(bits), ni = avail - nd;
+  // Gap word: the min lags the key's own count by at least the word's
+  // deletes (mu = m - x, mu + nd <= A0). Every insert passes the gate and
+  // deletes only shrink caps that stay above every row (c_i + nd <= A_i + x),
+  // so a row's offset v = c_i - m drops by one per insert down to 0, each
+  // insert at v = 0 being one raise.
+  {
+    bool gap = (uint64_t)m + nd <= (uint64_t)(uint32_t)(A0 + x);
 #pragma unroll
     for (int i = 0; i < D; ++i)
-      if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
-  } else if (MODE == 0) {
-    // b_min strictly increases along a same-key insert run: the first k
-    // with b_k > m0 raises, and so does every later op
-    uint32_t k = 0;
-    while (k < L && a.opdata[e0 + k] <= m0) ++k;
-    const uint32_t s = L - k;
-    if (s) {
-      const uint64_t tgt = (uint64_t)m0 + s;
+      gap = gap && (int64_t)O[i] <= (int64_t)(uint32_t)(A[i] + x) - (int64_t)nd &&
+            (uint64_t)c[i] + nd <= (uint64_t)(uint32_t)(A[i] + x);
+    if (gap) {
 #pragma unroll
-      for (int i = 0; i < D; ++i)
-        if ((uint64_t)c[i] < tgt) { raised[i] += (uint32_t)(tgt - c[i]); c[i] = (uint32_t)tgt; }
+      for (int i = 0; i < D; ++i) {
+        const uint32_t v = c[i] - m;
+        raised[i] += ni > v ? ni - v : 0u;
+        c[i] = m + ni + (v > ni ? v - ni : 0u);
+      }
+      m += ni;
+      x += ni - nd;
+      ++ws[0];
+      return;
     }
-  } else {
-    const bool head_del = (a.delbits[e0 >> 5] >> (e0 & 31)) & 1u;
-    uint32_t A[D], O[D];
-    uint32_t A0 = U32MAX;
+  }
+  // Steady word: the min is caught up (m == A0 + x, so it stays A0 + x) and
+  // no other slot can exceed the key's own count within the word. Rows then
+  // evolve independently: with v_i = c_i - m an insert maps v -> max(v-1, 0)
+  // (a push at 0 is one raise) and a delete v -> min(v+1, A_i - A0). With the
+  // upper bound out of reach, v_end = max(v + S, max suffix sum) (Lindley)
+  // and the pushes are v_end - (v + S).
+  {
+    bool steady = avail >= 8u && m == A0 + x;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      const uint2 ob = a.obs2[(size_t)th * D + i];
-      A[i] = head_del ? ob.x + 1u : ob.x - 1u;
-      O[i] = ob.y;
-      A0 = min(A0, A[i]);
+      const uint32_t v = c[i] - m, W = A[i] - A0;
+      steady = steady && (int64_t)O[i] <= (int64_t)(uint32_t)(A[i] + x) - (int64_t)nd &&
+               ((uint64_t)v + nd <= (uint64_t)W || (W == 0 && v == 0));
     }
-    uint32_t m = m0, x = 0;  // x: net inserts (mod 2^32; every A_i + x is a true count)
-    uint32_t e = e0, rem = L;
-    uint32_t word = a.delbits[e >> 5];
-    while (rem) {
-      const uint32_t off = e & 31u;
-      const uint32_t avail = min(32u - off, rem);
-      const uint32_t bits = (word >> off) & (avail == 32u ? 0xffffffffu : ((1u << avail) - 1u));
-      if (avail < rem) word = a.delbits[(e >> 5) + 1];  // prefetch the next word
-      uint32_t pos = 0;
-      while (pos < avail) {
-        const uint32_t rest = bits >> pos;
-        const uint32_t s = min(rest ? (uint32_t)(__ffs(rest) - 1) : 32u, avail - pos);
-        if (s) {
-          // k-th insert of the stretch raises iff m < A0 + x + k; once one
-          // raises, all later ones do
-          const int64_t diff = (int64_t)m - (int64_t)(uint32_t)(A0 + x);
-          const int64_t kstar = diff + 1 > 1 ? diff + 1 : 1;
-          if (kstar <= (int64_t)s) {
-            m += (uint32_t)((int64_t)s - kstar + 1);
+    if (steady) {
+      int32_t msuf = 0;
+      for (uint32_t k = 0; k < avail; ++k) msuf = max(msuf, 2 * __popc(bits >> k) - (int32_t)(avail - k));
+      const int32_t S = (int32_t)nd - (int32_t)ni;
+      const uint32_t mnew = m + ni - nd;
 #pragma unroll
-            for (int i = 0; i < D; ++i)
-              if (c[i] < m) { raised[i] += m - c[i]; c[i] = m; }
-          }
-          x += s;
-          pos += s;
+      for (int i = 0; i < D; ++i) {
+        const uint32_t v = c[i] - m;
+        uint32_t vend, push;
+        if ((uint64_t)v + nd <= (uint64_t)(A[i] - A0)) {
+          vend = (uint32_t)max((int64_t)v + S, (int64_t)msuf);
+          push = (uint32_t)((int64_t)vend - ((int64_t)v + S));
+        } else {  // W == 0, v == 0: the row sits on both bounds
+          vend = 0;
+          push = ni;
         }
-        if (pos < avail) {  // a delete
-          x -= 1u;
-          m = U32MAX;
-#pragma unroll
-          for (int i = 0; i < D; ++i) {
-            c[i] = min(c[i], max(A[i] + x, O[i]));
-            m = min(m, c[i]);
-          }
-          pos += 1;
-        }
+        raised[i] += push;
+        c[i] = mnew + vend;
       }
-      e += avail;
-      rem -= avail;
+      m = mnew;
+      x += ni - nd;
+      ++ws[1];
+      return;
+    }
+  }
+  // general word: op by op, insert stretches in closed form (b_min rises by
+  // exactly one per insert, so once one raises all later ones do)
+  ++ws[2];
+  uint32_t pos = 0;
+  while (pos < avail) {
+    const uint32_t rest = bits >> pos;
+    const uint32_t s = min(rest ? (uint32_t)(__ffs(rest) - 1) : 32u, avail - pos);
+    if (s) {
+      const int64_t diff = (int64_t)m - (int64_t)(uint32_t)(A0 + x);
+      const int64_t kstar = diff + 1 > 1 ? diff + 1 : 1;
+      if (kstar <= (int64_t)s) {
+        m += (uint32_t)((int64_t)s - kstar + 1);
+        raise_to<D>(m, c, raised);
+      }
+      x += s;
+      pos += s;
+    }
+    if (pos < avail) {  // a delete
+      x -= 1u;
+      m = U32MAX;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        c[i] = min(c[i], max(A[i] + x, O[i]));
+        m = min(m, c[i]);
+      }
+      pos += 1;
     }
   }
 }
 
-// Dataflow engine over the run DAG. A run executes exactly once, after every
-// run holding an earlier op on one of its cells finished: each finishing run
-// decrements its successors' dependency counters (acq_rel) and the lane that
-// releases the last dependency runs that successor directly (further newly
-// ready runs go to a global queue that idle lanes pop). No lane ever waits
-// while holding a run, so the engine cannot deadlock; it ends when every run
-// has executed.
+// Advance the run a lane executes; true once it is complete.
+// MODE 0: SF1 (insert-only runs; b_min strictly increases along a same-key
+//         run, so the first op with b_k > m0 raises and so does every later)
+// MODE 1: CU (every insert raises; saturation ruled out by the host precheck)
+// MODE 2: SFF (see replay_word)
 template <int D, int MODE>
-__global__ void __launch_bounds__(256) dag_engine_k(EngineArgs<D> a) {
-  __shared__ uint32_t blk_pending;  // completions not yet published to ctl->executed
-  __shared__ volatile int blk_exit;
-  if (threadIdx.x == 0) {
-    blk_pending = 0;
-    blk_exit = 0;
+__device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, uint32_t e0, uint32_t info,
+                                            uint32_t bits0, const uint32_t (&A)[D], const uint32_t (&O)[D],
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3]) {
+  const uint32_t L = info & 0x7fffffffu;
+  if (MODE == 1) {
+    raise_to<D>(k.m + L, c, raised);  // m0 + L fits: the precheck bounds every counter
+    return true;
   }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (MODE == 0) {
+    uint32_t j = 0;
+    while (j < L && a.opdata[e0 + j] <= k.m) ++j;
+    if (L - j) raise_to<D>(k.m + (L - j), c, raised);
+    return true;
+  }
+  if (!(info >> 31)) {  // insert-only SFF run: the j-th insert raises iff m0 < A0 + j
+    const int64_t jstar = max((int64_t)k.m - (int64_t)k.A0 + 1, (int64_t)1);
+    if (jstar <= (int64_t)L) raise_to<D>(k.m + (uint32_t)((int64_t)L - jstar + 1), c, raised);
+    return true;
+  }
+  const uint32_t wlast = (e0 + L - 1) >> 5;
+  uint32_t budget = REPLAY_BUDGET;
+  while (k.rem && budget) {
+    uint32_t bits, avail;
+    const uint32_t done = k.e - e0;
+    if (done < 32u) {
+      avail = min(32u - done, k.rem);
+      bits = bits0 >> done;
+    } else {
+      if (!k.ring) {
+        k.wi = k.e >> 5;
+        k.w0 = a.delbits[k.wi];
+        k.w1 = k.wi + 1 <= wlast ? a.delbits[k.wi + 1] : 0u;
+        k.w2 = k.wi + 2 <= wlast ? a.delbits[k.wi + 2] : 0u;
+        k.w3 = k.wi + 3 <= wlast ? a.delbits[k.wi + 3] : 0u;
+        k.ring = true;
+      }
+      const uint32_t off = k.e & 31u;
+      avail = min(32u - off, k.rem);
+      bits = k.w0 >> off;
+      k.w0 = k.w1;
+      k.w1 = k.w2;
+      k.w2 = k.w3;
+      k.w3 = k.wi + 4 <= wlast ? a.delbits[k.wi + 4] : 0u;
+      ++k.wi;
+    }
+    if (avail < 32u) bits &= (1u << avail) - 1u;
+    replay_word<D>(bits, avail, A, O, k.A0, k.m, k.x, c, raised, ws);
+    k.e += avail;
+    k.rem -= avail;
+    budget = budget > avail ? budget - avail : 0u;
+  }
+  return k.rem == 0;
+}
+
+// Ordered engine over runs. Each slim cell is one 64-bit word
+// (seq << 32 | value); a run whose head has rank r_i in cell i may execute
+// once seq_i == r_i in all its cells, and publishes (r_i + L, value) with a
+// single store per cell, so one load both signals readiness and delivers the
+// value. Lanes claim runs in stream order of their heads (warp-aggregated
+// ticket), so the earliest unfinished run is always ready and the engine
+// cannot deadlock. A waiting lane polls only its cells that are not ready
+// yet (a ready cell stays ready: nobody else writes it before this run); a
+// long run is replayed REPLAY_BUDGET ops per iteration.
+template <int D, int MODE>
+__global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
+  const uint32_t lane = lane_id();
   const uint32_t R = a.ctl->n_runs;
-  uint32_t cur = NONE32, slot = NONE32, done_local = 0, backoff = 0, idle_iters = 0;
-  uint32_t raised[D];
+  bool has = false, exhausted = false;
+  uint32_t cells[D], rank[D], A[D], O[D], c[D], raised[D];
+  uint32_t e0 = 0, info = 0, bits0 = 0, pend = 0;  // pend: bit i = cell i not seen ready yet
 #pragma unroll
-  for (int i = 0; i < D; ++i) raised[i] = 0;
+  for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0, A[i] = 0, O[i] = 0, c[i] = 0;
+  Cursor k{};
+  uint32_t idle = 0;
+  uint32_t ws[3] = {0, 0, 0};
+  unsigned long long st_cyc = 0, st_runs = 0, st_iters = 0;
   while (true) {
-    const unsigned need = __ballot_sync(0xffffffffu, cur == NONE32 && slot == NONE32);
+    ++st_iters;
+    const unsigned need = __ballot_sync(0xffffffffu, !has && !exhausted);
     if (need) {
       const int leader = __ffs(need) - 1;
       uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&a.ctl->qhead, (uint32_t)__popc(need));
+      if ((int)lane == leader) base = atomicAdd(&a.ctl->qhead, (uint32_t)__popc(need));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (cur == NONE32 && slot == NONE32) slot = base + __popc(need & lanemask_lt());
-    }
-    if (cur == NONE32 && slot < R) {
-      const uint32_t v = ld_relaxed_u32(a.queue + slot);
-      if (v != NONE32) {
-        fence_acq_rel_gpu();  // acquire: the pusher's release pattern covers the run's inputs
-        cur = v;
-        slot = NONE32;
+      if (!has && !exhausted) {
+        const uint32_t r = base + __popc(need & lanemask_lt());
+        if (r < R) {
+          const RunRec<D>& rec = a.recs[r];
+          e0 = rec.e0;
+          info = rec.info;
+          bits0 = rec.bits0;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            cells[i] = rec.cells[i];
+            rank[i] = rec.rank[i];
+            if (MODE == 2) A[i] = rec.A[i], O[i] = rec.O[i];
+          }
+          pend = (1u << D) - 1u;
+          has = true;
+        } else {
+          exhausted = true;
+        }
       }
     }
-    const bool busy = cur != NONE32;
-    if (busy) {
-      const uint32_t r = cur;
-      const uint32_t e0 = a.run_e0[r], info = a.run_info[r], th = a.run_t[r];
-      uint32_t cells[D], succ[D], c[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        cells[i] = a.run_cells[(size_t)r * D + i];
-        succ[i] = a.run_succ[(size_t)r * D + i];
-      }
-#pragma unroll
-      for (int i = 0; i < D; ++i) c[i] = ld_relaxed_u32(a.slim + cells[i]);
-      replay_run<D, MODE>(a, e0, info, th, c, raised);
-#pragma unroll
-      for (int i = 0; i < D; ++i) st_relaxed_u32(a.slim + cells[i], c[i]);
-      fence_acq_rel_gpu();  // release the cell values before the dependency decrements
-      uint32_t ready[D];
-      int nready = 0;
+    if (__all_sync(0xffffffffu, !has)) break;  // no lane holds a run and none can get one
+    bool progressed = false;
+    if (has && pend) {
+      unsigned long long wv[D];
 #pragma unroll
       for (int i = 0; i < D; ++i)
-        if (succ[i] != NONE32 && atom_add_relaxed(a.run_dep + succ[i], 0xFFFFFFFFu) == 1u) ready[nready++] = succ[i];
-      uint32_t next = NONE32;
-      if (nready) {
-        fence_acq_rel_gpu();  // acquire the other producers' cells; release for the pushes
-        next = ready[0];
-        for (int k = 1; k < nready; ++k) {
-          const uint32_t q = atomicAdd(&a.ctl->qtail, 1u);
-          st_relaxed_u32(a.queue + q, ready[k]);
+        if (pend & (1u << i)) wv[i] = ld_relaxed_u64(a.slim64 + cells[i]);
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+        if ((pend & (1u << i)) && (uint32_t)(wv[i] >> 32) == rank[i]) {
+          c[i] = (uint32_t)wv[i];
+          pend &= ~(1u << i);
         }
+      if (!pend) {  // all cells acquired: start the replay
+        k.m = c[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) k.m = min(k.m, c[i]);
+        k.A0 = A[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) k.A0 = min(k.A0, A[i]);
+        k.x = 0;
+        k.e = e0;
+        k.rem = info & 0x7fffffffu;
+        k.ring = false;
       }
-      ++done_local;
-      cur = next;
     }
-    if (!__any_sync(0xffffffffu, busy)) {
-      // idle warp: publish completions to the block, warp 0 moves them to the
-      // global count now and then and raises the block's exit flag at the end
-      uint32_t dsum = done_local;
-      for (int off = 16; off > 0; off >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, off);
-      done_local = 0;
-      if (lane == 0 && dsum) atomicAdd(&blk_pending, dsum);
-      if (wid == 0 && (++idle_iters & 7u) == 0) {
-        uint32_t ex = 0;
-        if (lane == 0) {
-          const uint32_t p = atomicExch(&blk_pending, 0u);
-          ex = p ? atomicAdd(&a.ctl->executed, p) + p : ld_relaxed_u32(&a.ctl->executed);
-          if (ex >= R) blk_exit = 1;
-        }
+    if (has && !pend) {
+      const long long t0 = clock64();
+      const bool done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws);
+      st_cyc += clock64() - t0;
+      if (done) {
+        const uint32_t L = info & 0x7fffffffu;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
+        has = false;
+        ++st_runs;
       }
-      __syncwarp();
-      if (blk_exit) break;
-      if (backoff) __nanosleep(backoff);
-      backoff = min(backoff * 2 + 16, 256u);
-    } else {
-      backoff = 0;
+      progressed = true;
+    }
+    if (__any_sync(0xffffffffu, progressed)) {
+      idle = 0;
+    } else if (++idle > 4) {
+      __nanosleep(min(idle * 8u, 128u));
     }
   }
 #pragma unroll
@@ -686,6 +777,22 @@ __global__ void __launch_bounds__(256) dag_engine_k(EngineArgs<D> a) {
     for (int off = 16; off > 0; off >>= 1) r += __shfl_down_sync(0xffffffffu, r, off);
     if (lane == 0 && r) atomicAdd(a.inc + i, r);
   }
+  // diagnostics (sfk_engine_stats): words by replay path, replay cycles, runs, warp iterations
+  unsigned long long sv[6] = {ws[0], ws[1], ws[2], (unsigned long long)st_cyc, st_runs, lane == 0 ? st_iters : 0ull};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    unsigned long long v = sv[q];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0 && v) atomicAdd(&g_engine_stats[q], v);
+  }
+}
+
+__global__ void pack_slim_k(const uint32_t* __restrict__ slim, unsigned long long* __restrict__ s64, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) s64[c] = slim[c];
+}
+__global__ void unpack_slim_k(const unsigned long long* __restrict__ s64, uint32_t* __restrict__ slim, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
+    slim[c] = (uint32_t)s64[c];
 }
 
 __global__ void ctl_init_k(Ctl* ctl) {
@@ -860,10 +967,12 @@ struct Layout {
   uint8_t* opflags;
   uint32_t* opdata;
   uint32_t* headflag;
+  uint32_t *bnd, *bidx, *bpos, *isdel, *delpre;
   uint32_t* head_e0;
   uint32_t* ridx;
   uint32_t *run_e0, *run_info, *run_t;
-  uint32_t *run_cells, *run_succ, *run_dep, *queue;
+  void* recs;
+  unsigned long long* slim64;
   Ctl* ctl;
   Stats* stats;
   size_t total;
@@ -881,7 +990,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.v_in = cv.take<uint32_t>(N);
   L.k_out = cv.take<uint32_t>(N);
   L.v_out = cv.take<uint32_t>(N);
-  L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n));
+  L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n + 1));
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
@@ -899,18 +1008,30 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
   L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);
   L.headflag = cv.take<uint32_t>(engine ? n : 1);
+  L.bnd = cv.take<uint32_t>(engine ? n + 1 : 1);
+  L.bidx = cv.take<uint32_t>(engine ? n + 1 : 1);
+  L.bpos = cv.take<uint32_t>(engine ? n + 2 : 1);
+  L.isdel = cv.take<uint32_t>(engine ? n + 1 : 1);
+  L.delpre = cv.take<uint32_t>(engine ? n + 1 : 1);
   L.head_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
   L.run_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.run_info = cv.take<uint32_t>(engine ? n : 1);
   L.run_t = cv.take<uint32_t>(engine ? n : 1);
-  L.run_cells = cv.take<uint32_t>(engine ? N : 1);
-  L.run_succ = cv.take<uint32_t>(engine ? N : 1);
-  L.run_dep = cv.take<uint32_t>(engine ? n : 1);
-  L.queue = cv.take<uint32_t>(engine ? n : 1);
+  L.recs = cv.take<char>(engine ? (uint64_t)n * (12 + 16 * (uint64_t)d) : 1);
+  L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
   L.total = cv.off + 256;
   L.ok = cv.ok;
   return L;
+}
+
+int engine_stats(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_engine_stats, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_engine_stats, z, sizeof(z));
+  }
+  return (int)e;
 }
 
 size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
@@ -999,58 +1120,52 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.headflag = L.headflag;
   ra.head_e0 = L.head_e0;
   ra.delbits = MODE == 2 ? L.delbits : nullptr;
+  ra.bnd = L.bnd;
+  ra.isdel = L.isdel;
   ra.ctl = L.ctl;
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.headflag, L.ridx, (int)n, st);
+  // run extents: boundaries (row-0 order) and delete prefix counts
+  cudaMemsetAsync(L.isdel + n, 0, 4, st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.bnd, L.bidx, (int)n, st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.isdel, L.delpre, (int)n + 1, st);
   if (e != cudaSuccess) {
     set_error("run scan: %s", cudaGetErrorString(e));
     return (int)e;
   }
-  cudaMemsetAsync(L.queue, 0xFF, (size_t)n * 4, st);
+  { note_launch(); boundary_pos_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.bnd, L.bidx, n, L.bpos); }
   BuildArgs<D> ba;
   ba.headflag = L.headflag;
   ba.ridx = L.ridx;
   ba.head_e0 = L.head_e0;
   ba.opflags = L.opflags;
-  ba.vals0 = L.v_out;
+  ba.bidx = L.bidx;
+  ba.bpos = L.bpos;
+  ba.delpre = L.delpre;
+  ba.delbits = MODE == 2 ? L.delbits : nullptr;
+  ba.obs2 = MODE == 2 ? L.obs2 : nullptr;
   ba.links = L.links;
-  ba.kb = kb;
   ba.n = n;
   ba.keys = ks;
   for (int i = 0; i < D; ++i) ba.seeds.s[i] = slim_seeds[i];
   ba.wm = make_mod((uint64_t)w);
   ba.w = (uint32_t)w;
-  ba.run_e0 = L.run_e0;
-  ba.run_info = L.run_info;
-  ba.run_t = L.run_t;
-  ba.run_cells = L.run_cells;
-  ba.run_succ = L.run_succ;
-  ba.run_dep = L.run_dep;
-  ba.queue = L.queue;
+  ba.recs = static_cast<RunRec<D>*>(L.recs);
   ba.ctl = L.ctl;
   { note_launch(); runs_build_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ba); }
+  const uint32_t cells = (uint32_t)(D * w);
+  { note_launch(); pack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(slim, L.slim64, cells); }
   EngineArgs<D> ea;
-  ea.slim = slim;
-  ea.run_e0 = L.run_e0;
-  ea.run_info = L.run_info;
-  ea.run_t = L.run_t;
-  ea.run_cells = L.run_cells;
-  ea.run_succ = L.run_succ;
-  ea.run_dep = L.run_dep;
-  ea.queue = L.queue;
+  ea.slim64 = L.slim64;
+  ea.recs = static_cast<const RunRec<D>*>(L.recs);
   ea.opdata = L.opdata;
-  ea.obs2 = L.obs2;
   ea.delbits = L.delbits;
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
-  static int occ = -1;
-  if (occ < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dag_engine_k<D, MODE>, 256, 0);
-    if (occ < 1) occ = 1;
-  }
-  { note_launch(); dag_engine_k<D, MODE><<<sms * std::min(occ, 4), 256, 0, st>>>(ea); }
-  return check_launch("dag_engine");
+  { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea); }
+  { note_launch(); unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells); }
+  return check_launch("poll_engine");
 }
 
 template <int D>

@@ -39,3 +39,8 @@ for r in range(reps):
     sk.apply_ops(ops_d, keys_d)
     torch.cuda.synchronize()
     print(f"{kind} alpha={alpha} rep {r}: {(time.perf_counter() - t0) * 1e3:.2f} ms for {len(c['ops'])} ops", flush=True)
+import ctypes  # noqa: E402
+from paper_1701_04148_b200 import _lib  # noqa: E402
+st = (ctypes.c_ulonglong * 8)()
+_lib.load_library().sfk_engine_stats(st, 1)
+print("engine stats (all reps): gap_words=%d steady_words=%d slow_words=%d replay_cycles=%d runs=%d warp_iters=%d" % tuple(st[:6]))
