@@ -23,6 +23,7 @@ queries on all host threads, extrapolated from a bounded sample.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -44,7 +45,7 @@ D, W, Z = 4, 65536, 4
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--queries", type=int, default=1_000_000_000)
@@ -232,9 +233,11 @@ def run_ours(args):
 
     def step():
         ev[0].record()
+        eng = 0.0
         if rank == 0:
             reset()
             sk.apply_ops(ops_d, keys_d)
+            eng = float(L.sfk_engine_last_ms())
         ev[1].record()
         if world > 1:
             sk.broadcast_slim_(src=0)
@@ -244,8 +247,12 @@ def run_ours(args):
         _lib.check(rc, "sfk_min_query")
         ev[3].record()
         torch.cuda.synchronize()
-        return [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+        return [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]), eng]
 
+    # nvidia-smi needs ~0.5 s to start sampling: start it before the warm-up
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(1.0)
     for _ in range(args.warmup):
         step()
         flush.fill_(1)
@@ -253,9 +260,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
     launches0 = L.sfk_launch_count()
+    L.sfk_engine_timing(1)
+    est0 = (ctypes.c_ulonglong * 8)()
+    L.sfk_engine_stats(est0, 1)
     phases = []
     for _ in range(args.steps):
         phases.append(step())
@@ -264,9 +272,12 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     launches = L.sfk_launch_count() - launches0
+    L.sfk_engine_timing(0)
+    est = (ctypes.c_ulonglong * 8)()
+    L.sfk_engine_stats(est, 1)
     clk = clocks.stop()
-    tot = np.array(phases).sum(axis=0)  # build, bcast, query (ms over K steps)
-    step_ms_local = float(tot.sum()) / args.steps
+    tot = np.array(phases).sum(axis=0)  # build, bcast, query, engine kernel (ms over K steps)
+    step_ms_local = float(tot[:3].sum()) / args.steps
     t = torch.tensor([step_ms_local, tot[0] / args.steps, tot[1] / args.steps, tot[2] / args.steps],
                      dtype=torch.float64, device=dev)
     if world > 1:
@@ -276,19 +287,38 @@ def run_ours(args):
     value = items / (step_ms * 1e-3) / 1e6
 
     hbm, hbm_src, gather = measured_peaks()
-    # dominant kernel: the query kernel on this rank (CUDA events on its stream)
+    # per-kernel rooflines from CUDA events on the launching stream
     q_s = float(tot[2]) / args.steps * 1e-3
     achieved_gbs = qn * 12 / q_s / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
+    rf_query = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved_gbs / hbm, 4), "traffic": None,
-                "kernel": "min_query (fused key load + 4x hash + 4 gathers + min + int64 store)",
-                "algorithmic_bytes_per_query": 12, "peak_source": hbm_src}
+                "kernel": "min_query_l2 (fused key load + 4x hash + 4 gathers + min + int64 store)",
+                "algorithmic_bytes_per_launch": int(qn * 12), "launch_ms": round(q_s * 1e3, 3),
+                "peak_source": hbm_src}
     if gather:
         gpk = float(gather.get("gather_1MiB_Gps", 0.0))
         gachieved = qn * 4 / q_s / 1e9
-        roofline["gather"] = {"achieved_Gps": round(gachieved, 1), "peak_Gps": gpk,
+        rf_query["gather"] = {"achieved_Gps": round(gachieved, 1), "peak_Gps": gpk,
                               "frac": round(gachieved / gpk, 4) if gpk else None,
                               "peak_source": "profiles/gather_peaks.json (random 4-B loads, 1 MiB table, L2)"}
+    rf = {"query": rf_query}
+    eng_ms = float(tot[3]) / args.steps
+    if rank == 0 and eng_ms > 0:
+        runs = est[4] / args.steps
+        # per run: its record (12 + 16 d bytes) + d slim words read and written (8 B each); 1 bit per op
+        eng_bytes = runs * (12 + 16 * D + 16 * D) + n_ops / 8
+        ach = eng_bytes / (eng_ms * 1e-3) / 1e9
+        rf["engine"] = {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 5), "traffic": None,
+                        "kernel": "poll_engine_k<4,2> (ordered slim engine, SFF)",
+                        "algorithmic_bytes_per_launch": int(eng_bytes), "launch_ms": round(eng_ms, 3),
+                        "runs_per_launch": int(runs), "peak_source": hbm_src,
+                        "note": "latency-bound: runs wait on the slim cells their predecessors write; "
+                                "see DESIGN.md for the critical-path depth"}
+    dominant = "engine" if "engine" in rf and eng_ms > query_ms else "query"
+    roofline = dict(rf[dominant])
+    roofline["dominant"] = dominant
+    roofline["kernels"] = rf
 
     breakdown = {"build_ms": round(build_ms, 3), "bcast_ms": round(bcast_ms, 3), "query_ms": round(query_ms, 3),
                  "insert_Mitems_s": round(n_ops / (build_ms * 1e-3) / 1e6, 2) if build_ms else None,

@@ -77,6 +77,12 @@ unsigned long long sfk_launch_count(void);
  * replayed op by op, replay cycles, runs executed, warp iterations, 0, 0}. */
 int sfk_engine_stats(unsigned long long* out8, int reset);
 
+/* Bench instrumentation: when on, CUDA events bracket every launch of the
+ * ordered slim engine kernel; sfk_engine_last_ms() synchronises on the last
+ * one and returns its duration in ms (-1 if none was recorded). */
+int sfk_engine_timing(int on);
+float sfk_engine_last_ms(void);
+
 /* Workload utility (no reference counterpart; SURVEY.md §8(d) cfg 5): keys
  * t0 .. t0+n-1 of the counter-based query stream of
  * paper_1701_04148_b200.workloads.query_keys, generated on the device.

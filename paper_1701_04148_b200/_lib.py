@@ -38,6 +38,8 @@ EXPORTS = (
     "sfk_launch_count",
     "sfk_gen_query_keys",
     "sfk_engine_stats",
+    "sfk_engine_timing",
+    "sfk_engine_last_ms",
 )
 
 _lib = None
@@ -78,6 +80,8 @@ def load_library() -> ctypes.CDLL:
     L.sfk_oracle_slim_apply.argtypes = [P, P, I, I64, P, I, I, P, I64, P, P, P]
     L.sfk_launch_count.restype = ctypes.c_ulonglong
     L.sfk_engine_stats.argtypes = [P, I]
+    L.sfk_engine_timing.argtypes = [I]
+    L.sfk_engine_last_ms.restype = ctypes.c_float
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]
     _lib = L
     return L

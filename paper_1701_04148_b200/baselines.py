@@ -84,13 +84,9 @@ class CmSketch(_CounterSketch):
         """Merge stream-sharded replicas in place: counters and tallies are
         sums over shards (count-min updates commute). uint32 counters travel
         as int32; two's-complement sums wrap exactly like uint32 sums."""
-        import torch.distributed as dist
+        from .distributed import allreduce_counters_
 
-        dist.all_reduce(self.counters.view(torch.int32), op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(self.increment_counts, op=dist.ReduceOp.SUM, group=group)
-        seen = torch.tensor([self.insertions_seen], dtype=torch.int64, device=self.counters.device)
-        dist.all_reduce(seen, op=dist.ReduceOp.SUM, group=group)
-        self.insertions_seen = int(seen.item())
+        self.insertions_seen = allreduce_counters_(self.counters, self.increment_counts, self.insertions_seen, group)
 
 
 class CuSketch(_CounterSketch):

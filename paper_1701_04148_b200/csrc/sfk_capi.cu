@@ -55,6 +55,8 @@ int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint3
                      const int64_t* true_counts, int64_t n, int64_t* inc, int64_t* result, cudaStream_t st);
 size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n);
 int engine_stats(unsigned long long* out, int reset);
+int engine_timing(int on);
+float engine_last_ms();
 int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
                    int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
                    int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -136,6 +138,10 @@ int sfk_abi_version(void) { return 1; }
 unsigned long long sfk_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int sfk_engine_stats(unsigned long long* out8, int reset) { return engine_stats(out8, reset); }
+
+int sfk_engine_timing(int on) { return engine_timing(on); }
+
+float sfk_engine_last_ms(void) { return engine_last_ms(); }
 
 int sfk_gen_query_keys(uint64_t seed, const uint32_t* present, const uint32_t* sorted_present, uint32_t v,
                        const double* cdf, int64_t t0, int64_t n, uint32_t* out, void* stream) {

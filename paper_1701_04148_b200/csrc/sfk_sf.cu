@@ -1025,6 +1025,30 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   return L;
 }
 
+// optional CUDA-event timing of the engine kernel (bench instrumentation)
+static bool g_time_engine = false;
+static bool g_ev_pending = false;
+static cudaEvent_t g_ev[2];
+
+int engine_timing(int on) {
+  if (on && !g_time_engine) {
+    cudaEventCreate(&g_ev[0]);
+    cudaEventCreate(&g_ev[1]);
+  }
+  g_time_engine = on != 0;
+  g_ev_pending = false;
+  return 0;
+}
+
+// elapsed ms of the last timed engine launch (synchronises on it); -1 if none
+float engine_last_ms() {
+  if (!g_ev_pending) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(g_ev[1]) == cudaSuccess) cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]);
+  g_ev_pending = false;
+  return ms;
+}
+
 int engine_stats(unsigned long long* out, int reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_engine_stats, sizeof(unsigned long long) * 8);
   if (e == cudaSuccess && reset) {
@@ -1163,7 +1187,12 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.delbits = L.delbits;
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
+  if (g_time_engine) cudaEventRecord(g_ev[0], st);
   { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea); }
+  if (g_time_engine) {
+    cudaEventRecord(g_ev[1], st);
+    g_ev_pending = true;
+  }
   { note_launch(); unpack_slim_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.slim64, slim, cells); }
   return check_launch("poll_engine");
 }

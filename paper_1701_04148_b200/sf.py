@@ -285,6 +285,6 @@ class SfSketch:
     def broadcast_slim_(self, src: int = 0, group=None) -> None:
         """Replicate the query side from rank ``src`` (NCCL broadcast over
         NVLink; the uint32 counters travel as their int32 bit pattern)."""
-        import torch.distributed as dist
+        from .distributed import broadcast_counters_
 
-        dist.broadcast(self.slim.counters.view(torch.int32), src=src, group=group)
+        broadcast_counters_(self.slim.counters, src=src, group=group)

@@ -1,0 +1,193 @@
+"""GPU tests of the drop-in API surface: the reference's pinned
+micro-scenarios (tests/test_sf.py, test_baselines.py, test_serialize.py of the
+reference restated), error semantics, edge shapes (empty batches, d = 1 / 8 /
+9, z = 1 / 8, non-power-of-two widths, 64-bit / 32-bit / record keys), the
+export -> import -> collector round trip and the oracle-assisted mode, each
+checked against the CPU oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import apply_batches, assert_state_equal, host, make_sketch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1701_04148_b200 as P  # noqa: E402
+from paper_1701_04148_b200 import workloads as W  # noqa: E402
+from paper_1701_04148_b200.hashing import bucket_hash, derive_seeds, slot_hash  # noqa: E402
+
+ALL = ("sf1", "sf2", "sf3", "sf4", "sff")
+DELETING = ("sf2", "sf3", "sf4", "sff")
+
+
+@pytest.mark.parametrize("variant", ALL)
+def test_first_insert_sets_all_slim_counters(variant):
+    s = P.SfSketch(P.SketchParams(d=3, w=8, z=2), variant)
+    s.insert(42)
+    assert int(s.slim.counters.to(torch.int64).sum()) == 3
+    assert s.query(42) == 1 and s.query(7) == 0
+
+
+@pytest.mark.parametrize("variant", ALL)
+def test_single_item_counts_exactly(variant):
+    s = P.SfSketch(P.SketchParams(d=2, w=4, z=2), variant)
+    for _ in range(9):
+        s.insert(123)
+    assert s.query(123) == 9
+
+
+@pytest.mark.parametrize("variant", DELETING)
+def test_insert_then_delete_returns_to_zero(variant):
+    s = P.SfSketch(P.SketchParams(d=3, w=16, z=2), variant)
+    s.insert(77)
+    s.delete(77)
+    assert s.query(77) == 0
+    assert int(s.fat.counters.to(torch.int64).sum()) == 0
+
+
+def test_second_insert_skips_non_minimal_shared_counter():
+    d, w, z = 2, 8, 16
+    fam = derive_seeds(0, d)
+    e1 = 1
+    b1 = [bucket_hash(fam, i, e1, w) for i in range(d)]
+    e2 = next(c for c in range(2, 50000)
+              if bucket_hash(fam, 0, c, w) == b1[0] and bucket_hash(fam, 1, c, w) != b1[1]
+              and slot_hash(fam, 0, c, z) != slot_hash(fam, 0, e1, z))
+    s = P.SfSketch(P.SketchParams(d=d, w=w, z=z), "sff")
+    s.insert(e1)
+    s.insert(e2)
+    sl = host(s.slim.counters)
+    assert sl[0, b1[0]] == 1 and s.query(e1) == 1 and s.query(e2) == 1
+
+
+def test_error_semantics():
+    s = P.SfSketch(P.SketchParams(d=2, w=4), "sf1")
+    s.insert(5)
+    with pytest.raises(P.UnsupportedOperationError):
+        s.delete(5)
+    for v in DELETING:
+        with pytest.raises(P.PhantomDeletionError):
+            P.SfSketch(P.SketchParams(d=2, w=4, z=2), v).delete(5)
+    t = P.SfSketch(P.SketchParams(d=2, w=4, z=2), "sff")
+    t.fat.counters.fill_(0xFFFFFFFF)
+    with pytest.raises(P.SaturationError):
+        t.insert(1)
+    with pytest.raises(P.ConfigurationError):
+        P.SfSketch(P.SketchParams(d=2, w=4, z=2, w_prime=9), "sf3")
+    with pytest.raises(P.ConfigurationError):
+        s.apply_ops(np.array([0, 2], np.uint8), np.array([1, 2], np.uint64))
+    with pytest.raises(P.ConfigurationError):
+        s.apply_ops(np.array([0], np.uint8), np.array([1, 2], np.uint64))
+    with pytest.raises(P.UnsupportedOperationError):
+        P.CuSketch(P.SketchParams(d=2, w=4)).delete(3)
+
+
+def test_prefix_applied_and_seen_counted_on_abort(oracle):
+    ops = np.array([0, 0, 0, 1, 0], np.uint8)
+    keys = np.array([1, 2, 3, 99, 4], np.uint64)
+    s = P.SfSketch(P.SketchParams(d=2, w=8, z=2, master_seed=3), "sff")
+    with pytest.raises(P.PhantomDeletionError) as ei:
+        s.apply_ops(ops, keys)
+    assert "op 3" in str(ei.value) and "99" in str(ei.value)
+    assert s.slim.insertions_seen == 3
+    o = oracle.OracleSketch("sff", 2, 8, 2, None, 3)
+    o.apply_ops(ops, keys)
+    assert_state_equal(s, o.slim, o.inc, o.seen, o.fat)
+
+
+@pytest.mark.parametrize("kind", ["sff", "sf1", "cm", "cu", "sf4", "sf2", "sf3"])
+def test_empty_batch(kind):
+    sk = make_sketch(kind, 2, 8, 2, None, 0)
+    sk.apply_ops(np.zeros(0, np.uint8), np.zeros(0, np.uint64))
+    assert host(sk.query_many(np.zeros(0, np.uint64))).shape == (0,)
+
+
+@pytest.mark.parametrize("kind,d,w,z,wp", [
+    ("sff", 1, 64, 1, None), ("sff", 8, 128, 8, None), ("sff", 9, 32, 3, None), ("sff", 4, 100, 5, None),
+    ("sf1", 1, 37, 1, 91), ("sf1", 8, 64, 2, None), ("sf1", 9, 32, 1, 1000), ("sf1", 4, 12800, 1, 4194304),
+    ("cu", 8, 50, 1, None), ("cm", 9, 33, 1, None), ("cu", 1, 7, 1, None), ("cm", 3, 65536, 1, None),
+])
+def test_shapes_against_oracle(oracle, kind, d, w, z, wp):
+    c = W.cfg3(seed=d * 7 + w, n_ins=30_000, v=800, alpha=1.1)
+    ops, keys = c["ops"], c["keys"]
+    if kind in ("sf1", "cu"):
+        ops = np.zeros_like(ops)
+    o = oracle.OracleSketch(kind, d, w, z, wp, 11)
+    st = o.apply_ops(ops, keys.astype(np.uint64))
+    sk = make_sketch(kind, d, w, z, wp, 11)
+    assert apply_batches(sk, ops, keys) == st[:2]
+    assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+    np.testing.assert_array_equal(host(sk.query_many(c["distinct"])), o.query_many(c["distinct"].astype(np.uint64)))
+
+
+def test_key_dtypes_agree():
+    rng = np.random.Generator(np.random.PCG64(1))
+    k32 = rng.integers(0, 1 << 32, size=5000, dtype=np.uint64).astype(np.uint32)
+    res = []
+    for keys in (k32, k32.astype(np.uint64), k32.astype(np.int64), torch.from_numpy(k32).cuda(), list(map(int, k32))):
+        s = P.SfSketch(P.SketchParams(d=4, w=256, z=4, master_seed=9), "sff")
+        s.apply_ops(np.zeros(len(k32), np.uint8), keys)
+        res.append(host(s.slim.counters))
+    for r in res[1:]:
+        np.testing.assert_array_equal(res[0], r)
+    big = np.array([2**64 - 1, 2**63, 0], np.uint64)
+    s = P.CmSketch(P.SketchParams(d=3, w=16))
+    s.apply_ops(np.zeros(3, np.uint8), big)
+    assert [s.query(int(k)) for k in big] == [1, 1, 1]
+
+
+def test_record_keys_match_key_from_string(oracle):
+    recs = np.frombuffer(b"flow:10.0.0.1" b"flow:10.0.0.2" b"flow:10.0.0.1", dtype=np.uint8).reshape(3, 13)
+    s = P.SfSketch(P.SketchParams(d=4, w=64, w_prime=1000, master_seed=2), "sf1")
+    s.apply_ops(np.zeros(3, np.uint8), recs)
+    assert s.query(P.key_from_string("flow:10.0.0.1")) == 2
+    assert s.query(P.key_from_string("flow:10.0.0.2")) == 1
+    assert host(s.query_many(recs)).tolist() == [2, 1, 2]
+
+
+def test_export_import_collector_roundtrip():
+    c = W.cfg3(seed=3, n_ins=50_000, v=2000)
+    s = P.SfSketch(P.SketchParams(d=4, w=512, z=4, master_seed=77), "sff")
+    s.apply_ops(c["ops"], c["keys"])
+    payload = s.export_slim()
+    col = P.import_slim(payload)
+    assert col.export() == payload and col.insertions_seen == 50_000 and col.variant_code == 6
+    np.testing.assert_array_equal(host(col.query_many(c["distinct"])), host(s.query_many(c["distinct"])))
+    for cls in (P.CmSketch, P.CuSketch):
+        b = cls(P.SketchParams(d=3, w=64, master_seed=5))
+        b.apply_ops(np.zeros(1000, np.uint8), c["keys"][:1000])
+        bc = P.import_slim(P.export_slim(b))
+        np.testing.assert_array_equal(host(bc.query_many(c["distinct"][:100])), host(b.query_many(c["distinct"][:100])))
+
+
+def test_oracle_assisted_mode(oracle):
+    keys = np.array([5, 5, 6, 5, 7, 6], np.uint64)
+    true = np.array([1, 2, 1, 3, 1, 2], np.int64)
+    s = P.SfSketch(P.SketchParams(d=3, w=8, z=2, master_seed=1), "sff")
+    s.oracle_assisted_apply(keys, true)
+    slim = np.zeros((3, 8), np.uint32)
+    inc = np.zeros(3, np.int64)
+    oracle.oracle_slim_apply(slim, oracle.seed_array(1, 0, 3), keys, true, inc)
+    np.testing.assert_array_equal(host(s.slim.counters), slim)
+    with pytest.raises(P.UnsupportedOperationError):
+        s.insert(3)
+
+
+def test_invariants_hold_after_mixed_stream():
+    c = W.cfg3(seed=8, n_ins=100_000, v=3000, alpha=1.3)
+    for v in ("sff", "sf4"):
+        s = P.SfSketch(P.SketchParams(d=4, w=256, z=4, master_seed=8), v)
+        s.apply_ops(c["ops"], c["keys"])
+        s.check_invariants()
+
+
+def test_parallel_equals_sequential_engine():
+    c = W.cfg3(seed=12, n_ins=200_000, v=4000, alpha=1.2)
+    a = P.SfSketch(P.SketchParams(d=4, w=1024, z=4, master_seed=12), "sff")
+    b = P.SfSketch(P.SketchParams(d=4, w=1024, z=4, master_seed=12), "sff")
+    a.apply_ops(c["ops"], c["keys"])
+    b.apply_ops(c["ops"], c["keys"], sequential=True)
+    np.testing.assert_array_equal(host(a.slim.counters), host(b.slim.counters))
+    np.testing.assert_array_equal(host(a.fat.counters), host(b.fat.counters))
+    np.testing.assert_array_equal(host(a.slim.increment_counts), host(b.slim.increment_counts))
