@@ -81,6 +81,11 @@ int sfk_engine_stats(unsigned long long* out8, int reset);
  * ordered slim engine kernel; sfk_engine_last_ms() synchronises on the last
  * one and returns its duration in ms (-1 if none was recorded). */
 int sfk_engine_timing(int on);
+
+/* Diagnostics: with SFK_ENGINE_TRACE set in the environment the engine
+ * records {claim, ready, done} globaltimer stamps (ns) per run; this copies
+ * the last launch's stamps for the first `runs` runs to host memory. */
+int sfk_engine_trace(unsigned long long* host_out, size_t runs);
 float sfk_engine_last_ms(void);
 
 /* Workload utility (no reference counterpart; SURVEY.md §8(d) cfg 5): keys

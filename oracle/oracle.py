@@ -113,8 +113,9 @@ def keys_from_records(recs: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- query
-def min_query(counters: np.ndarray, seeds: np.ndarray, keys, threads: int = 1) -> np.ndarray:
-    """_kernels.py:229-241; ``threads > 1`` splits keys like bench.py:153-162."""
+def min_query(counters: np.ndarray, seeds: np.ndarray, keys, threads: int = 1, out=None) -> np.ndarray:
+    """_kernels.py:229-241; ``threads > 1`` splits keys like bench.py:153-162.
+    ``out`` (int64, len(keys)) may be passed to avoid page-faulting a fresh array."""
     counters = np.ascontiguousarray(counters, dtype=np.uint32)
     seeds = _u64(seeds)
     keys = np.ascontiguousarray(keys)
@@ -124,7 +125,8 @@ def min_query(counters: np.ndarray, seeds: np.ndarray, keys, threads: int = 1) -
         keys = _u64(keys)
         key32 = 0
     d, w = counters.shape
-    out = np.empty(keys.shape[0], dtype=np.int64)
+    if out is None:
+        out = np.empty(keys.shape[0], dtype=np.int64)
     if threads == 1 and not key32:
         lib().orc_min_query(_ptr(counters), _ptr(seeds), d, w, _ptr(keys), keys.shape[0], _ptr(out))
     else:
@@ -242,5 +244,5 @@ class OracleSketch:
         self.seen += r[2]
         return r
 
-    def query_many(self, keys, threads: int = 1):
-        return min_query(self.slim, self.slim_seeds, keys, threads)
+    def query_many(self, keys, threads: int = 1, out=None):
+        return min_query(self.slim, self.slim_seeds, keys, threads, out)

@@ -40,6 +40,7 @@ EXPORTS = (
     "sfk_engine_stats",
     "sfk_engine_timing",
     "sfk_engine_last_ms",
+    "sfk_engine_trace",
 )
 
 _lib = None
@@ -82,6 +83,7 @@ def load_library() -> ctypes.CDLL:
     L.sfk_engine_stats.argtypes = [P, I]
     L.sfk_engine_timing.argtypes = [I]
     L.sfk_engine_last_ms.restype = ctypes.c_float
+    L.sfk_engine_trace.argtypes = [P, SZ]
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]
     _lib = L
     return L

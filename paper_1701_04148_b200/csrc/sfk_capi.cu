@@ -56,6 +56,7 @@ int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint3
 size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n);
 int engine_stats(unsigned long long* out, int reset);
 int engine_timing(int on);
+int engine_trace(unsigned long long* host_out, size_t runs);
 float engine_last_ms();
 int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
                    int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
@@ -140,6 +141,8 @@ unsigned long long sfk_launch_count(void) { return __atomic_load_n(&g_launches, 
 int sfk_engine_stats(unsigned long long* out8, int reset) { return engine_stats(out8, reset); }
 
 int sfk_engine_timing(int on) { return engine_timing(on); }
+
+int sfk_engine_trace(unsigned long long* host_out, size_t runs) { return engine_trace(host_out, runs); }
 
 float sfk_engine_last_ms(void) { return engine_last_ms(); }
 

@@ -42,6 +42,19 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 constexpr int ENGINE_BLOCKS_PER_SM = 1;
+// default replay budget: a long run never stalls the other lanes of its warp
+// for more than ~this many ops
+constexpr uint32_t REPLAY_BUDGET = 1024;
+
+static uint32_t engine_budget() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SFK_ENGINE_BUDGET");  // tuning knob
+    v = s ? atoi(s) : (int)REPLAY_BUDGET;
+    if (v < 32) v = (int)REPLAY_BUDGET;
+  }
+  return (uint32_t)v;
+}
 
 static int engine_blocks_per_sm() {
   static int v = -1;
@@ -491,25 +504,96 @@ struct EngineArgs {
   const uint32_t* delbits;     // SFF: delete flags in row-0 order, one bit per op
   Ctl* ctl;
   unsigned long long* inc;     // int64[d] tallies (two's complement add)
+  uint32_t budget;             // ops a lane replays per engine iteration before it yields
+  unsigned long long* trace;   // diagnostics: per run {claim, ready, done} globaltimer ns (or null)
 };
 
-// ops one lane replays per engine iteration before it yields, so a long run
-// never stalls the other lanes of its warp
-constexpr uint32_t REPLAY_BUDGET = 1024;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+
 
 // Replay position inside the run a lane executes (SFF runs may span several
 // engine iterations).
 struct Cursor {
   uint32_t m, x, e, rem, A0;
-  uint32_t wi, w0, w1, w2, w3;  // delete-bit prefetch ring for the word-aligned part
+  uint32_t blk;      // 128-op block (4 words) held in q0
+  uint4 q0, q1, q2;  // delete-bit prefetch: up to 12 words ahead of the replay
   bool ring;
 };
+
+__device__ __forceinline__ uint32_t pick_word(const uint4& q, uint32_t sel) {
+  return sel == 0 ? q.x : sel == 1 ? q.y : sel == 2 ? q.z : q.w;
+}
 
 template <int D>
 __device__ __forceinline__ void raise_to(uint32_t tgt, uint32_t (&c)[D], uint32_t (&raised)[D]) {
 #pragma unroll
   for (int i = 0; i < D; ++i)
     if (c[i] < tgt) { raised[i] += tgt - c[i]; c[i] = tgt; }
+}
+
+// Walk summaries of +1 (delete) / -1 (insert) step sequences. For a byte b
+// (8 steps, bit j = step j) lut[b] packs, each biased by +8 into one byte:
+// the total, the minimum and maximum prefix sums (empty prefix included) and
+// the maximum draw-up (largest rise between two prefixes).
+struct WalkSum {
+  int32_t t, mn, mx, du;
+};
+
+__device__ __forceinline__ void build_step_lut(uint32_t* lut) {
+  for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
+    int32_t p = 0, mn = 0, mx = 0, du = 0;
+    for (int j = 0; j < 8; ++j) {
+      p += ((b >> j) & 1u) ? 1 : -1;
+      mn = min(mn, p);
+      mx = max(mx, p);
+      du = max(du, p - mn);
+    }
+    lut[b] = (uint32_t)(p + 8) | ((uint32_t)(mn + 8) << 8) | ((uint32_t)(mx + 8) << 16) | ((uint32_t)(du + 8) << 24);
+  }
+}
+
+// Two-sided reflection tables for narrow rows: for an upper bound W in
+// [1, WMAX], a start v in [0, 7] and a byte of steps b, rlut[((W-1)*8+v)*256+b]
+// = (pushes at the lower bound << 4) | end value, where an insert maps
+// v -> max(v-1, 0) (v == 0 is a push) and a delete v -> min(v+1, W).
+constexpr int WMAX = 7;
+
+__device__ __forceinline__ void build_reflect_lut(uint8_t* rlut) {
+  for (uint32_t idx = threadIdx.x; idx < (uint32_t)WMAX * 8 * 256; idx += blockDim.x) {
+    const uint32_t b = idx & 255u, v0 = (idx >> 8) & 7u, W = (idx >> 11) + 1u;
+    uint32_t v = v0, push = 0;
+    for (int j = 0; j < 8; ++j) {
+      if ((b >> j) & 1u) {
+        v = min(v + 1u, W);
+      } else if (v == 0) {
+        ++push;
+      } else {
+        --v;
+      }
+    }
+    rlut[idx] = (uint8_t)((push << 4) | v);
+  }
+}
+
+// summary of a full 32-step word: fold the four byte summaries
+__device__ __forceinline__ WalkSum walk_sum32(uint32_t bits, const uint32_t* lut) {
+  WalkSum w{0, 0, 0, 0};
+#pragma unroll
+  for (int byte = 0; byte < 4; ++byte) {
+    const uint32_t e = lut[(bits >> (8 * byte)) & 0xFFu];
+    const int32_t t = (int32_t)(e & 0xFFu) - 8, mn = (int32_t)((e >> 8) & 0xFFu) - 8;
+    const int32_t mx = (int32_t)((e >> 16) & 0xFFu) - 8, du = (int32_t)(e >> 24) - 8;
+    w.du = max(max(w.du, du), w.t + mx - w.mn);
+    w.mn = min(w.mn, w.t + mn);
+    w.mx = max(w.mx, w.t + mx);
+    w.t += t;
+  }
+  return w;
 }
 
 // SFF: replay `avail` ops of a run whose delete flags are the low bits of
@@ -520,7 +604,8 @@ __device__ __forceinline__ void raise_to(uint32_t tgt, uint32_t (&c)[D], uint32_
 template <int D>
 __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const uint32_t (&A)[D],
                                             const uint32_t (&O)[D], uint32_t A0, uint32_t& m, uint32_t& x,
-                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3]) {
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3],
+                                            const uint32_t* lut, const uint8_t* rlut) {
   const uint32_t nd = __popc(bits), ni = avail - nd;
   // Gap word: the min lags the key's own count by at least the word's
   // deletes (mu = m - x, mu + nd <= A0). Every insert passes the gate and
@@ -549,35 +634,73 @@ __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const
   // Steady word: the min is caught up (m == A0 + x, so it stays A0 + x) and
   // no other slot can exceed the key's own count within the word. Rows then
   // evolve independently: with v_i = c_i - m an insert maps v -> max(v-1, 0)
-  // (a push at 0 is one raise) and a delete v -> min(v+1, A_i - A0). With the
-  // upper bound out of reach, v_end = max(v + S, max suffix sum) (Lindley)
-  // and the pushes are v_end - (v + S).
+  // (a push at 0 is one raise) and a delete v -> min(v+1, W_i), W_i = A_i -
+  // A0. The lower-reflected walk peaks at max(v + max prefix, max draw-up);
+  // while that stays <= W_i the upper bound never binds and
+  // v_end = max(v + S, S - min prefix) (Lindley), pushes = v_end - (v + S).
+  // W_i == 0 pins the row to the min; otherwise the row steps bit by bit.
   {
-    bool steady = avail >= 8u && m == A0 + x;
+    bool steady = m == A0 + x;
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      const uint32_t v = c[i] - m, W = A[i] - A0;
-      steady = steady && (int64_t)O[i] <= (int64_t)(uint32_t)(A[i] + x) - (int64_t)nd &&
-               ((uint64_t)v + nd <= (uint64_t)W || (W == 0 && v == 0));
-    }
+    for (int i = 0; i < D; ++i) steady = steady && (int64_t)O[i] <= (int64_t)(uint32_t)(A[i] + x) - (int64_t)nd;
     if (steady) {
-      int32_t msuf = 0;
-      for (uint32_t k = 0; k < avail; ++k) msuf = max(msuf, 2 * __popc(bits >> k) - (int32_t)(avail - k));
       const int32_t S = (int32_t)nd - (int32_t)ni;
       const uint32_t mnew = m + ni - nd;
+      uint32_t v[D], W[D], push[D];
+      bool done[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        const uint32_t v = c[i] - m;
-        uint32_t vend, push;
-        if ((uint64_t)v + nd <= (uint64_t)(A[i] - A0)) {
-          vend = (uint32_t)max((int64_t)v + S, (int64_t)msuf);
-          push = (uint32_t)((int64_t)vend - ((int64_t)v + S));
-        } else {  // W == 0, v == 0: the row sits on both bounds
-          vend = 0;
-          push = ni;
+        v[i] = c[i] - m;
+        W[i] = A[i] - A0;
+        push[i] = 0;
+        done[i] = false;
+      }
+      if (avail == 32u) {
+        const WalkSum w = walk_sum32(bits, lut);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          if ((int64_t)max((int64_t)v[i] + w.mx, (int64_t)w.du) <= (int64_t)W[i]) {  // Lindley
+            const int64_t vend = max((int64_t)v[i] + S, (int64_t)(S - w.mn));
+            push[i] = (uint32_t)(vend - ((int64_t)v[i] + S));
+            v[i] = (uint32_t)vend;
+            done[i] = true;
+          } else if (W[i] == 0 && v[i] == 0) {  // the row sits on both bounds
+            push[i] = ni;
+            done[i] = true;
+          }
         }
-        raised[i] += push;
-        c[i] = mnew + vend;
+        // narrow rows: four table steps each, the d chains interleaved
+#pragma unroll
+        for (int byte = 0; byte < 4; ++byte) {
+          const uint32_t b = (bits >> (8 * byte)) & 0xFFu;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            if (!done[i] && W[i] <= (uint32_t)WMAX && W[i] > 0 && v[i] <= 7u) {
+              const uint32_t e = rlut[((W[i] - 1u) * 8u + v[i]) * 256u + b];
+              push[i] += e >> 4;
+              v[i] = e & 15u;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (!done[i] && W[i] <= (uint32_t)WMAX && W[i] > 0 && v[i] <= 7u) done[i] = true;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        if (!done[i]) {
+          if (W[i] == 0 && v[i] == 0) {
+            push[i] = ni;
+          } else {
+            for (uint32_t k = 0; k < avail; ++k) {
+              const uint32_t del = (bits >> k) & 1u;
+              push[i] += (del == 0u) & (v[i] == 0u);
+              v[i] = del ? min(v[i] + 1u, W[i]) : (v[i] ? v[i] - 1u : 0u);
+            }
+          }
+        }
+        raised[i] += push[i];
+        c[i] = mnew + v[i];
       }
       m = mnew;
       x += ni - nd;
@@ -623,7 +746,8 @@ __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const
 template <int D, int MODE>
 __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, uint32_t e0, uint32_t info,
                                             uint32_t bits0, const uint32_t (&A)[D], const uint32_t (&O)[D],
-                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3]) {
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3],
+                                            const uint32_t* lut, const uint8_t* rlut) {
   const uint32_t L = info & 0x7fffffffu;
   if (MODE == 1) {
     raise_to<D>(k.m + L, c, raised);  // m0 + L fits: the precheck bounds every counter
@@ -641,7 +765,7 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     return true;
   }
   const uint32_t wlast = (e0 + L - 1) >> 5;
-  uint32_t budget = REPLAY_BUDGET;
+  uint32_t budget = a.budget;
   while (k.rem && budget) {
     uint32_t bits, avail;
     const uint32_t done = k.e - e0;
@@ -649,25 +773,28 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
       avail = min(32u - done, k.rem);
       bits = bits0 >> done;
     } else {
+      const uint4* blocks = reinterpret_cast<const uint4*>(a.delbits);
+      const uint32_t lastblk = wlast >> 2;
+      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
       if (!k.ring) {
-        k.wi = k.e >> 5;
-        k.w0 = a.delbits[k.wi];
-        k.w1 = k.wi + 1 <= wlast ? a.delbits[k.wi + 1] : 0u;
-        k.w2 = k.wi + 2 <= wlast ? a.delbits[k.wi + 2] : 0u;
-        k.w3 = k.wi + 3 <= wlast ? a.delbits[k.wi + 3] : 0u;
+        k.blk = k.e >> 7;
+        k.q0 = blocks[k.blk];
+        k.q1 = k.blk + 1 <= lastblk ? blocks[k.blk + 1] : zero4;
+        k.q2 = k.blk + 2 <= lastblk ? blocks[k.blk + 2] : zero4;
         k.ring = true;
+      }
+      if ((k.e >> 7) != k.blk) {  // advance one block, keep two in flight
+        k.q0 = k.q1;
+        k.q1 = k.q2;
+        ++k.blk;
+        k.q2 = k.blk + 2 <= lastblk ? blocks[k.blk + 2] : zero4;
       }
       const uint32_t off = k.e & 31u;
       avail = min(32u - off, k.rem);
-      bits = k.w0 >> off;
-      k.w0 = k.w1;
-      k.w1 = k.w2;
-      k.w2 = k.w3;
-      k.w3 = k.wi + 4 <= wlast ? a.delbits[k.wi + 4] : 0u;
-      ++k.wi;
+      bits = pick_word(k.q0, (k.e >> 5) & 3u) >> off;
     }
     if (avail < 32u) bits &= (1u << avail) - 1u;
-    replay_word<D>(bits, avail, A, O, k.A0, k.m, k.x, c, raised, ws);
+    replay_word<D>(bits, avail, A, O, k.A0, k.m, k.x, c, raised, ws, lut, rlut);
     k.e += avail;
     k.rem -= avail;
     budget = budget > avail ? budget - avail : 0u;
@@ -686,11 +813,17 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
 // long run is replayed REPLAY_BUDGET ops per iteration.
 template <int D, int MODE>
 __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
+  __shared__ uint32_t lut[256];
+  __shared__ uint8_t rlut[WMAX * 8 * 256];
+  build_step_lut(lut);
+  if (MODE == 2) build_reflect_lut(rlut);
+  __syncthreads();
   const uint32_t lane = lane_id();
   const uint32_t R = a.ctl->n_runs;
   bool has = false, exhausted = false;
   uint32_t cells[D], rank[D], A[D], O[D], c[D], raised[D];
   uint32_t e0 = 0, info = 0, bits0 = 0, pend = 0;  // pend: bit i = cell i not seen ready yet
+  uint32_t rid = 0;
 #pragma unroll
   for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0, A[i] = 0, O[i] = 0, c[i] = 0;
   Cursor k{};
@@ -708,6 +841,8 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
       if (!has && !exhausted) {
         const uint32_t r = base + __popc(need & lanemask_lt());
         if (r < R) {
+          rid = r;
+          if (a.trace) a.trace[3ull * r] = gtimer();
           const RunRec<D>& rec = a.recs[r];
           e0 = rec.e0;
           info = rec.info;
@@ -739,6 +874,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
           pend &= ~(1u << i);
         }
       if (!pend) {  // all cells acquired: start the replay
+        if (a.trace) a.trace[3ull * rid + 1] = gtimer();
         k.m = c[0];
 #pragma unroll
         for (int i = 1; i < D; ++i) k.m = min(k.m, c[i]);
@@ -753,7 +889,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
     }
     if (has && !pend) {
       const long long t0 = clock64();
-      const bool done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws);
+      const bool done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws, lut, rlut);
       st_cyc += clock64() - t0;
       if (done) {
         const uint32_t L = info & 0x7fffffffu;
@@ -762,6 +898,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
           st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
         has = false;
         ++st_runs;
+        if (a.trace) a.trace[3ull * rid + 2] = gtimer();
       }
       progressed = true;
     }
@@ -1002,7 +1139,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   const bool need_obs = kind == 1;
   L.obs = cv.take<uint32_t>(need_obs ? N : 1);
   L.obs2 = cv.take<uint2>(kind == 0 ? N : 1);
-  L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 2 : 1);
+  L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 16 : 1);
   const bool engine = kind != 3;
   L.links = cv.take<uint2>(engine ? N : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
@@ -1023,6 +1160,16 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.total = cv.off + 256;
   L.ok = cv.ok;
   return L;
+}
+
+// optional per-run engine trace (diagnostics; SFK_ENGINE_TRACE=1)
+static unsigned long long* g_trace = nullptr;
+static uint32_t g_trace_cap = 0;
+
+int engine_trace(unsigned long long* host_out, size_t runs) {
+  if (!g_trace) return -1;
+  const size_t m = runs < g_trace_cap ? runs : g_trace_cap;
+  return (int)cudaMemcpy(host_out, g_trace, sizeof(unsigned long long) * 3 * m, cudaMemcpyDeviceToHost);
 }
 
 // optional CUDA-event timing of the engine kernel (bench instrumentation)
@@ -1187,6 +1334,16 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.delbits = L.delbits;
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
+  ea.budget = engine_budget();
+  ea.trace = nullptr;
+  if (getenv("SFK_ENGINE_TRACE")) {  // diagnostics only: per-run timestamps
+    if (g_trace_cap < n) {
+      if (g_trace) cudaFree(g_trace);
+      cudaMalloc(&g_trace, sizeof(unsigned long long) * 3 * (size_t)n);
+      g_trace_cap = n;
+    }
+    ea.trace = g_trace;
+  }
   if (g_time_engine) cudaEventRecord(g_ev[0], st);
   { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea); }
   if (g_time_engine) {
