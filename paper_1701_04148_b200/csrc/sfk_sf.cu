@@ -502,6 +502,7 @@ struct EngineArgs {
   const RunRec<D>* recs;
   const uint32_t* opdata;      // SF1: b_min per op (row-0 order)
   const uint32_t* delbits;     // SFF: delete flags in row-0 order, one bit per op
+  const uint32_t* wsum;        // SFF: per aligned word, nd | -min prefix << 6 | max prefix << 12 | draw-up << 18
   Ctl* ctl;
   unsigned long long* inc;     // int64[d] tallies (two's complement add)
   uint32_t budget;             // ops a lane replays per engine iteration before it yields
@@ -594,6 +595,19 @@ __device__ __forceinline__ WalkSum walk_sum32(uint32_t bits, const uint32_t* lut
     w.t += t;
   }
   return w;
+}
+
+// per-word walk summaries of the delete bits (for the steady fast loop)
+__global__ void __launch_bounds__(256) word_sums_k(const uint32_t* __restrict__ delbits, uint32_t nwords,
+                                                   uint32_t* __restrict__ wsum) {
+  __shared__ uint32_t lut[256];
+  build_step_lut(lut);
+  __syncthreads();
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
+    const uint32_t bits = delbits[w];
+    const WalkSum s = walk_sum32(bits, lut);
+    wsum[w] = (uint32_t)__popc(bits) | ((uint32_t)(-s.mn) << 6) | ((uint32_t)s.mx << 12) | ((uint32_t)s.du << 18);
+  }
 }
 
 // SFF: replay `avail` ops of a run whose delete flags are the low bits of
@@ -766,7 +780,108 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
   }
   const uint32_t wlast = (e0 + L - 1) >> 5;
   uint32_t budget = a.budget;
+  // steady-word fast loop constants: rows' widths and the largest O_i - A_i
+  uint32_t W[D];
+  int64_t omax = INT64_MIN;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    W[i] = A[i] - k.A0;
+    omax = max(omax, (int64_t)O[i] - (int64_t)A[i]);
+  }
   while (k.rem && budget) {
+    // Fast loop over whole aligned words in the steady regime (see
+    // replay_word) from the precomputed walk summaries: per word only the
+    // regime test and d Lindley updates remain on the sequential path.
+    bool fast = (k.e & 31u) == 0 && k.rem >= 32u && budget >= 32u && k.m == k.A0 + k.x;
+#pragma unroll
+    for (int i = 0; i < D; ++i) fast = fast && W[i] < (1u << 30) && c[i] - k.m < (1u << 30);
+    if (fast) {
+      // Steady fast loop (32-bit, branch-free per row). m == A0 + x holds by
+      // construction inside the loop, so only the O bound and each row's
+      // "upper bound out of reach" test remain per word.
+      const uint4* ws4 = reinterpret_cast<const uint4*>(a.wsum);
+      const uint4* db4 = reinterpret_cast<const uint4*>(a.delbits);
+      uint32_t w = k.e >> 5;
+      uint4 b0 = ws4[w >> 2], b1 = ws4[(w >> 2) + 1], b2 = ws4[(w >> 2) + 2];
+      uint4 d0 = db4[w >> 2], d1 = db4[(w >> 2) + 1], d2 = db4[(w >> 2) + 2];
+      int32_t v[D], Wi[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] = (int32_t)(c[i] - k.m);
+        Wi[i] = (int32_t)W[i];
+      }
+      const int32_t om = (int32_t)max(min(omax, (int64_t)INT32_MAX), (int64_t)INT32_MIN + 64);
+      int32_t x32 = (int32_t)k.x;
+      uint32_t words = 0, wmax = min(k.rem, budget) >> 5;
+      while (words < wmax) {
+        const uint32_t q = pick_word(b0, w & 3u);
+        const int32_t nd = (int32_t)(q & 63u), mn = (int32_t)((q >> 6) & 63u);  // mn = -(min prefix)
+        const int32_t mx = (int32_t)((q >> 12) & 63u), du = (int32_t)((q >> 18) & 63u);
+        if (x32 - nd < om) break;
+        bool easy = true;
+#pragma unroll
+        for (int i = 0; i < D; ++i) easy = easy & (((v[i] | Wi[i]) == 0) | (max(v[i] + mx, du) <= Wi[i]));
+        const int32_t S = 2 * nd - 32;
+        if (easy) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const bool pinned = (v[i] | Wi[i]) == 0;
+            const int32_t vend = pinned ? 0 : max(v[i] + S, S + mn);
+            raised[i] += (uint32_t)(pinned ? 32 - nd : vend - v[i] - S);
+            v[i] = vend;
+          }
+        } else {
+          // some row can reach its upper bound: narrow rows walk the
+          // reflection table, anything wider leaves the fast loop
+          bool ok = true;
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            ok = ok & (((v[i] | Wi[i]) == 0) | (max(v[i] + mx, du) <= Wi[i]) | ((Wi[i] <= WMAX) & (v[i] <= 7)));
+          if (!ok) break;
+          const uint32_t bits = pick_word(d0, w & 3u);
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const bool pinned = (v[i] | Wi[i]) == 0;
+            if (!pinned && max(v[i] + mx, du) > Wi[i]) {  // two-sided reflection: four table steps
+              uint32_t vv = (uint32_t)v[i], push = 0;
+              const uint8_t* tab = rlut + (uint32_t)(Wi[i] - 1) * 8u * 256u;
+#pragma unroll
+              for (int byte = 0; byte < 4; ++byte) {
+                const uint32_t e = tab[vv * 256u + ((bits >> (8 * byte)) & 0xFFu)];
+                push += e >> 4;
+                vv = e & 15u;
+              }
+              raised[i] += push;
+              v[i] = (int32_t)vv;
+            } else {
+              const int32_t vend = pinned ? 0 : max(v[i] + S, S + mn);
+              raised[i] += (uint32_t)(pinned ? 32 - nd : vend - v[i] - S);
+              v[i] = vend;
+            }
+          }
+        }
+        x32 += 32 - 2 * nd;
+        ++words;
+        ++w;
+        if ((w & 3u) == 0) {
+          b0 = b1;
+          b1 = b2;
+          b2 = ws4[(w >> 2) + 2];
+          d0 = d1;
+          d1 = d2;
+          d2 = db4[(w >> 2) + 2];
+        }
+      }
+      k.x = (uint32_t)x32;
+      k.m = k.A0 + k.x;
+#pragma unroll
+      for (int i = 0; i < D; ++i) c[i] = k.m + (uint32_t)v[i];
+      k.e += words * 32u;
+      k.rem -= words * 32u;
+      budget -= words * 32u;
+      ws[1] += words;
+      if (!k.rem || !budget) break;
+    }
     uint32_t bits, avail;
     const uint32_t done = k.e - e0;
     if (done < 32u) {
@@ -776,14 +891,13 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
       const uint4* blocks = reinterpret_cast<const uint4*>(a.delbits);
       const uint32_t lastblk = wlast >> 2;
       const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-      if (!k.ring) {
+      if (!k.ring || (k.e >> 7) > k.blk + 1u) {
         k.blk = k.e >> 7;
         k.q0 = blocks[k.blk];
         k.q1 = k.blk + 1 <= lastblk ? blocks[k.blk + 1] : zero4;
         k.q2 = k.blk + 2 <= lastblk ? blocks[k.blk + 2] : zero4;
         k.ring = true;
-      }
-      if ((k.e >> 7) != k.blk) {  // advance one block, keep two in flight
+      } else if ((k.e >> 7) != k.blk) {  // advance one block, keep two in flight
         k.q0 = k.q1;
         k.q1 = k.q2;
         ++k.blk;
@@ -1100,6 +1214,7 @@ struct Layout {
   uint32_t* obs;
   uint2* obs2;
   uint32_t* delbits;
+  uint32_t* wsum;
   uint2* links;
   uint8_t* opflags;
   uint32_t* opdata;
@@ -1140,6 +1255,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.obs = cv.take<uint32_t>(need_obs ? N : 1);
   L.obs2 = cv.take<uint2>(kind == 0 ? N : 1);
   L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 16 : 1);
+  L.wsum = cv.take<uint32_t>(kind == 0 ? n / 32 + 32 : 1);
   const bool engine = kind != 3;
   L.links = cv.take<uint2>(engine ? N : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
@@ -1332,6 +1448,11 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.recs = static_cast<const RunRec<D>*>(L.recs);
   ea.opdata = L.opdata;
   ea.delbits = L.delbits;
+  ea.wsum = L.wsum;
+  if (MODE == 2) {
+    const uint32_t nwords = (n + 31) / 32;
+    { note_launch(); word_sums_k<<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(L.delbits, nwords, L.wsum); }
+  }
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
   ea.budget = engine_budget();

@@ -57,7 +57,12 @@ int main(int argc, char** argv) {
   unsigned long long* d_out;
   cudaMalloc(&d_out, 64);
   EngineArgs<4> a{};
+  std::vector<uint32_t> hw(bits.size());
   a.delbits = d_bits;
+  uint32_t* d_ws;
+  cudaMalloc(&d_ws, bits.size() * 4 + 256);
+  word_sums_k<<<64, 256>>>(d_bits, (uint32_t)bits.size(), d_ws);
+  a.wsum = d_ws;
   a.budget = 0xFFFFFFFFu;
   const uint32_t Ws[][3] = {{0, 0, 0}, {2, 3, 5}, {20, 30, 50}};
   for (auto& w : Ws) {
