@@ -320,7 +320,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
 #pragma unroll
         for (int q2 = 0; q2 < Z; ++q2)
           if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q2] + run.v[q2]));
-        o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
+        if (WRITE_LINKS) {  // links and observations interleaved: one 16-B store
+          const uint32_t prev = (e > run.head) ? prev_t : NONE32;
+          reinterpret_cast<uint4*>(o.links)[(size_t)t * o.D + row] =
+              make_uint4(e - run.head, prev, (uint32_t)post_own, others);
+        } else {
+          o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
+        }
       }
       if (WRITE_OBS == 1) {
         uint32_t ob;
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
         for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
       }
     }
-    if (WRITE_LINKS) {
+    if (WRITE_LINKS && !(HAS_FAT && WRITE_OBS == 2)) {
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
       o.links[(size_t)t * o.D + row] = make_uint2(e - run.head, prev);
     }
@@ -354,7 +360,8 @@ struct RunArgs {
   const uint32_t* vals0;  // row-0 sorted vals (slim cells)
   int kb;
   uint32_t n;
-  const uint2* links;      // {rank in cell, prev op} per (t, row)
+  const uint2* links;      // {rank in cell, prev op} per (t, row), every lstride-th uint2
+  int lstride;
   const uint32_t* obs;     // SF1: post-insert own fat count per (t, row); null otherwise
   KeySrc keys;
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const bool valid = t < tstar;
     uint32_t prev[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) prev[i] = a.links[(size_t)t * D + i].y;
+    for (int i = 0; i < D; ++i) prev[i] = a.links[((size_t)t * D + i) * a.lstride].y;
     bool cont = valid && prev[0] != NONE32;
 #pragma unroll
     for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
@@ -435,6 +442,7 @@ struct BuildArgs {
   const uint32_t* delbits;  // SFF
   const uint2* obs2;        // SFF
   const uint2* links;
+  int lstride;              // 2 when links and obs2 are interleaved in one uint4 per (t, row)
   uint32_t n;
   KeySrc keys;
   Seeds<D> seeds;
@@ -478,9 +486,9 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       rec.cells[i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
-      rec.rank[i] = a.links[(size_t)t * D + i].x;
+      rec.rank[i] = a.links[((size_t)t * D + i) * a.lstride].x;
       if (a.obs2) {
-        const uint2 ob = a.obs2[(size_t)t * D + i];
+        const uint2 ob = a.obs2[((size_t)t * D + i) * a.lstride];
         rec.A[i] = head_del ? ob.x + 1u : ob.x - 1u;
         rec.O[i] = ob.y;
       } else {
@@ -1253,11 +1261,11 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
   const bool need_obs = kind == 1;
   L.obs = cv.take<uint32_t>(need_obs ? N : 1);
-  L.obs2 = cv.take<uint2>(kind == 0 ? N : 1);
+  L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
   L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 16 : 1);
   L.wsum = cv.take<uint32_t>(kind == 0 ? n / 32 + 32 : 1);
   const bool engine = kind != 3;
-  L.links = cv.take<uint2>(engine ? N : 1);
+  L.links = cv.take<uint2>(engine ? (kind == 0 ? 2 * N : N) : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
   L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);
   L.headflag = cv.take<uint32_t>(engine ? n : 1);
@@ -1400,6 +1408,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.kb = kb;
   ra.n = n;
   ra.links = L.links;
+  ra.lstride = MODE == 2 ? 2 : 1;
   ra.obs = MODE == 0 ? L.obs : nullptr;
   ra.keys = ks;
   ra.opflags = L.opflags;
@@ -1431,8 +1440,9 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.bpos = L.bpos;
   ba.delpre = L.delpre;
   ba.delbits = MODE == 2 ? L.delbits : nullptr;
-  ba.obs2 = MODE == 2 ? L.obs2 : nullptr;
+  ba.obs2 = MODE == 2 ? L.links + 1 : nullptr;
   ba.links = L.links;
+  ba.lstride = MODE == 2 ? 2 : 1;
   ba.n = n;
   ba.keys = ks;
   for (int i = 0; i < D; ++i) ba.seeds.s[i] = slim_seeds[i];
