@@ -27,7 +27,6 @@ import ctypes
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -69,53 +68,67 @@ def workload_config(args, world):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+    """SM clocks + clock-event reasons sampled DURING the timed region through
+    NVML (pynvml) in a background thread; nvidia-smi is the fallback."""
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.proc = None
-        self.lines = []
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.idx = device_index
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reason_bits)
+        self.err = None
+        self._stop = threading.Event()
+        self.t = None
+
+    def _handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(self.idx).uuid)
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
+        except Exception:  # noqa: BLE001 - fall back to the visible-index mapping
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip()]
+            phys = int(ids[self.idx]) if ids and ids[self.idx].strip().isdigit() else self.idx
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(phys)
+
+    def _run(self):
+        try:
+            nv, h = self._handle()
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, rs, time.perf_counter()))
+                self._stop.wait(self.period)
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml: {type(e).__name__}: {e}"
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+    def stop(self, t_begin=None, t_end=None):
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=5)
+        timed = [s for s in self.samples if (t_begin is None or s[3] >= t_begin) and (t_end is None or s[3] <= t_end)]
+        timed = timed or self.samples
+        # only samples taken under load (GpuIdle bit clear) count toward the median
+        load = [s for s in timed if not (s[2] & 0x1)] or timed
+        sm = [s[0] for s in load]
+        reasons = sorted({nm for s in load for nm, bit in self.REASONS.items() if s[2] & bit})
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": max(s[1] for s in self.samples) if self.samples else None,
+               "reasons": reasons, "samples": len(timed), "samples_under_load": len(load),
+               "source": "nvml (pynvml), 10 ms period, samples inside the timed region"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 def measured_peaks():
@@ -267,6 +280,7 @@ def run_ours(args):
     est0 = (ctypes.c_ulonglong * 8)()
     L.sfk_engine_stats(est0, 1)
     phases = []
+    t_begin = time.perf_counter()
     for _ in range(args.steps):
         phases.append(step())
         flush.fill_(1)
@@ -277,7 +291,8 @@ def run_ours(args):
     L.sfk_engine_timing(0)
     est = (ctypes.c_ulonglong * 8)()
     L.sfk_engine_stats(est, 1)
-    clk = clocks.stop()
+    t_end = time.perf_counter()
+    clk = clocks.stop(t_begin, t_end)
     tot = np.array(phases).sum(axis=0)  # build, bcast, query, engine kernel (ms over K steps)
     step_ms_local = float(tot[:3].sum()) / args.steps
     t = torch.tensor([step_ms_local, tot[0] / args.steps, tot[1] / args.steps, tot[2] / args.steps],

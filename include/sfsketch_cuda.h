@@ -110,6 +110,16 @@ int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_
                   const void* keys, int key_kind, int rec_len, int64_t n, int64_t* out,
                   void* stream);
 
+/* Query kernel selection (no reference counterpart: the reference has one
+ * numba loop). mode: 0 = automatic (default), 1 = L2 gathers, 2 = whole table
+ * in one SM's shared memory (only if it fits), 3 = row-partitioned cluster
+ * (d CTAs, one row each, DSMEM min-reduction; only for 2 <= d <= 8 and a row
+ * that fits); a mode that does not apply falls back to the L2 path. A
+ * negative mode only reads. Returns the previous mode. sfk_query_last_path()
+ * returns the path (1/2/3) the last sfk_min_query launch took. */
+int sfk_query_path(int mode);
+int sfk_query_last_path(void);
+
 /* Replaces _kernels.cm_apply (_kernels.py:62-88), called from
  * CmSketch.apply_ops (baselines.py:72-78). */
 size_t sfk_cm_workspace_size(int d, int64_t w, int64_t n);

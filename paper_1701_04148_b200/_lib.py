@@ -41,6 +41,8 @@ EXPORTS = (
     "sfk_engine_timing",
     "sfk_engine_last_ms",
     "sfk_engine_trace",
+    "sfk_query_path",
+    "sfk_query_last_path",
 )
 
 _lib = None
@@ -84,6 +86,7 @@ def load_library() -> ctypes.CDLL:
     L.sfk_engine_timing.argtypes = [I]
     L.sfk_engine_last_ms.restype = ctypes.c_float
     L.sfk_engine_trace.argtypes = [P, SZ]
+    L.sfk_query_path.argtypes = [I]
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]
     _lib = L
     return L

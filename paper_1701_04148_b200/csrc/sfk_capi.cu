@@ -47,6 +47,8 @@ int sm_count() {
 // implemented in sfk_query.cu / sfk_seq.cu / sfk_sf.cu
 int launch_min_query(const uint32_t*, const uint64_t*, int, int64_t, KeySrc, int64_t, int64_t*, cudaStream_t);
 int launch_mix_batch(const uint64_t*, int64_t, uint64_t*, cudaStream_t);
+int query_path(int mode);
+int query_last_path();
 int launch_load_keys(KeySrc, int64_t, uint64_t*, cudaStream_t);
 int launch_gen_query_keys(uint64_t, const uint32_t*, const uint32_t*, uint32_t, const double*, int64_t, int64_t,
                           uint32_t*, cudaStream_t);
@@ -141,6 +143,10 @@ unsigned long long sfk_launch_count(void) { return __atomic_load_n(&g_launches, 
 int sfk_engine_stats(unsigned long long* out8, int reset) { return engine_stats(out8, reset); }
 
 int sfk_engine_timing(int on) { return engine_timing(on); }
+
+int sfk_query_path(int mode) { return query_path(mode); }
+
+int sfk_query_last_path(void) { return query_last_path(); }
 
 int sfk_engine_trace(unsigned long long* host_out, size_t runs) { return engine_trace(host_out, runs); }
 

@@ -1,0 +1,131 @@
+"""Every point-query kernel path (L2 gathers, whole table in shared memory,
+row-partitioned cluster with DSMEM min-reduction) against the oracle's
+min_query (the restatement of _kernels.min_query, _kernels.py:229-241), with
+the path forced through sfk_query_path. Covers the cluster path's u16 rows
+with the exact >= 65535 re-gather, u32 rows, odd d, non-power-of-two widths,
+tile tails, misaligned key / output pointers and all three key kinds."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_1701_04148_b200 import _lib  # noqa: E402
+from paper_1701_04148_b200.hashing import seed_array  # noqa: E402
+
+L2, SMEM, CLUSTER = 1, 2, 3
+
+
+def run_query(counters, seeds, keys_t, kind, rec, n, out_t, path):
+    L = _lib.lib()
+    prev = L.sfk_query_path(path)
+    try:
+        rc = L.sfk_min_query(counters.data_ptr(), seeds.ctypes.data_as(ctypes.c_void_p), counters.shape[0],
+                             counters.shape[1], keys_t.data_ptr(), kind, rec, n, out_t.data_ptr(),
+                             _lib.stream_ptr())
+        _lib.check(rc, "sfk_min_query")
+        torch.cuda.synchronize()
+        return L.sfk_query_last_path()
+    finally:
+        L.sfk_query_path(prev)
+
+
+def table(rng, d, w, hi):
+    c = rng.integers(0, hi, size=(d, w), dtype=np.uint64).astype(np.uint32)
+    return c
+
+
+@pytest.mark.parametrize("d,w,hi,path", [
+    (4, 65536, 1 << 20, CLUSTER),   # cfg 3/5 shape: u16 rows, many clamped cells
+    (4, 65536, 70000, CLUSTER),     # values straddling 65535
+    (4, 65536, 1000, CLUSTER),      # no clamping at all
+    (4, 16384, 1 << 32, CLUSTER),   # cfg 1 shape: u32 rows
+    (3, 65536, 1 << 18, CLUSTER),   # odd cluster size
+    (5, 12345, 1 << 32, CLUSTER),   # non-pow2 width, u32 rows
+    (8, 50000, 1 << 17, CLUSTER),   # portable maximum cluster, u16 rows, non-pow2
+    (2, 40000, 1 << 32, CLUSTER),
+    (4, 12800, 1 << 32, SMEM),      # cfg 4 shape
+    (4, 65536, 1 << 32, L2),
+])
+@pytest.mark.parametrize("n", [1, 4097, 100_003, 1_000_000])
+def test_query_paths_u32_keys(oracle, d, w, hi, path, n):
+    rng = np.random.default_rng(d * 1000 + w + n)
+    c = table(rng, d, w, hi)
+    # make some cells exactly 65534 / 65535 / 65536 so every clamp edge is hit
+    c.flat[rng.integers(0, c.size, 512)] = rng.choice(np.array([65534, 65535, 65536], np.uint32), 512)
+    seeds = seed_array(7 + d, 0, d)
+    keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    ct = torch.from_numpy(c).cuda()
+    kt = torch.from_numpy(keys).cuda()
+    out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    took = run_query(ct, seeds, kt, _lib.KEY_U32, 0, n, out, path)
+    assert took == path
+    want = oracle.min_query(c, seeds, keys.astype(np.uint64))
+    np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_cluster_hot_keys_take_the_exact_regather(oracle):
+    """Keys whose every row counter is >= 65535 (the hot keys of a Zipf
+    stream) must come back with their exact u32 minimum."""
+    d, w = 4, 65536
+    rng = np.random.default_rng(3)
+    seeds = seed_array(2017, 0, d)
+    keys = rng.integers(0, 1 << 32, size=300_000, dtype=np.uint64).astype(np.uint32)
+    c = rng.integers(0, 60000, size=(d, w), dtype=np.uint64).astype(np.uint32)
+    hot = keys[:1000].astype(np.uint64)
+    for i in range(d):
+        idx = oracle.min_query(np.arange(w, dtype=np.uint32)[None, :].repeat(1, 0), seeds[i:i + 1], hot)
+        c[i, idx] = 65535 + rng.integers(0, 1 << 20, size=idx.size).astype(np.uint32)
+    ct = torch.from_numpy(c).cuda()
+    kt = torch.from_numpy(keys).cuda()
+    out = torch.empty(keys.size, dtype=torch.int64, device="cuda")
+    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, keys.size, out, CLUSTER) == CLUSTER
+    got = out.cpu().numpy()
+    want = oracle.min_query(c, seeds, keys.astype(np.uint64))
+    np.testing.assert_array_equal(got, want)
+    assert (got[:1000] >= 65535).all()
+
+
+@pytest.mark.parametrize("path", [L2, CLUSTER])
+def test_query_paths_misaligned_views(oracle, path):
+    d, w, n = 4, 65536, 200_001
+    rng = np.random.default_rng(11)
+    c = table(rng, d, w, 1 << 17)
+    seeds = seed_array(1, 0, d)
+    keys = rng.integers(0, 1 << 32, size=n + 3, dtype=np.uint64).astype(np.uint32)
+    kt = torch.from_numpy(keys).cuda()[1:n + 1]          # 4-B aligned only
+    out_base = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    out = out_base[1:]                                   # 8-B aligned only
+    ct = torch.from_numpy(c).cuda()
+    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, n, out, path) == path
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, keys[1:n + 1].astype(np.uint64)))
+
+
+@pytest.mark.parametrize("path", [L2, SMEM, CLUSTER])
+def test_query_paths_u64_and_record_keys(oracle, path):
+    d, w, n = 4, 16384 if path != SMEM else 12800, 150_000
+    rng = np.random.default_rng(5)
+    c = table(rng, d, w, 1 << 32)
+    seeds = seed_array(99, 0, d)
+    ct = torch.from_numpy(c).cuda()
+    k64 = rng.integers(0, np.iinfo(np.uint64).max, size=n, dtype=np.uint64)
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    assert run_query(ct, seeds, torch.from_numpy(k64).cuda(), _lib.KEY_U64, 0, n, out, path) == path
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, k64))
+    recs = rng.integers(0, 256, size=(n, 13), dtype=np.uint8)
+    assert run_query(ct, seeds, torch.from_numpy(recs.reshape(-1)).cuda(), _lib.KEY_RECORD, 13, n, out,
+                     path) == path
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, oracle.keys_from_records(recs)))
+
+
+def test_auto_path_picks_cluster_for_cfg5_shape():
+    d, w, n = 4, 65536, 1 << 22
+    c = torch.zeros((d, w), dtype=torch.uint32, device="cuda")
+    seeds = seed_array(2017, 0, d)
+    keys = torch.zeros(n, dtype=torch.uint32, device="cuda")
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    assert run_query(c, seeds, keys, _lib.KEY_U32, 0, n, out, 0) == CLUSTER
+    assert int(out.max()) == 0
