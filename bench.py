@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--alpha-q", type=float, default=1.0, help="query rank skew (cfg 5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cm", action="store_true", help="skip the cfg-2 CM merge leg")
     return ap.parse_args()
 
 
@@ -131,6 +132,17 @@ class ClockSampler:
         return out
 
 
+def ncu_traffic(name, units):
+    """DRAM bytes per launch of `name` scaled from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        e = json.load(fh).get(name)
+    return None if e is None else int(e["bytes_per_unit"] * units)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
@@ -202,6 +214,60 @@ def run_reference(args):
         "e2e": {"value": round(value, 3), "unit": "Mitems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ CM merge leg
+def run_cm_leg(args, world, rank, dev):
+    """cfg 2 count-min build: every rank applies its contiguous slice of the
+    10M-op stream (warp-aggregated atomics) and the replicas are summed with
+    one NCCL all-reduce (distributed.sharded_cm_apply). Timed like the
+    headline (CUDA events, max over ranks), not part of `value`."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1701_04148_b200 as P
+    from paper_1701_04148_b200 import distributed as Dd, workloads as Wl
+
+    c = Wl.cfg2(seed=SEED)
+    ops_d = torch.from_numpy(c["ops"]).to(dev)
+    keys_d = torch.from_numpy(c["keys"]).to(dev)
+    cm = P.CmSketch(P.SketchParams(d=D, w=W, master_seed=SEED))
+    times = []
+    for k in range(args.warmup + args.steps):
+        cm.counters.zero_()
+        cm.increment_counts.zero_()
+        cm.insertions_seen = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if world > 1:
+            Dd.sharded_cm_apply(cm, ops_d, keys_d)
+        else:
+            cm.apply_ops(ops_d, keys_d)
+        e1.record()
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            times.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    n = int(c["ops"].shape[0])
+    out = {"workload": "cfg2 CM d=4 w=65536, 10M inserts Zipf(1.0) over 1M distinct uint32 keys, stream sharded "
+                       "over %d GPU(s) + NCCL sum all-reduce of the counters" % world,
+           "ms": round(ms, 3), "Mitems_s": round(n / (ms * 1e-3) / 1e6, 2), "ops": n}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+
+        o = orc.OracleSketch("cm", D, W, master_seed=SEED)
+        t0 = time.perf_counter()
+        o.apply_ops(c["ops"], c["keys"].astype(np.uint64))
+        out["cpu_port_Mitems_s"] = round(n / (time.perf_counter() - t0) / 1e6, 2)
+        assert np.array_equal(cm.counters.cpu().numpy(), o.slim), "CM counters differ from the oracle"
+        out["parity"] = "counters bit-exact vs oracle"
+    return out
 
 
 # ------------------------------------------------------------------ our arm
@@ -307,17 +373,24 @@ def run_ours(args):
     # per-kernel rooflines from CUDA events on the launching stream
     q_s = float(tot[2]) / args.steps * 1e-3
     achieved_gbs = qn * 12 / q_s / 1e9
+    qpath = int(L.sfk_query_last_path())
+    qkern = {1: "min_query_l2 (fused key load + 4x hash + 4 L2 gathers + min + int64 store)",
+             2: "min_query_smem (whole slim in one SM's shared memory)",
+             3: "min_query_cluster<4,u16> (4-CTA cluster, one slim row per CTA in smem, DSMEM st.async "
+                "partials, min + int64 store)"}.get(qpath, "?")
     rf_query = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved_gbs / hbm, 4), "traffic": None,
-                "kernel": "min_query_l2 (fused key load + 4x hash + 4 gathers + min + int64 store)",
+                "frac": round(achieved_gbs / hbm, 4),
+                "traffic": ncu_traffic("query_cluster", qn) if qpath == 3 else None, "kernel": qkern,
                 "algorithmic_bytes_per_launch": int(qn * 12), "launch_ms": round(q_s * 1e3, 3),
                 "peak_source": hbm_src}
     if gather:
-        gpk = float(gather.get("gather_1MiB_Gps", 0.0))
+        # the gather level the path reads from: L2 for path 1, shared memory otherwise
+        key, lvl = ("gather_1MiB_Gps", "L2, 1 MiB table") if qpath == 1 else ("gather_smem128KiB_Gps", "smem")
+        gpk = float(gather.get(key, 0.0))
         gachieved = qn * 4 / q_s / 1e9
         rf_query["gather"] = {"achieved_Gps": round(gachieved, 1), "peak_Gps": gpk,
                               "frac": round(gachieved / gpk, 4) if gpk else None,
-                              "peak_source": "profiles/gather_peaks.json (random 4-B loads, 1 MiB table, L2)"}
+                              "peak_source": f"profiles/gather_peaks.json (random 4-B loads, {lvl})"}
     rf = {"query": rf_query}
     eng_ms = float(tot[3]) / args.steps
     if rank == 0 and eng_ms > 0:
@@ -326,7 +399,7 @@ def run_ours(args):
         eng_bytes = runs * (12 + 16 * D + 16 * D) + n_ops / 8
         ach = eng_bytes / (eng_ms * 1e-3) / 1e9
         rf["engine"] = {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
-                        "frac": round(ach / hbm, 5), "traffic": None,
+                        "frac": round(ach / hbm, 5), "traffic": ncu_traffic("engine_sff", runs),
                         "kernel": "poll_engine_k<4,2> (ordered slim engine, SFF)",
                         "algorithmic_bytes_per_launch": int(eng_bytes), "launch_ms": round(eng_ms, 3),
                         "runs_per_launch": int(runs), "peak_source": hbm_src,
@@ -377,6 +450,9 @@ def run_ours(args):
         # the estimates must equal the device-resident run's
         assert torch.equal(qo_h.to(dev), qout), "e2e estimates differ from device-resident run"
 
+    # ------------------------------------------------ CM merge leg (cfg 2), reported beside the headline
+    cm_leg = None if args.no_cm else run_cm_leg(args, world, rank, dev)
+
     # ------------------------------------------------ parity gate + CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0:
@@ -400,7 +476,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
             "config": workload_config(args, world), "breakdown": breakdown, "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "cpu_baseline": cpu, "e2e": e2e, "cm_merge": cm_leg, "gpu_launches": int(launches),
             "gpu_launches_note": "own kernels only (sfk_launch_count); CUB radix-sort/scan launches not counted",
             "clocks": clk,
         }

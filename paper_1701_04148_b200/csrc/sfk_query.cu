@@ -2,7 +2,7 @@
 // (replaces _kernels.min_query, _kernels.py:229-241), plus mix_batch
 // (_kernels.py:56-59) and key materialisation.
 //
-// Two kernels, chosen per call:
+// Three kernels, chosen per call:
 //   * L2 path: the counters stay in global memory (L2-resident for the
 //     configs' 256 KiB - 1 MiB tables); every thread answers UNR keys per
 //     iteration so UNR*d independent gathers are in flight.
@@ -16,9 +16,9 @@
 //     Each CTA hashes every key of a tile for its own row and gathers locally;
 //     the per-row partial counters meet over DSMEM, where CTA r takes the min
 //     for its quarter of the tile and stores the int64 estimates. Rows wider
-//     than 16 bits are stored clamped to 0xFFFF; a clamped min of 0xFFFF
-//     means the true min is >= 65535 and that key re-gathers its d u32
-//     counters from global memory, so estimates stay exact.
+//     than 16 bits are stored as u16 codes: small values as is, large ones
+//     (>= 0xF000) as an index into a per-CTA overflow array of exact u32
+//     values, so estimates stay exact (see OVF_BASE).
 #include <cooperative_groups.h>
 
 #include "sfk_common.cuh"
@@ -111,147 +111,338 @@ int query_path(int mode) {
 }
 int query_last_path() { return g_query_last; }
 
-template <typename CT>
-__device__ __forceinline__ CT clamp_ct(uint32_t v) {
-  return sizeof(CT) == 2 ? (CT)min(v, 0xFFFFu) : (CT)v;
+// ---- cluster path: PTX helpers (mbarrier, DSMEM st.async) -------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_arrive(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+// arrive on a peer CTA's mbarrier. Relaxed: it only signals that this CTA's
+// reads of a receive buffer are done, and those reads have already returned
+// (their values were consumed before the __syncthreads preceding the arrive);
+// a .release arrive would cost a GPU-scope MEMBAR per tile.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  } while (!done);
+}
+// asynchronous remote store that completes `bytes` of the peer's mbarrier tx
+__device__ __forceinline__ void st_async_v2(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t cluster_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(cluster_addr),
+               "r"(a), "r"(b), "r"(cluster_mbar) : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t cluster_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(cluster_mbar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Vector of 4 counters of type CT (u16 -> 8 B, u32 -> 16 B).
-template <typename CT>
-struct V4;
-template <>
-struct V4<uint16_t> {
-  using T = uint2;
-  __device__ static void unpack(const uint2& v, uint32_t o[4]) {
-    o[0] = v.x & 0xFFFFu; o[1] = v.x >> 16; o[2] = v.y & 0xFFFFu; o[3] = v.y >> 16;
+// Row index for the cluster kernel: the low 32 bits of finalize64(key ^ seed)
+// suffice for a power-of-two width (x ^ (x >> 31) masked), else the exact
+// 64-bit reduction.
+template <bool POW2>
+__device__ __forceinline__ uint32_t row_index(uint64_t key, uint64_t seed, const Mod& M) {
+  if (POW2) {
+    uint64_t x = key ^ seed;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return ((uint32_t)x ^ (uint32_t)(x >> 31)) & (uint32_t)M.mask;
   }
-  __device__ static uint2 pack(const uint32_t o[4]) { return make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16)); }
-};
-template <>
-struct V4<uint32_t> {
-  using T = uint4;
-  __device__ static void unpack(const uint4& v, uint32_t o[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-  __device__ static uint4 pack(const uint32_t o[4]) { return make_uint4(o[0], o[1], o[2], o[3]); }
-};
+  return (uint32_t)fmod64(mix64(key ^ seed), M);
+}
 
-// One cluster of D CTAs; TILE keys per cluster iteration; NT threads per CTA.
-// Shared memory: [row r: w x CT, 16-B padded][partials: 2 x TILE x CT].
-template <int D, typename CT, int TILE, int NT>
+// u16 row encoding: values below OVF_BASE are stored as is; a larger value
+// gets the code OVF_BASE + s and its exact u32 value in overflow slot s of
+// its row; OVF_NONE marks a large value that found no slot (re-read from
+// global memory). Codes order below every large value, so a min over codes
+// that is < OVF_BASE is the exact min. Every CTA keeps a copy of all D rows'
+// overflow tables (a few hot cells each), so decoding stays in local smem.
+constexpr uint32_t OVF_BASE = 0xF800u;
+constexpr uint32_t OVF_NONE = 0xFFFFu;
+constexpr int OVF_SLOTS = (int)(OVF_NONE - OVF_BASE);  // 2047 per row
+constexpr int OVF_STRIDE = OVF_SLOTS + 1;               // + the slot count
+constexpr int QNB = 2;                                 // receive buffers per CTA
+
+template <int KK>
+__device__ __forceinline__ uint64_t key_at(const KeySrc& k, int64_t t) {
+  if (KK == SFK_KEY_U32) return (uint64_t)__ldg(static_cast<const unsigned int*>(k.p) + t);
+  if (KK == SFK_KEY_U64) return __ldg(static_cast<const unsigned long long*>(k.p) + t);
+  return record_key(static_cast<const uint8_t*>(k.p) + t * (int64_t)k.rec, k.rec);
+}
+
+// Row-partitioned cluster query. A cluster of D CTAs; CTA r holds slim row r
+// in shared memory. Per tile of TILE keys (the cluster's tiles are strided
+// over the grid's clusters):
+//   phase 1 (every CTA): row-r counter of each key; the partials of the keys
+//     CTA q owns (the q-th 1/D of the tile) go to CTA q's receive buffer with
+//     st.async, which completes bytes on CTA q's `full` mbarrier;
+//   phase 2 (owner q, one tile behind phase 1 so the transfers overlap the
+//     hashing): wait `full`, min over the D partials, decode large values,
+//     int64 stores; then release the buffer with a remote arrive on every
+//     producer's `empty` mbarrier.
+// Shared memory: [row: w x CT][overflow: D x OVF_STRIDE u32, u16 rows only]
+// [recv: QNB x D x Q x CT][mbarriers: full[QNB], empty[QNB]].
+template <int D, typename CT, int TILE, int NT, int KK, bool VEC, bool POW2>
 __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __restrict__ counters, Seeds<D> seeds,
                                                            Mod wm, int64_t w, KeySrc keys, int64_t n,
-                                                           int64_t* __restrict__ out, int vec_ok) {
-  extern __shared__ uint4 smem_c[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int r = (int)cl.block_rank();
-  CT* row = reinterpret_cast<CT*>(smem_c);
+                                                           int64_t* __restrict__ out, int out_vec) {
+  constexpr bool U16 = sizeof(CT) == 2;
+  constexpr int KPT = TILE / NT;  // keys per thread per tile (phase 1)
+  constexpr int VPT = KPT / 4;    // 4-key groups per thread
+  constexpr int Q = ((TILE + D - 1) / D + 3) & ~3;
+  static_assert(TILE % (4 * NT) == 0, "tile shape");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t r = cg::this_cluster().block_rank();
+  CT* row = reinterpret_cast<CT*>(smem_raw);
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
-  CT* part = reinterpret_cast<CT*>(reinterpret_cast<char*>(smem_c) + row_bytes);
-  // stage row r (16-B loads when the row start is aligned)
-  const uint32_t* src = counters + (int64_t)r * w;
-  int64_t k0 = 0;
-  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    const int64_t nv = w / 4;
-    for (int64_t k = threadIdx.x; k < nv; k += NT) {
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + k);
-      row[4 * k] = clamp_ct<CT>(v.x); row[4 * k + 1] = clamp_ct<CT>(v.y);
-      row[4 * k + 2] = clamp_ct<CT>(v.z); row[4 * k + 3] = clamp_ct<CT>(v.w);
+  uint32_t* ovf = reinterpret_cast<uint32_t*>(smem_raw + row_bytes);
+  CT* recv = reinterpret_cast<CT*>(smem_raw + row_bytes + (U16 ? D * OVF_STRIDE * 4 : 0));
+  uint32_t* my_ovf = ovf + r * OVF_STRIDE;
+  int& novf = *reinterpret_cast<int*>(my_ovf + OVF_SLOTS);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(recv + (size_t)QNB * D * Q);
+  // bars[0..QNB) = full, bars[QNB..2QNB) = empty
+  if (threadIdx.x == 0) {
+    novf = 0;
+    for (int b = 0; b < QNB; ++b) {
+      mbar_init(smem_addr(bars + b), 1);
+      mbar_init(smem_addr(bars + QNB + b), D);
     }
-    k0 = nv * 4;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int64_t k = k0 + threadIdx.x; k < w; k += NT) row[k] = clamp_ct<CT>(__ldg(src + k));
+  __syncthreads();
+  // stage row r (u16 rows: large values into the overflow slots)
+  const uint32_t* src = counters + (int64_t)r * w;
+  for (int64_t k = threadIdx.x; k < w; k += NT) {
+    uint32_t v = __ldg(src + k);
+    if (U16 && v >= OVF_BASE) {
+      int s = atomicAdd(&novf, 1);
+      if (s < OVF_SLOTS) {
+        my_ovf[s] = v;
+        v = OVF_BASE + (uint32_t)s;
+      } else {
+        v = OVF_NONE;
+      }
+    }
+    row[k] = (CT)v;
+  }
   uint64_t seed = seeds.s[0];
 #pragma unroll
   for (int i = 1; i < D; ++i)
-    if (i == r) seed = seeds.s[i];
-  const CT* rpart[D];
+    if (i == (int)r) seed = seeds.s[i];
+  const uint32_t recv_a = smem_addr(recv), bars_a = smem_addr(bars);
+  uint32_t peer_recv[D], peer_full[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) rpart[i] = cl.map_shared_rank(part, i);
-  cl.sync();
+  for (int q = 0; q < D; ++q) {
+    peer_recv[q] = mapa_u32(recv_a, q);
+    peer_full[q] = mapa_u32(bars_a, q);
+  }
+  cluster_sync_all();  // rows staged, barriers initialised cluster-wide
+  if (U16) {  // copy the peers' overflow tables
+#pragma unroll 1
+    for (int q = 0; q < D; ++q) {
+      if (q == (int)r) continue;
+      const uint32_t* pt = cg::this_cluster().map_shared_rank(ovf + q * OVF_STRIDE, q);
+      const int cnt = min(pt[OVF_SLOTS], OVF_SLOTS);
+      for (int s = threadIdx.x; s < cnt; s += NT) ovf[q * OVF_STRIDE + s] = pt[s];
+    }
+    __syncthreads();
+  }
 
   const int64_t ntiles = (n + TILE - 1) / TILE;
   const int64_t nclusters = gridDim.x / D;
-  constexpr int Q = ((TILE + D - 1) / D + 3) & ~3;  // keys each CTA finalises per tile
-  static_assert(TILE % (4 * NT) == 0, "tile shape");
-  const int kend = min((r + 1) * Q, TILE);
-  const bool u32v = vec_ok && keys.kind == SFK_KEY_U32;
-  int it = 0;
-  for (int64_t tile = blockIdx.x / D; tile < ntiles; tile += nclusters, ++it) {
-    const int64_t base = tile * TILE;
-    CT* P = part + (it & 1) * TILE;
-    // phase 1: this CTA's row counter for every key of the tile, 4
-    // consecutive keys per thread per step (one 16-B key load for u32 keys)
-#pragma unroll 2
-    for (int k = 4 * threadIdx.x; k < TILE; k += 4 * NT) {
-      const int64_t t = base + k;
-      uint32_t c[4];
-      if (u32v && t + 3 < n) {
-        uint4 kk = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(keys.p) + t));
-        c[0] = row[fmod64(mix64((uint64_t)kk.x ^ seed), wm)];
-        c[1] = row[fmod64(mix64((uint64_t)kk.y ^ seed), wm)];
-        c[2] = row[fmod64(mix64((uint64_t)kk.z ^ seed), wm)];
-        c[3] = row[fmod64(mix64((uint64_t)kk.w ^ seed), wm)];
+  const int64_t cid = blockIdx.x / D;
+  const int64_t T = cid < ntiles ? (ntiles - 1 - cid) / nclusters + 1 : 0;  // tiles of this cluster
+  const int own_lo = (int)r * Q, own_hi = min(((int)r + 1) * Q, TILE);
+  const int owned = max(own_hi - own_lo, 0);
+  const uint32_t* k32 = static_cast<const uint32_t*>(keys.p);
+
+  uint4 kn[VEC ? VPT : 1];
+  auto prefetch = [&](int64_t it) {
+    if (VEC && it < T) {
+      const int64_t base = (cid + it * nclusters) * TILE;
+      const uint4* src4 = reinterpret_cast<const uint4*>(k32 + base) + threadIdx.x;
+      if (base + TILE <= n) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) kn[j] = __ldcs(src4 + j * NT);
       } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          c[u] = (t + u < n) ? (uint32_t)row[fmod64(mix64(load_key(keys, t + u) ^ seed), wm)] : 0u;
-      }
-      *reinterpret_cast<typename V4<CT>::T*>(P + k) = V4<CT>::pack(c);
-    }
-    cl.sync();
-    // phase 2: min over the D partials for keys [r*Q, (r+1)*Q) of the tile
-    const CT* PP[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) PP[i] = rpart[i] + (it & 1) * TILE;
-    for (int k = r * Q + 4 * threadIdx.x; k < kend; k += 4 * NT) {
-      const int64_t t = base + k;
-      if (t >= n) break;
-      uint32_t m[4], c[4];
-      V4<CT>::unpack(*reinterpret_cast<const typename V4<CT>::T*>(PP[0] + k), m);
-#pragma unroll
-      for (int i = 1; i < D; ++i) {
-        V4<CT>::unpack(*reinterpret_cast<const typename V4<CT>::T*>(PP[i] + k), c);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) m[u] = min(m[u], c[u]);
-      }
-      if (sizeof(CT) == 2) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (m[u] == 0xFFFFu && t + u < n) {  // true min >= 65535: exact u32 re-gather
-            const uint64_t key = load_key(keys, t + u);
-            uint32_t mm = U32MAX;
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-              mm = min(mm, __ldg(counters + (int64_t)i * w + (int64_t)fmod64(mix64(key ^ seeds.s[i]), wm)));
-            m[u] = mm;
-          }
+        for (int j = 0; j < VPT; ++j) {
+          const int64_t t = base + 4 * threadIdx.x + (int64_t)j * 4 * NT;
+          kn[j] = (t + 3 < n) ? __ldcs(src4 + j * NT) : make_uint4(0, 0, 0, 0);
         }
       }
-      if (vec_ok && t + 3 < n) {
-        longlong2* o2 = reinterpret_cast<longlong2*>(out + t);
-        __stcs(o2, make_longlong2((long long)m[0], (long long)m[1]));
-        __stcs(o2 + 1, make_longlong2((long long)m[2], (long long)m[3]));
+    }
+  };
+  prefetch(0);
+
+  for (int64_t i = 0; i <= T; ++i) {
+    if (i < T) {
+      // ---------------- phase 1: tile i into buffer i % QNB of every owner
+      const int b = (int)(i % QNB);
+      if (threadIdx.x == 0) mbar_expect_arrive(bars_a + b * 8, (uint32_t)(D * owned * sizeof(CT)));
+      if (i >= QNB) mbar_wait(bars_a + (QNB + b) * 8, (uint32_t)((i / QNB - 1) & 1));  // owners released it
+      const int64_t base = (cid + i * nclusters) * TILE;
+      uint4 kk[VEC ? VPT : 1];
+      if (VEC) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) kk[j] = kn[j];
+        prefetch(i + 1);
+      }
+      // all VPT x 4 row counters first (independent hash chains and smem
+      // gathers in flight together), then the D-way scatter with st.async
+      uint32_t c[VPT][4];
+      if (VEC && base + TILE <= n) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          c[j][0] = row[row_index<POW2>(VEC ? kk[j].x : 0u, seed, wm)];
+          c[j][1] = row[row_index<POW2>(VEC ? kk[j].y : 0u, seed, wm)];
+          c[j][2] = row[row_index<POW2>(VEC ? kk[j].z : 0u, seed, wm)];
+          c[j][3] = row[row_index<POW2>(VEC ? kk[j].w : 0u, seed, wm)];
+        }
       } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (t + u < n) out[t + u] = (int64_t)m[u];
+        for (int j = 0; j < VPT; ++j) {
+          const int64_t t = base + 4 * threadIdx.x + j * 4 * NT;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            c[j][u] = (t + u < n) ? (uint32_t)row[row_index<POW2>(key_at<KK>(keys, t + u), seed, wm)] : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int k = 4 * threadIdx.x + j * 4 * NT;
+        // owner of keys k .. k+3 (Q is a multiple of 4); compile-time when
+        // each thread's 4-key groups map one-to-one onto the D owners
+        const int q = (Q == 4 * NT) ? j : k / Q;
+        uint32_t qa = 0, qb = 0;
+#pragma unroll
+        for (int p = 0; p < D; ++p)
+          if (p == q) qa = peer_recv[p], qb = peer_full[p];
+        const uint32_t off = (uint32_t)((((size_t)b * D + r) * Q + (k - q * Q)) * sizeof(CT));
+        if (U16)
+          st_async_v2(qa + off, c[j][0] | (c[j][1] << 16), c[j][2] | (c[j][3] << 16), qb + b * 8);
+        else
+          st_async_v4(qa + off, c[j][0], c[j][1], c[j][2], c[j][3], qb + b * 8);
+      }
+    }
+    if (i >= 1) {
+      // ---------------- phase 2: tile i-1 from buffer (i-1) % QNB
+      const int64_t ip = i - 1;
+      const int b = (int)(ip % QNB);
+      mbar_wait(bars_a + b * 8, (uint32_t)((ip / QNB) & 1));
+      const int64_t base = (cid + ip * nclusters) * TILE + own_lo;
+      const CT* R = recv + (size_t)b * D * Q;
+      for (int k = 4 * threadIdx.x; k < owned; k += 4 * NT) {
+        const int64_t t = base + k;
+        if (t >= n) break;
+        uint32_t cc[D][4], m[4];
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+          if (U16) {
+            const uint2 v = *reinterpret_cast<const uint2*>(R + (size_t)p * Q + k);
+            cc[p][0] = v.x & 0xFFFFu; cc[p][1] = v.x >> 16; cc[p][2] = v.y & 0xFFFFu; cc[p][3] = v.y >> 16;
+          } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(R + (size_t)p * Q + k);
+            cc[p][0] = v.x; cc[p][1] = v.y; cc[p][2] = v.z; cc[p][3] = v.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          m[u] = cc[0][u];
+#pragma unroll
+          for (int p = 1; p < D; ++p) m[u] = min(m[u], cc[p][u]);
+        }
+        if (U16) {
+          // keys whose every row holds a large value: decode all of their
+          // codes in one batch of predicated local loads
+          bool need[4], any = false;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            need[u] = m[u] >= OVF_BASE && t + u < n;
+            any |= need[u];
+          }
+          if (any) {
+            uint32_t v[D][4];
+            bool none = false;
+#pragma unroll
+            for (int p = 0; p < D; ++p)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const bool slot = need[u] && cc[p][u] != OVF_NONE;
+                v[p][u] = slot ? ovf[p * OVF_STRIDE + (cc[p][u] - OVF_BASE)] : U32MAX;
+                none |= need[u] && !slot;
+              }
+            if (none) {  // overflow slots exhausted for some row: exact global re-read
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (!need[u]) continue;
+                const uint64_t key = key_at<KK>(keys, t + u);
+#pragma unroll
+                for (int p = 0; p < D; ++p)
+                  if (cc[p][u] == OVF_NONE)
+                    v[p][u] = __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (!need[u]) continue;
+              uint32_t mm = v[0][u];
+#pragma unroll
+              for (int p = 1; p < D; ++p) mm = min(mm, v[p][u]);
+              m[u] = mm;
+            }
+          }
+        }
+        if (out_vec && t + 3 < n) {
+          longlong2* o2 = reinterpret_cast<longlong2*>(out + t);
+          __stcs(o2, make_longlong2((long long)m[0], (long long)m[1]));
+          __stcs(o2 + 1, make_longlong2((long long)m[2], (long long)m[3]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (t + u < n) out[t + u] = (int64_t)m[u];
+        }
+      }
+      // release the buffer to every producer, unless nobody will refill it
+      if (ip + QNB < T) {
+        __syncthreads();
+        if (threadIdx.x < D) mbar_arrive_remote(mapa_u32(bars_a + (QNB + b) * 8, threadIdx.x));
       }
     }
   }
-  cl.sync();  // no CTA may exit while a peer still reads its partials
+  cluster_sync_all();  // no CTA exits while peers may still touch its shared memory
 }
 
 // Launch the cluster kernel if this (d, w, n) suits it; returns -1 if not.
-template <int D, typename CT, int TILE>
-static int try_cluster(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
-                       int64_t* out, cudaStream_t st, int optin) {
-  constexpr int NT = 1024;
+template <int D, typename CT, int TILE, int KK, bool VEC, bool POW2>
+static int try_cluster_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                         int64_t* out, cudaStream_t st, int optin) {
+  constexpr int NT = 512;
+  constexpr int Q = ((TILE + D - 1) / D + 3) & ~3;
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
-  const size_t smem = row_bytes + 2 * (size_t)TILE * sizeof(CT);
-  if (smem > (size_t)optin) return -1;
-  auto kern = min_query_cluster<D, CT, TILE, NT>;
+  const size_t smem = row_bytes + (sizeof(CT) == 2 ? D * OVF_STRIDE * 4 : 0) + (size_t)QNB * D * Q * sizeof(CT) +
+                      2 * QNB * 8;
+  if (smem + 1024 > (size_t)optin) return -1;
+  auto kern = min_query_cluster<D, CT, TILE, NT, KK, VEC, POW2>;
   static int attr_done = 0;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess) {
       cudaGetLastError();
       return -1;
     }
@@ -277,16 +468,37 @@ static int try_cluster(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int
   const int64_t ntiles = (n + TILE - 1) / TILE;
   if ((int64_t)nclusters > ntiles) nclusters = (int)ntiles;
   cfg.gridDim = dim3(D * nclusters);
-  const int vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) &&
-                     (ks.kind != SFK_KEY_U32 || (reinterpret_cast<uintptr_t>(ks.p) & 15) == 0);
+  const int out_vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   note_launch();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, counters, sd, wm, w, ks, n, out, vec_ok);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, counters, sd, wm, w, ks, n, out, out_vec);
   if (e != cudaSuccess) {
     set_error("min_query_cluster launch: %s", cudaGetErrorString(e));
     return (int)e;
   }
   g_query_last = 3;
   return check_launch("min_query_cluster");
+}
+
+template <int D, typename CT, int TILE, bool POW2>
+static int try_cluster_p(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                         int64_t* out, cudaStream_t st, int optin) {
+  if (ks.kind == SFK_KEY_U32) {
+    // 512 threads x 16 keys each per tile measured faster than 1024 x 8
+    if ((reinterpret_cast<uintptr_t>(ks.p) & 15) == 0)
+      return try_cluster_k<D, CT, TILE, SFK_KEY_U32, true, POW2>(counters, sd, wm, w, ks, n, out, st, optin);
+    return try_cluster_k<D, CT, TILE, SFK_KEY_U32, false, POW2>(counters, sd, wm, w, ks, n, out, st, optin);
+  }
+  if (ks.kind == SFK_KEY_U64)
+    return try_cluster_k<D, CT, TILE, SFK_KEY_U64, false, POW2>(counters, sd, wm, w, ks, n, out, st, optin);
+  return try_cluster_k<D, CT, TILE, SFK_KEY_RECORD, false, POW2>(counters, sd, wm, w, ks, n, out, st, optin);
+}
+
+template <int D, typename CT, int TILE>
+static int try_cluster(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                       int64_t* out, cudaStream_t st, int optin) {
+  if (wm.pow2 && w <= (int64_t(1) << 32))
+    return try_cluster_p<D, CT, TILE, true>(counters, sd, wm, w, ks, n, out, st, optin);
+  return try_cluster_p<D, CT, TILE, false>(counters, sd, wm, w, ks, n, out, st, optin);
 }
 
 // Any d up to MAXSEEDS: seeds passed by value.
@@ -343,10 +555,10 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
   // pays once the batch is well beyond the per-CTA row staging (~2M keys)
   if (D >= 2 && D <= 8 && ((mode == 0 && !smem_fits && n >= (int64_t(1) << 21)) || mode == 3)) {
     int rc = -1;
-    if ((size_t)w * 4 + 2 * 8192 * 4 + 16 <= (size_t)optin)
+    if ((size_t)w * 4 + 2 * 8192 * 4 + 64 + 1024 <= (size_t)optin)
       rc = try_cluster<D, uint32_t, 8192>(counters, sd, wm, w, ks, n, out, st, optin);
     else
-      rc = try_cluster<D, uint16_t, 16384>(counters, sd, wm, w, ks, n, out, st, optin);
+      rc = try_cluster<D, uint16_t, 8192>(counters, sd, wm, w, ks, n, out, st, optin);
     if (rc >= 0) return rc;
   }
   int blocks = grid_for(n, 256 * 4, sms * 8);
