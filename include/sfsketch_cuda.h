@@ -74,7 +74,8 @@ unsigned long long sfk_launch_count(void);
 
 /* Diagnostics of the ordered slim engine, summed over launches since the last
  * reset: out8 = {words on the gap path, words on the steady path, words
- * replayed op by op, replay cycles, runs executed, warp iterations, 0, 0}. */
+ * replayed op by op, replay cycles, runs executed, warp iterations, long-run
+ * pieces applied, ops finished by long-run pieces}. */
 int sfk_engine_stats(unsigned long long* out8, int reset);
 
 /* Bench instrumentation: when on, CUDA events bracket every launch of the

@@ -45,6 +45,10 @@ constexpr int ENGINE_BLOCKS_PER_SM = 1;
 // default replay budget: a long run never stalls the other lanes of its warp
 // for more than ~this many ops
 constexpr uint32_t REPLAY_BUDGET = 1024;
+// engine run claiming: run ids per warp atomic, and how far ahead of a claim
+// the run records are prefetched into L2
+constexpr uint32_t CLAIM_POOL = 64;
+constexpr uint32_t CLAIM_PREFETCH = 16384;
 
 static uint32_t engine_budget() {
   static int v = -1;
@@ -504,6 +508,16 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
 __device__ unsigned long long g_engine_stats[8];
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+struct RowMap {
+  int32_t l, u, p0, pW;
+};
+struct WalkPiece {
+  int32_t S, mx;  // net steps (delete +1 / insert -1) and max prefix (dominance over the piece)
+};
+constexpr int32_t MAP_INF = 0x3fffffff;
+constexpr uint32_t NO_OWNER = 0xFFFFFFFFu;
+constexpr int MAP_LEVELS = 3;  // pieces of 1, 32 and 1024 words
+
 template <int D>
 struct EngineArgs {
   unsigned long long* slim64;  // (seq << 32 | value) per slim cell
@@ -511,6 +525,8 @@ struct EngineArgs {
   const uint32_t* opdata;      // SF1: b_min per op (row-0 order)
   const uint32_t* delbits;     // SFF: delete flags in row-0 order, one bit per op
   const uint32_t* wsum;        // SFF: per aligned word, nd | -min prefix << 6 | max prefix << 12 | draw-up << 18
+  const WalkPiece* piece[3];   // SFF long runs: pieces of 1, 32, 1024 aligned words (word_maps_k, block_maps_k)
+  const RowMap* rmap[3];       //   and their per-row reflected-walk maps (null: no long-run path)
   Ctl* ctl;
   unsigned long long* inc;     // int64[d] tallies (two's complement add)
   uint32_t budget;             // ops a lane replays per engine iteration before it yields
@@ -618,6 +634,167 @@ __global__ void __launch_bounds__(256) word_sums_k(const uint32_t* __restrict__ 
   }
 }
 
+// ---- reflected-walk maps for long SFF runs ----------------------------------
+// Inside a run in the steady regime (m == A0 + x) with the key's own slot
+// dominating its buckets (O_i <= A_i + x), every row evolves on its own as a
+// two-sided reflected walk v -> [0, W_i] (v_i = c_i - A0 - x, W_i = A_i - A0):
+// an insert maps v -> max(v - 1, 0) (a push at 0 is one raise), a delete
+// v -> min(v + 1, W_i). Any stretch of such steps acts on [0, W] as
+// h(v) = min(max(v + S, l), u) and raises p(v) = pW + max(p0 - pW - v, 0)
+// times (coupling: paths from v and v + 1 stay one apart until the lower one
+// is pushed or the upper one capped; lower pushes come first for small v).
+// Both compose in O(1), so the engine finishes a long run by applying a few
+// precomputed pieces (32-op words, 1024-op and 32768-op blocks) instead of
+// replaying it op by op.
+
+__device__ __forceinline__ int32_t rowmap_apply(const RowMap& f, int32_t S, int32_t v) {
+  return min(max(v + S, f.l), f.u);
+}
+__device__ __forceinline__ int32_t rowmap_push(const RowMap& f, int32_t v) {
+  return f.pW + max(f.p0 - f.pW - v, 0);
+}
+// f (net S1) followed by g (net S2), on [0, W]
+__device__ __forceinline__ RowMap rowmap_cat(const RowMap& f, int32_t S1, const RowMap& g, int32_t S2, int32_t W) {
+  RowMap h;
+  int32_t L = max(f.l + S2, g.l);
+  int32_t U = min(max(f.u + S2, g.l), g.u);
+  if (L > U) L = U;
+  h.l = max(L, -MAP_INF);
+  h.u = min(U, MAP_INF);
+  h.p0 = f.p0 + rowmap_push(g, rowmap_apply(f, S1, 0));
+  h.pW = f.pW + rowmap_push(g, rowmap_apply(f, S1, W));
+  return h;
+}
+
+// owner of every aligned word of a long SFF run (hasdel, L > 32): the run id
+template <int D>
+__global__ void __launch_bounds__(256) long_owner_k(const RunRec<D>* __restrict__ recs, const Ctl* __restrict__ ctl,
+                                                    uint32_t* __restrict__ wowner) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t R = ctl->n_runs;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = warp * 32u; base < R; base += nwarps * 32u) {
+    const uint32_t r = base + lane;
+    uint32_t wa = 1, wl = 0;
+    if (r < R) {
+      const uint32_t e0 = recs[r].e0, info = recs[r].info, L = info & 0x7fffffffu;
+      if ((info >> 31) && L > 32u) wa = (e0 + 31u) >> 5, wl = (e0 + L - 1u) >> 5;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, wa <= wl);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const uint32_t a0 = __shfl_sync(0xffffffffu, wa, src), a1 = __shfl_sync(0xffffffffu, wl, src);
+      const uint32_t rr = base + (uint32_t)src;
+      for (uint32_t w = a0 + lane; w <= a1; w += 32u) wowner[w] = rr;
+    }
+  }
+}
+
+// validated owner of word w (stale entries from earlier calls never match)
+template <int D>
+__device__ __forceinline__ uint32_t word_owner(const uint32_t* wowner, const RunRec<D>* recs, uint32_t R, uint32_t w,
+                                               uint32_t& e0, uint32_t& L) {
+  const uint32_t r = wowner[w];
+  if (r >= R) return NO_OWNER;
+  e0 = recs[r].e0;
+  const uint32_t info = recs[r].info;
+  L = info & 0x7fffffffu;
+  if (!(info >> 31) || L <= 32u) return NO_OWNER;
+  if (w < ((e0 + 31u) >> 5) || w > ((e0 + L - 1u) >> 5)) return NO_OWNER;
+  return r;
+}
+
+// level 0: one piece per aligned word of a long run (the run's last word
+// masked to its end), every row with its own W_i
+template <int D>
+__global__ void __launch_bounds__(256) word_maps_k(const RunRec<D>* __restrict__ recs, const Ctl* __restrict__ ctl,
+                                                   const uint32_t* __restrict__ wowner,
+                                                   const uint32_t* __restrict__ delbits, uint32_t nwords,
+                                                   WalkPiece* __restrict__ piece, RowMap* __restrict__ rmap) {
+  const uint32_t R = ctl->n_runs;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
+    uint32_t e0, L;
+    const uint32_t r = word_owner<D>(wowner, recs, R, w, e0, L);
+    if (r == NO_OWNER) continue;
+    const uint32_t cnt = min(e0 + L - w * 32u, 32u);
+    const uint32_t bits = delbits[w] & (cnt == 32u ? 0xFFFFFFFFu : ((1u << cnt) - 1u));
+    uint32_t A0 = recs[r].A[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) A0 = min(A0, recs[r].A[i]);
+    int32_t S = 0, mx = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      S += ((bits >> j) & 1u) ? 1 : -1;
+      mx = max(mx, S);
+    }
+    piece[w] = WalkPiece{S, mx};
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int32_t W = (int32_t)min(recs[r].A[i] - A0, (uint32_t)MAP_INF);
+      int32_t l = -MAP_INF, u = MAP_INF, s = 0, v0 = 0, vW = W, p0 = 0, pW = 0;
+      for (uint32_t j = 0; j < cnt; ++j) {
+        if ((bits >> j) & 1u) {  // delete: (a = +1, l = -inf, u = W)
+          l = l + 1;
+          u = min(u + 1, W);
+          if (l > u) l = u;
+          ++s;
+          v0 = min(v0 + 1, W);
+          vW = min(vW + 1, W);
+        } else {  // insert: (a = -1, l = 0, u = inf)
+          l = max(l - 1, 0);
+          u = max(u - 1, 0);
+          --s;
+          p0 += v0 == 0;
+          pW += vW == 0;
+          v0 = max(v0 - 1, 0);
+          vW = max(vW - 1, 0);
+        }
+      }
+      rmap[(size_t)w * D + i] = RowMap{max(l, -MAP_INF), min(u, MAP_INF), p0, pW};
+    }
+  }
+}
+
+// level k > 0: piece b composes 32 consecutive level-(k-1) pieces when its
+// 32^k words all belong to one long run
+template <int D>
+__global__ void __launch_bounds__(256) block_maps_k(const RunRec<D>* __restrict__ recs, const Ctl* __restrict__ ctl,
+                                                    const uint32_t* __restrict__ wowner, uint32_t nwords,
+                                                    uint32_t span, const WalkPiece* __restrict__ pin,
+                                                    const RowMap* __restrict__ rin, WalkPiece* __restrict__ pout,
+                                                    RowMap* __restrict__ rout, uint32_t nblocks) {
+  const uint32_t R = ctl->n_runs;
+  for (uint32_t bk = blockIdx.x * blockDim.x + threadIdx.x; bk < nblocks; bk += gridDim.x * blockDim.x) {
+    const uint32_t w0 = bk * span, w1 = w0 + span - 1u;
+    if (w1 >= nwords) continue;
+    uint32_t e0, L, e0b, Lb;
+    const uint32_t r = word_owner<D>(wowner, recs, R, w0, e0, L);
+    if (r == NO_OWNER || word_owner<D>(wowner, recs, R, w1, e0b, Lb) != r) continue;
+    uint32_t A0 = recs[r].A[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) A0 = min(A0, recs[r].A[i]);
+    int32_t W[D];
+    RowMap acc[D];
+    WalkPiece pc = pin[bk * 32u];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      W[i] = (int32_t)min(recs[r].A[i] - A0, (uint32_t)MAP_INF);
+      acc[i] = rin[(size_t)(bk * 32u) * D + i];
+    }
+    for (uint32_t q = 1; q < 32u; ++q) {
+      const WalkPiece nx = pin[bk * 32u + q];
+#pragma unroll
+      for (int i = 0; i < D; ++i) acc[i] = rowmap_cat(acc[i], pc.S, rin[(size_t)(bk * 32u + q) * D + i], nx.S, W[i]);
+      pc.mx = max(pc.mx, pc.S + nx.mx);
+      pc.S += nx.S;
+    }
+    pout[bk] = pc;
+#pragma unroll
+    for (int i = 0; i < D; ++i) rout[(size_t)bk * D + i] = acc[i];
+  }
+}
+
 // SFF: replay `avail` ops of a run whose delete flags are the low bits of
 // `bits`. Within a run no other op touches the key's d buckets, so in row i
 // the key's own slot count is A_i + x (x = the run's net inserts so far) and
@@ -626,7 +803,7 @@ __global__ void __launch_bounds__(256) word_sums_k(const uint32_t* __restrict__ 
 template <int D>
 __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const uint32_t (&A)[D],
                                             const uint32_t (&O)[D], uint32_t A0, uint32_t& m, uint32_t& x,
-                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3],
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[5],
                                             const uint32_t* lut, const uint8_t* rlut) {
   const uint32_t nd = __popc(bits), ni = avail - nd;
   // Gap word: the min lags the key's own count by at least the word's
@@ -768,7 +945,7 @@ __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const
 template <int D, int MODE>
 __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, uint32_t e0, uint32_t info,
                                             uint32_t bits0, const uint32_t (&A)[D], const uint32_t (&O)[D],
-                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[3],
+                                            uint32_t (&c)[D], uint32_t (&raised)[D], uint32_t (&ws)[5],
                                             const uint32_t* lut, const uint8_t* rlut) {
   const uint32_t L = info & 0x7fffffffu;
   if (MODE == 1) {
@@ -776,8 +953,13 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     return true;
   }
   if (MODE == 0) {
-    uint32_t j = 0;
-    while (j < L && a.opdata[e0 + j] <= k.m) ++j;
+    // b_min strictly increases along a same-key SF1 run (the key's own fat
+    // cells gain one per op): the first raising op by binary search
+    uint32_t j = 0, hi = L;
+    while (j < hi) {
+      const uint32_t mid = (j + hi) >> 1;
+      if (a.opdata[e0 + mid] <= k.m) j = mid + 1; else hi = mid;
+    }
     if (L - j) raise_to<D>(k.m + (L - j), c, raised);
     return true;
   }
@@ -797,6 +979,57 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     omax = max(omax, (int64_t)O[i] - (int64_t)A[i]);
   }
   while (k.rem && budget) {
+    // Long-run path: at an aligned word in the steady regime with every row
+    // inside [0, W_i], apply precomputed reflected-walk pieces (1, 32 or
+    // 1024 words) while the key's own slot keeps dominating its buckets.
+    if (a.rmap[0] && L > 32u && (k.e & 31u) == 0 && k.m == k.A0 + k.x) {
+      int32_t v[D];
+      bool ok = true;
+      int64_t omax = INT64_MIN;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const uint32_t vi = c[i] - k.m, Wi = A[i] - k.A0;
+        ok = ok && vi <= Wi && Wi < (uint32_t)MAP_INF;
+        v[i] = (int32_t)vi;
+        omax = max(omax, (int64_t)O[i] - (int64_t)A[i]);
+      }
+      if (ok) {
+        const uint32_t end = e0 + L, wl = (end - 1u) >> 5;
+        uint32_t w = k.e >> 5;
+        int64_t x = (int64_t)(int32_t)k.x;
+        while (w <= wl) {
+          int lvl = 0;
+          if ((w & 1023u) == 0 && w + 1023u <= wl) lvl = 2;
+          else if ((w & 31u) == 0 && w + 31u <= wl) lvl = 1;
+          const uint32_t idx = w >> (5 * lvl);
+          // (selects, not a dynamic index into the kernel parameters)
+          const WalkPiece* pp = lvl == 2 ? a.piece[2] : lvl == 1 ? a.piece[1] : a.piece[0];
+          const RowMap* rp = lvl == 2 ? a.rmap[2] : lvl == 1 ? a.rmap[1] : a.rmap[0];
+          const WalkPiece pc = pp[idx];
+          if (omax > x - pc.mx) break;  // the own slot may stop dominating inside this piece
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const RowMap f = rp[(size_t)idx * D + i];
+            raised[i] += (uint32_t)rowmap_push(f, v[i]);
+            v[i] = rowmap_apply(f, pc.S, v[i]);
+          }
+          x -= pc.S;
+          w += 1u << (5 * lvl);
+          ++ws[3];
+        }
+        const uint32_t ne = min(w * 32u, end);
+        ws[4] += ne - k.e;
+        if (ne != k.e) {
+          k.x = (uint32_t)(int32_t)x;
+          k.m = k.A0 + k.x;
+#pragma unroll
+          for (int i = 0; i < D; ++i) c[i] = k.m + (uint32_t)v[i];
+          k.rem -= ne - k.e;
+          k.e = ne;
+          if (!k.rem) break;
+        }
+      }
+    }
     // Fast loop over whole aligned words in the steady regime (see
     // replay_word) from the precomputed walk summaries: per word only the
     // regime test and d Lindley updates remain on the sequential path.
@@ -950,18 +1183,37 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
   for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0, A[i] = 0, O[i] = 0, c[i] = 0;
   Cursor k{};
   uint32_t idle = 0;
-  uint32_t ws[3] = {0, 0, 0};
+  uint32_t ws[5] = {0, 0, 0, 0, 0};
   unsigned long long st_cyc = 0, st_runs = 0, st_iters = 0;
+  uint32_t pool_base = 0, pool_cnt = 0;  // warp-uniform
   while (true) {
     ++st_iters;
     const unsigned need = __ballot_sync(0xffffffffu, !has && !exhausted);
     if (need) {
+      // Claim from the warp's pool of consecutive run ids (one atomic per
+      // CLAIM_POOL runs); ids are handed out in increasing order, so the
+      // earliest unfinished run is always held by a lane or next in a pool.
       const int leader = __ffs(need) - 1;
-      uint32_t base = 0;
-      if ((int)lane == leader) base = atomicAdd(&a.ctl->qhead, (uint32_t)__popc(need));
-      base = __shfl_sync(0xffffffffu, base, leader);
+      const uint32_t kneed = (uint32_t)__popc(need), pos = (uint32_t)__popc(need & lanemask_lt());
+      uint32_t r;
+      if (pool_cnt >= kneed) {
+        r = pool_base + pos;
+        pool_base += kneed;
+        pool_cnt -= kneed;
+      } else {
+        uint32_t nb = 0;
+        if ((int)lane == leader) nb = atomicAdd(&a.ctl->qhead, CLAIM_POOL);
+        nb = __shfl_sync(0xffffffffu, nb, leader);
+        r = pos < pool_cnt ? pool_base + pos : nb + (pos - pool_cnt);
+        pool_base = nb + (kneed - pool_cnt);
+        pool_cnt = CLAIM_POOL - (kneed - pool_cnt);
+      }
       if (!has && !exhausted) {
-        const uint32_t r = base + __popc(need & lanemask_lt());
+        if (r + CLAIM_PREFETCH < R) {  // pull a record far ahead into L2 (records exceed L2)
+          const char* pf = reinterpret_cast<const char*>(a.recs + r + CLAIM_PREFETCH);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + sizeof(RunRec<D>) - 1));
+        }
         if (r < R) {
           rid = r;
           if (a.trace) a.trace[3ull * r] = gtimer();
@@ -1027,7 +1279,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
     if (__any_sync(0xffffffffu, progressed)) {
       idle = 0;
     } else if (++idle > 4) {
-      __nanosleep(min(idle * 8u, 128u));
+      __nanosleep(min(idle * 4u, 32u));
     }
   }
 #pragma unroll
@@ -1037,9 +1289,10 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
     if (lane == 0 && r) atomicAdd(a.inc + i, r);
   }
   // diagnostics (sfk_engine_stats): words by replay path, replay cycles, runs, warp iterations
-  unsigned long long sv[6] = {ws[0], ws[1], ws[2], (unsigned long long)st_cyc, st_runs, lane == 0 ? st_iters : 0ull};
+  unsigned long long sv[8] = {ws[0], ws[1], ws[2], (unsigned long long)st_cyc, st_runs, lane == 0 ? st_iters : 0ull,
+                              ws[3], ws[4]};
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < 8; ++q) {
     unsigned long long v = sv[q];
     for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
     if (lane == 0 && v) atomicAdd(&g_engine_stats[q], v);
@@ -1223,6 +1476,9 @@ struct Layout {
   uint2* obs2;
   uint32_t* delbits;
   uint32_t* wsum;
+  uint32_t* wowner;
+  WalkPiece* piece[3];
+  RowMap* rmap[3];
   uint2* links;
   uint8_t* opflags;
   uint32_t* opdata;
@@ -1264,6 +1520,15 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
   L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 16 : 1);
   L.wsum = cv.take<uint32_t>(kind == 0 ? n / 32 + 32 : 1);
+  {
+    const uint64_t nw = kind == 0 ? n / 32 + 32 : 1;
+    L.wowner = cv.take<uint32_t>(nw);
+    for (int lv = 0; lv < MAP_LEVELS; ++lv) {
+      const uint64_t cnt = kind == 0 ? (nw >> (5 * lv)) + 1 : 1;
+      L.piece[lv] = cv.take<WalkPiece>(cnt);
+      L.rmap[lv] = cv.take<RowMap>(cnt * (uint64_t)d);
+    }
+  }
   const bool engine = kind != 3;
   L.links = cv.take<uint2>(engine ? (kind == 0 ? 2 * N : N) : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
@@ -1459,9 +1724,20 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.opdata = L.opdata;
   ea.delbits = L.delbits;
   ea.wsum = L.wsum;
+  for (int lv = 0; lv < MAP_LEVELS; ++lv) ea.piece[lv] = nullptr, ea.rmap[lv] = nullptr;
   if (MODE == 2) {
     const uint32_t nwords = (n + 31) / 32;
     { note_launch(); word_sums_k<<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(L.delbits, nwords, L.wsum); }
+    if (!getenv("SFK_NO_LONGRUN")) {  // diagnostics knob: the word-by-word replay only
+      const RunRec<D>* rp = static_cast<const RunRec<D>*>(L.recs);
+      { note_launch(); long_owner_k<D><<<sms * 8, 256, 0, st>>>(rp, L.ctl, L.wowner); }
+      { note_launch(); word_maps_k<D><<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, L.delbits, nwords, L.piece[0], L.rmap[0]); }
+      for (int lv = 1; lv < MAP_LEVELS; ++lv) {
+        const uint32_t nb = nwords >> (5 * lv);
+        if (nb) { note_launch(); block_maps_k<D><<<grid_for(nb, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, nwords, 1u << (5 * lv), L.piece[lv - 1], L.rmap[lv - 1], L.piece[lv], L.rmap[lv], nb); }
+      }
+      for (int lv = 0; lv < MAP_LEVELS; ++lv) ea.piece[lv] = L.piece[lv], ea.rmap[lv] = L.rmap[lv];
+    }
   }
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);

@@ -129,3 +129,41 @@ def test_saturation_prefix_at_scale(oracle):
         status, idx = apply_batches(sk, c["ops"], c["keys"])
         assert (status, idx) == st[:2]
         assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+
+
+def long_run_stream(seed, w, n_bg, blocks, block_len, del_p):
+    """Background traffic over many keys, interleaved with long blocks of one
+    hot key's own inserts and deletes (every delete valid): the engine's
+    multi-word runs, in and out of the steady regime."""
+    rng = np.random.default_rng(seed)
+    bg = rng.integers(1, 1 << 31, size=300, dtype=np.uint64).astype(np.uint32)
+    ops, keys = [], []
+    counts = {}
+    for b in range(blocks):
+        for _ in range(n_bg):  # background inserts (and deletes of inserted keys)
+            k = int(bg[rng.integers(0, bg.size)])
+            if counts.get(k, 0) and rng.random() < 0.3:
+                ops.append(1); counts[k] -= 1
+            else:
+                ops.append(0); counts[k] = counts.get(k, 0) + 1
+            keys.append(k)
+        hot = int(bg[b % 7])
+        for _ in range(block_len):
+            if counts.get(hot, 0) and rng.random() < del_p:
+                ops.append(1); counts[hot] -= 1
+            else:
+                ops.append(0); counts[hot] = counts.get(hot, 0) + 1
+            keys.append(hot)
+    return np.array(ops, np.uint8), np.array(keys, np.uint32)
+
+
+@pytest.mark.parametrize("seed,w,del_p", [(1, 64, 0.3), (2, 256, 0.45), (3, 32, 0.49), (4, 1024, 0.2),
+                                          (5, 16, 0.4)])
+def test_sff_long_runs(oracle, seed, w, del_p):
+    ops, keys = long_run_stream(seed, w, n_bg=400, blocks=12, block_len=3000, del_p=del_p)
+    for sequential in (False, True):
+        o, st = oracle_run(oracle, "sff", 4, w, 4, None, seed, ops, keys.astype(np.uint64))
+        sk = make_sketch("sff", 4, w, 4, None, seed)
+        status, idx = apply_batches(sk, ops, keys, sequential=sequential)
+        assert (status, idx) == st[:2]
+        assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)

@@ -43,4 +43,4 @@ import ctypes  # noqa: E402
 from paper_1701_04148_b200 import _lib  # noqa: E402
 st = (ctypes.c_ulonglong * 8)()
 _lib.load_library().sfk_engine_stats(st, 1)
-print("engine stats (all reps): gap_words=%d steady_words=%d slow_words=%d replay_cycles=%d runs=%d warp_iters=%d" % tuple(st[:6]))
+print("engine stats (all reps): gap_words=%d steady_words=%d slow_words=%d replay_cycles=%d runs=%d warp_iters=%d longrun_pieces=%d longrun_ops=%d" % tuple(st[:8]))
