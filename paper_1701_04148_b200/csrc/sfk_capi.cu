@@ -60,9 +60,9 @@ int engine_stats(unsigned long long* out, int reset);
 int engine_timing(int on);
 int engine_trace(unsigned long long* host_out, size_t runs);
 float engine_last_ms();
-int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
-                   int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
-                   int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st);
+int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
+                   const uint64_t* fat_seeds, int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
+                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st);
 int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64_t cells, void* ws, size_t ws_bytes,
                   Stats* host, cudaStream_t st);
 int cm_fast(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
@@ -198,8 +198,8 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
       { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, (int64_t)s.n_ins, inc_counts, d, (int64_t)s.n_ins); }
       return check_launch("set_result");
     }
-    return parallel_apply(3, counters, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,
-                          workspace, workspace_bytes, st);
+    return parallel_apply(3, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts,
+                          result, workspace, workspace_bytes, st);
   });
 }
 
@@ -224,24 +224,31 @@ int sfk_cu_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
     // the CU min can reach 0xFFFFFFFF only if some counter climbs that far:
     // counters grow by at most one per insert
     if ((uint64_t)s.cmax + s.ins_before_first_del < 0xFFFFFFFFull)
-      return parallel_apply(2, counters, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,
+      return parallel_apply(2, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, inc_counts, result,
                             workspace, workspace_bytes, st);
     return launch_seq_apply(1, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, nullptr, cnt,
                             inc_counts, result, st);
   });
 }
 
-static int sf_parallel_kind(int variant, int d, int z) {
+// parallel engine kind per variant (see carve() in sfk_sf.cu); -1: the exact
+// one-thread device engine
+static int sf_parallel_kind(int variant, int d, int z, int64_t w = 0, int64_t w_prime = 0) {
   if (d > MAXD) return -1;
   if (variant == SFK_VARIANT_SF1) return 1;
   if (variant == SFK_VARIANT_SFF && z >= 1 && z <= 8) return 0;
+  if (variant == SFK_VARIANT_SF4 && z >= 1 && z <= 8) return 4;
+  if (variant == SFK_VARIANT_SF3 && z >= 1 && z <= 8 && w_prime == (int64_t)z * w) return 5;
+  if (variant == SFK_VARIANT_SF2) return 6;
   return -1;
 }
 
+static int kind_z(int kind, int z) { return (kind == 0 || kind == 4 || kind == 5) ? z : 1; }
+
 size_t sfk_sf_workspace_size(int variant, int d, int64_t w, int64_t w_prime, int z, int64_t n) {
-  const int kind = sf_parallel_kind(variant, d, z);
+  const int kind = sf_parallel_kind(variant, d, z, w, w_prime);
   if (kind < 0) return 256;
-  return parallel_workspace_size(kind, d, w, w_prime, z, std::min<int64_t>(n, chunk_ops(d, kind == 0 ? z : 1)));
+  return parallel_workspace_size(kind, d, w, w_prime, z, std::min<int64_t>(n, chunk_ops(d, kind_z(kind, z))));
 }
 
 int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
@@ -260,7 +267,7 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
   }
   if (bucketed && (uint64_t)d * (uint64_t)w * (uint64_t)z >= (1ull << 32)) { set_error("fat too large"); return 1; }
   if (variant == SFK_VARIANT_SF2 && dsub == nullptr) { set_error("SF2 needs the deletion sub-sketch"); return 1; }
-  const int kind = sf_parallel_kind(variant, d, z);
+  const int kind = sf_parallel_kind(variant, d, z, w, w_prime);
   KeySrc all{keys, key_kind, rec_len};
   if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0) {
     if (flat)
@@ -269,10 +276,10 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
     return launch_seq_apply(3, variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, nullptr, slim_seeds, fat_seeds, d, w, 0,
                             z, ops, all, nullptr, n, inc_counts, result, st);
   }
-  return chunked(n, chunk_ops(d, kind == 0 ? z : 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+  return chunked(n, chunk_ops(d, kind_z(kind, z)), result, st, [&](int64_t t0, int64_t cnt) -> int {
     KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
-    return parallel_apply(kind, slim, fat, slim_seeds, fat_seeds, d, w, w_prime, z, ops + t0, ks, cnt, inc_counts,
-                          result, workspace, workspace_bytes, st);
+    return parallel_apply(kind, slim, fat, dsub, slim_seeds, fat_seeds, d, w, w_prime, z, ops + t0, ks, cnt,
+                          inc_counts, result, workspace, workspace_bytes, st);
   });
 }
 

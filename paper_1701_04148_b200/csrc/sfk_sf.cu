@@ -87,8 +87,9 @@ struct Ctl {
 };
 
 // ---------------------------------------------------------------- 1. hash_emit
-// kind: 0 bucketed (SFF: cell = bucket, slot in the low bits of val)
+// kind: 0 bucketed (SFF/SF4: cell = bucket, slot in the low bits of val)
 //       1 flat fat (cell = fat index), 2 slim-only (cell = slim index)
+//       3 fold (SF3: g = fat index; cell = g mod w, slot = g / w)
 template <int D>
 struct HashArgs {
   KeySrc keys;
@@ -100,6 +101,7 @@ struct HashArgs {
   Mod zm;  // slot range
   uint32_t row_cells;  // cells per row
   int kb;              // slot bits
+  uint32_t fold_w;     // KIND 3: the slim width w
   uint32_t* key_out;
   uint32_t* val_out;
   int unsupported_deletes;  // SF1 / CU: a delete is the failing op
@@ -115,8 +117,14 @@ __global__ void __launch_bounds__(256) hash_emit_k(HashArgs<D> a) {
     if (a.unsupported_deletes && op != 0 && local_fail == NONE32) local_fail = (uint32_t)t;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      uint32_t cell = (uint32_t)i * a.row_cells + (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
-      uint32_t v = ((uint32_t)t << (a.kb + 1)) | (op << a.kb);
+      uint32_t cell, v = ((uint32_t)t << (a.kb + 1)) | (op << a.kb);
+      if (KIND == 3) {
+        const uint32_t g = (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
+        cell = (uint32_t)i * a.fold_w + g % a.fold_w;
+        v |= g / a.fold_w;
+      } else {
+        cell = (uint32_t)i * a.row_cells + (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
+      }
       if (KIND == 0) v |= (uint32_t)bucket(key, a.slot_seeds.s[i], a.zm);
       a.key_out[(int64_t)i * a.n + t] = cell;
       a.val_out[(int64_t)i * a.n + t] = v;
@@ -282,7 +290,8 @@ struct ScanOut {
   Ctl* ctl;
 };
 
-// WRITE_OBS: 0 none, 1 obs (b_min / bucket max), 2 obs2 (own count, max of the others)
+// WRITE_OBS: 0 none, 1 obs (b_min / bucket max), 2 obs2 (own count, max of the others),
+//            3 obs2 (own count, sum of the others clamped to 2^32 - 1: the SF2/SF3/SF4 trigger)
 template <int Z, bool HAS_FAT, int WRITE_OBS, bool WRITE_LINKS>
 __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ vals, uint32_t N, int kb,
@@ -319,11 +328,19 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
       const int64_t post_own = (int64_t)init[k] + (int64_t)run.v[k];
       const int64_t pre_own = post_own + (op ? 1 : -1);
       if (op == 0 ? (pre_own == (int64_t)U32MAX) : (pre_own == 0)) local_fail = min(local_fail, t);
-      if (WRITE_OBS == 2) {
+      if (WRITE_OBS == 2 || WRITE_OBS == 3) {
         uint32_t others = 0;
+        if (WRITE_OBS == 2) {
 #pragma unroll
-        for (int q2 = 0; q2 < Z; ++q2)
-          if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+          for (int q2 = 0; q2 < Z; ++q2)
+            if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+        } else {
+          uint64_t sum = 0;
+#pragma unroll
+          for (int q2 = 0; q2 < Z; ++q2)
+            if (q2 != (int)k) sum += (uint64_t)((int64_t)init[q2] + run.v[q2]);
+          others = (uint32_t)min(sum, (uint64_t)U32MAX);
+        }
         if (WRITE_LINKS) {  // links and observations interleaved: one 16-B store
           const uint32_t prev = (e > run.head) ? prev_t : NONE32;
           reinterpret_cast<uint4*>(o.links)[(size_t)t * o.D + row] =
@@ -349,7 +366,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
         for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
       }
     }
-    if (WRITE_LINKS && !(HAS_FAT && WRITE_OBS == 2)) {
+    if (WRITE_LINKS && !(HAS_FAT && (WRITE_OBS == 2 || WRITE_OBS == 3))) {
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
       o.links[(size_t)t * o.D + row] = make_uint2(e - run.head, prev);
     }
@@ -530,6 +547,7 @@ struct EngineArgs {
   Ctl* ctl;
   unsigned long long* inc;     // int64[d] tallies (two's complement add)
   uint32_t budget;             // ops a lane replays per engine iteration before it yields
+  int b_opdata;                // MODE 3: an insert's b_min comes from opdata (SF2) instead of A0 + x
   unsigned long long* trace;   // diagnostics: per run {claim, ready, done} globaltimer ns (or null)
 };
 
@@ -666,6 +684,15 @@ __device__ __forceinline__ RowMap rowmap_cat(const RowMap& f, int32_t S1, const 
   return h;
 }
 
+// the upper bound of row i's reflected walk: W_i = A_i - A0 for the SFF max
+// clamp; K_i = A_i - A0 + O_i for the SF3/SF4 sum trigger (O_i = the other
+// slots' sum), whose rows step v -> v + [v < K_i] on a delete
+template <int D>
+__device__ __forceinline__ int32_t walk_width(const RunRec<D>& rec, int i, uint32_t A0, int sum_mode) {
+  const uint64_t wd = (uint64_t)(rec.A[i] - A0) + (sum_mode ? (uint64_t)rec.O[i] : 0ull);
+  return (int32_t)min(wd, (uint64_t)MAP_INF);
+}
+
 // owner of every aligned word of a long SFF run (hasdel, L > 32): the run id
 template <int D>
 __global__ void __launch_bounds__(256) long_owner_k(const RunRec<D>* __restrict__ recs, const Ctl* __restrict__ ctl,
@@ -712,7 +739,8 @@ template <int D>
 __global__ void __launch_bounds__(256) word_maps_k(const RunRec<D>* __restrict__ recs, const Ctl* __restrict__ ctl,
                                                    const uint32_t* __restrict__ wowner,
                                                    const uint32_t* __restrict__ delbits, uint32_t nwords,
-                                                   WalkPiece* __restrict__ piece, RowMap* __restrict__ rmap) {
+                                                   WalkPiece* __restrict__ piece, RowMap* __restrict__ rmap,
+                                                   int sum_mode) {
   const uint32_t R = ctl->n_runs;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
     uint32_t e0, L;
@@ -731,7 +759,7 @@ __global__ void __launch_bounds__(256) word_maps_k(const RunRec<D>* __restrict__
     piece[w] = WalkPiece{S, mx};
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      const int32_t W = (int32_t)min(recs[r].A[i] - A0, (uint32_t)MAP_INF);
+      const int32_t W = walk_width<D>(recs[r], i, A0, sum_mode);
       int32_t l = -MAP_INF, u = MAP_INF, s = 0, v0 = 0, vW = W, p0 = 0, pW = 0;
       for (uint32_t j = 0; j < cnt; ++j) {
         if ((bits >> j) & 1u) {  // delete: (a = +1, l = -inf, u = W)
@@ -763,7 +791,7 @@ __global__ void __launch_bounds__(256) block_maps_k(const RunRec<D>* __restrict_
                                                     const uint32_t* __restrict__ wowner, uint32_t nwords,
                                                     uint32_t span, const WalkPiece* __restrict__ pin,
                                                     const RowMap* __restrict__ rin, WalkPiece* __restrict__ pout,
-                                                    RowMap* __restrict__ rout, uint32_t nblocks) {
+                                                    RowMap* __restrict__ rout, uint32_t nblocks, int sum_mode) {
   const uint32_t R = ctl->n_runs;
   for (uint32_t bk = blockIdx.x * blockDim.x + threadIdx.x; bk < nblocks; bk += gridDim.x * blockDim.x) {
     const uint32_t w0 = bk * span, w1 = w0 + span - 1u;
@@ -779,7 +807,7 @@ __global__ void __launch_bounds__(256) block_maps_k(const RunRec<D>* __restrict_
     WalkPiece pc = pin[bk * 32u];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      W[i] = (int32_t)min(recs[r].A[i] - A0, (uint32_t)MAP_INF);
+      W[i] = walk_width<D>(recs[r], i, A0, sum_mode);
       acc[i] = rin[(size_t)(bk * 32u) * D + i];
     }
     for (uint32_t q = 1; q < 32u; ++q) {
@@ -942,6 +970,9 @@ __device__ __forceinline__ void replay_word(uint32_t bits, uint32_t avail, const
 //         run, so the first op with b_k > m0 raises and so does every later)
 // MODE 1: CU (every insert raises; saturation ruled out by the host precheck)
 // MODE 2: SFF (see replay_word)
+// MODE 3: SF2 / SF3 / SF4 (a delete decrements each row whose slim counter
+//         exceeds that row's observation: the bucket / fold-group sum, or the
+//         deletion sub-sketch counter; A_i + x + O_i within the run)
 template <int D, int MODE>
 __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, uint32_t e0, uint32_t info,
                                             uint32_t bits0, const uint32_t (&A)[D], const uint32_t (&O)[D],
@@ -962,6 +993,99 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     }
     if (L - j) raise_to<D>(k.m + (L - j), c, raised);
     return true;
+  }
+  if (MODE == 3) {
+    // insert-only SF3/SF4 run: b_min = A0 + j, closed form as SFF. (SF2's
+    // b_min comes from the flat fat, where other keys' deletes may lower it
+    // mid-run, so SF2 runs always replay op by op.)
+    if (!(info >> 31) && !a.b_opdata) {
+      const int64_t jstar = max((int64_t)k.m - (int64_t)k.A0 + 1, (int64_t)1);
+      if (jstar <= (int64_t)L) raise_to<D>(k.m + (uint32_t)((int64_t)L - jstar + 1), c, raised);
+      return true;
+    }
+    // op by op, one delete-bit word at a time; at aligned words of a long
+    // run with every row in [0, K_i] (c_i >= A0 + x: not lagging), rows are
+    // independent two-sided reflected walks and precomputed pieces apply
+    uint32_t budget = a.budget;
+    while (k.rem && budget) {
+      if (!a.b_opdata && a.rmap[0] && L > 32u && (k.e & 31u) == 0) {
+        const int64_t floor0 = (int64_t)(uint32_t)(k.A0 + k.x);
+        int32_t v[D];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const int64_t vi = (int64_t)c[i] - floor0;
+          const int64_t Ki = (int64_t)(A[i] - k.A0) + (int64_t)O[i];
+          ok = ok && vi >= 0 && vi <= Ki && Ki < (int64_t)MAP_INF;
+          v[i] = (int32_t)vi;
+        }
+        if (ok) {
+          const uint32_t end = e0 + L, wl = (end - 1u) >> 5;
+          uint32_t w = k.e >> 5;
+          int64_t x = (int64_t)(int32_t)k.x;
+          while (w <= wl) {
+            int lvl = 0;
+            if ((w & 1023u) == 0 && w + 1023u <= wl) lvl = 2;
+            else if ((w & 31u) == 0 && w + 31u <= wl) lvl = 1;
+            const uint32_t idx = w >> (5 * lvl);
+            const WalkPiece* pp = lvl == 2 ? a.piece[2] : lvl == 1 ? a.piece[1] : a.piece[0];
+            const RowMap* rp = lvl == 2 ? a.rmap[2] : lvl == 1 ? a.rmap[1] : a.rmap[0];
+            const WalkPiece pc = pp[idx];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const RowMap f = rp[(size_t)idx * D + i];
+              raised[i] += (uint32_t)rowmap_push(f, v[i]);
+              v[i] = rowmap_apply(f, pc.S, v[i]);
+            }
+            x -= pc.S;
+            w += 1u << (5 * lvl);
+            ++ws[3];
+          }
+          const uint32_t ne = end;
+          ws[4] += ne - k.e;
+          k.x = (uint32_t)(int32_t)x;
+          uint32_t m = U32MAX;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            c[i] = k.A0 + k.x + (uint32_t)v[i];
+            m = min(m, c[i]);
+          }
+          k.m = m;
+          k.rem = 0;
+          k.e = ne;
+          break;
+        }
+      }
+      const uint32_t off = k.e & 31u, avail = min(min(32u - off, k.rem), budget);
+      const uint32_t bits = a.delbits[k.e >> 5] >> off;
+      for (uint32_t j = 0; j < avail; ++j) {
+        if (!((bits >> j) & 1u)) {  // insert
+          k.x += 1u;
+          const uint32_t b = a.b_opdata ? a.opdata[k.e + j] : k.A0 + k.x;
+          if (k.m < b) {
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+              if (c[i] == k.m) c[i] += 1u, raised[i] += 1u;
+            k.m += 1u;
+          }
+        } else {  // delete
+          k.x -= 1u;
+          uint32_t m = U32MAX;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const int64_t T = (int64_t)A[i] + (int64_t)(int32_t)k.x + (int64_t)O[i];
+            if ((int64_t)c[i] > T) c[i] -= 1u;
+            m = min(m, c[i]);
+          }
+          k.m = m;
+        }
+      }
+      k.e += avail;
+      k.rem -= avail;
+      budget -= avail;
+      ws[2] += 1;
+    }
+    return k.rem == 0;
   }
   if (!(info >> 31)) {  // insert-only SFF run: the j-th insert raises iff m0 < A0 + j
     const int64_t jstar = max((int64_t)k.m - (int64_t)k.A0 + 1, (int64_t)1);
@@ -1225,7 +1349,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
           for (int i = 0; i < D; ++i) {
             cells[i] = rec.cells[i];
             rank[i] = rec.rank[i];
-            if (MODE == 2) A[i] = rec.A[i], O[i] = rec.O[i];
+            if (MODE >= 2) A[i] = rec.A[i], O[i] = rec.O[i];
           }
           pend = (1u << D) - 1u;
           has = true;
@@ -1472,6 +1596,7 @@ struct Layout {
   size_t cub_tmp_bytes;
   void* tiles;        // SegState<Z> per tile
   uint32_t* fat_snap;
+  uint32_t* fat_perm;  // SF3: the fat regrouped into fold-group order
   uint32_t* obs;
   uint2* obs2;
   uint32_t* delbits;
@@ -1495,7 +1620,8 @@ struct Layout {
   bool ok;
 };
 
-// kind: 0 SFF (bucketed), 1 SF1 (flat), 2 CU, 3 CM exact
+// kind: 0 SFF (bucketed), 1 SF1 (flat), 2 CU, 3 CM exact, 4 SF4 (bucketed, sum
+// trigger), 5 SF3 (fold groups as buckets), 6 SF2 (flat fat + deletion sub-sketch)
 static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
   Carver cv(base, cap);
   Layout L{};
@@ -1510,27 +1636,30 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
+  const bool bucketed = kind == 0 || kind == 4 || kind == 5;
+  const bool deletes = bucketed || kind == 6;  // runs carry delete bits and (own, other) observations
   uint64_t fat_cells = 0;
-  if (kind == 0) fat_cells = (uint64_t)d * w * z;
-  if (kind == 1) fat_cells = (uint64_t)d * wp;
+  if (bucketed) fat_cells = (uint64_t)d * w * z;
+  if (kind == 1 || kind == 6) fat_cells = std::max((uint64_t)d * wp, (uint64_t)d * w);
   if (kind == 3) fat_cells = (uint64_t)d * w;
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
-  const bool need_obs = kind == 1;
+  L.fat_perm = cv.take<uint32_t>(kind == 5 ? fat_cells : 1);
+  const bool need_obs = kind == 1 || kind == 6;
   L.obs = cv.take<uint32_t>(need_obs ? N : 1);
   L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
-  L.delbits = cv.take<uint32_t>(kind == 0 ? n / 32 + 16 : 1);
+  L.delbits = cv.take<uint32_t>(deletes ? n / 32 + 16 : 1);
   L.wsum = cv.take<uint32_t>(kind == 0 ? n / 32 + 32 : 1);
   {
-    const uint64_t nw = kind == 0 ? n / 32 + 32 : 1;
+    const uint64_t nw = (kind == 0 || kind == 4 || kind == 5) ? n / 32 + 32 : 1;  // long-run maps
     L.wowner = cv.take<uint32_t>(nw);
     for (int lv = 0; lv < MAP_LEVELS; ++lv) {
-      const uint64_t cnt = kind == 0 ? (nw >> (5 * lv)) + 1 : 1;
+      const uint64_t cnt = nw > 1 ? (nw >> (5 * lv)) + 1 : 1;
       L.piece[lv] = cv.take<WalkPiece>(cnt);
       L.rmap[lv] = cv.take<RowMap>(cnt * (uint64_t)d);
     }
   }
   const bool engine = kind != 3;
-  L.links = cv.take<uint2>(engine ? (kind == 0 ? 2 * N : N) : 1);
+  L.links = cv.take<uint2>(engine ? (deletes ? 2 * N : N) : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
   L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);
   L.headflag = cv.take<uint32_t>(engine ? n : 1);
@@ -1666,21 +1795,21 @@ static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uin
 // pairs (k_out/v_out), the links and the observations exist.
 template <int D, int MODE>
 static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int64_t w, KeySrc ks, uint32_t n, int kb,
-                      int64_t* inc, cudaStream_t st) {
+                      int64_t* inc, cudaStream_t st, bool b_opdata = false) {
   const int sms = sm_count();
   RunArgs<D> ra;
   ra.vals0 = L.v_out;
   ra.kb = kb;
   ra.n = n;
   ra.links = L.links;
-  ra.lstride = MODE == 2 ? 2 : 1;
-  ra.obs = MODE == 0 ? L.obs : nullptr;
+  ra.lstride = MODE >= 2 ? 2 : 1;
+  ra.obs = (MODE == 0 || b_opdata) ? L.obs : nullptr;
   ra.keys = ks;
   ra.opflags = L.opflags;
   ra.opdata = L.opdata;
   ra.headflag = L.headflag;
   ra.head_e0 = L.head_e0;
-  ra.delbits = MODE == 2 ? L.delbits : nullptr;
+  ra.delbits = MODE >= 2 ? L.delbits : nullptr;
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
   ra.ctl = L.ctl;
@@ -1704,10 +1833,10 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.bidx = L.bidx;
   ba.bpos = L.bpos;
   ba.delpre = L.delpre;
-  ba.delbits = MODE == 2 ? L.delbits : nullptr;
-  ba.obs2 = MODE == 2 ? L.links + 1 : nullptr;
+  ba.delbits = MODE >= 2 ? L.delbits : nullptr;
+  ba.obs2 = MODE >= 2 ? L.links + 1 : nullptr;
   ba.links = L.links;
-  ba.lstride = MODE == 2 ? 2 : 1;
+  ba.lstride = MODE >= 2 ? 2 : 1;
   ba.n = n;
   ba.keys = ks;
   for (int i = 0; i < D; ++i) ba.seeds.s[i] = slim_seeds[i];
@@ -1725,16 +1854,17 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.delbits = L.delbits;
   ea.wsum = L.wsum;
   for (int lv = 0; lv < MAP_LEVELS; ++lv) ea.piece[lv] = nullptr, ea.rmap[lv] = nullptr;
-  if (MODE == 2) {
+  if (MODE == 2 || (MODE == 3 && !b_opdata)) {
     const uint32_t nwords = (n + 31) / 32;
-    { note_launch(); word_sums_k<<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(L.delbits, nwords, L.wsum); }
+    const int sum_mode = MODE == 3 ? 1 : 0;
+    if (MODE == 2) { note_launch(); word_sums_k<<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(L.delbits, nwords, L.wsum); }
     if (!getenv("SFK_NO_LONGRUN")) {  // diagnostics knob: the word-by-word replay only
       const RunRec<D>* rp = static_cast<const RunRec<D>*>(L.recs);
       { note_launch(); long_owner_k<D><<<sms * 8, 256, 0, st>>>(rp, L.ctl, L.wowner); }
-      { note_launch(); word_maps_k<D><<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, L.delbits, nwords, L.piece[0], L.rmap[0]); }
+      { note_launch(); word_maps_k<D><<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, L.delbits, nwords, L.piece[0], L.rmap[0], sum_mode); }
       for (int lv = 1; lv < MAP_LEVELS; ++lv) {
         const uint32_t nb = nwords >> (5 * lv);
-        if (nb) { note_launch(); block_maps_k<D><<<grid_for(nb, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, nwords, 1u << (5 * lv), L.piece[lv - 1], L.rmap[lv - 1], L.piece[lv], L.rmap[lv], nb); }
+        if (nb) { note_launch(); block_maps_k<D><<<grid_for(nb, 256, sms * 8), 256, 0, st>>>(rp, L.ctl, L.wowner, nwords, 1u << (5 * lv), L.piece[lv - 1], L.rmap[lv - 1], L.piece[lv], L.rmap[lv], nb, sum_mode); }
       }
       for (int lv = 0; lv < MAP_LEVELS; ++lv) ea.piece[lv] = L.piece[lv], ea.rmap[lv] = L.rmap[lv];
     }
@@ -1742,6 +1872,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.ctl = L.ctl;
   ea.inc = reinterpret_cast<unsigned long long*>(inc);
   ea.budget = engine_budget();
+  ea.b_opdata = b_opdata ? 1 : 0;
   ea.trace = nullptr;
   if (getenv("SFK_ENGINE_TRACE")) {  // diagnostics only: per-run timestamps
     if (g_trace_cap < n) {
@@ -1761,10 +1892,30 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   return check_launch("poll_engine");
 }
 
+
+// SF3 fat (d, w') with w' = z w: fold group of slim cell (i, j) = fat cells
+// j + m w, m < z. Regrouped as (i, j, m) so the bucketed scan applies.
+__global__ void fold_gather_k(const uint32_t* __restrict__ fat, uint32_t* __restrict__ grp, uint32_t d, uint32_t w,
+                              uint32_t z) {
+  const uint64_t total = (uint64_t)d * w * z;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = q / ((uint64_t)w * z), r = q % ((uint64_t)w * z), j = r / z, m = r % z;
+    grp[q] = fat[i * w * z + m * w + j];
+  }
+}
+__global__ void fold_scatter_k(const uint32_t* __restrict__ grp, uint32_t* __restrict__ fat, uint32_t d, uint32_t w,
+                               uint32_t z) {
+  const uint64_t total = (uint64_t)d * w * z;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = q / ((uint64_t)w * z), r = q % ((uint64_t)w * z), j = r / z, m = r % z;
+    fat[i * w * z + m * w + j] = grp[q];
+  }
+}
+
 template <int D>
-static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds,
-                         int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n64, int64_t* inc,
-                         int64_t* result, Layout& L, cudaStream_t st) {
+static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
+                         const uint64_t* fat_seeds, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
+                         int64_t n64, int64_t* inc, int64_t* result, Layout& L, cudaStream_t st) {
   const int sms = sm_count();
   const uint32_t n = (uint32_t)n64;
   const uint32_t N = (uint32_t)(D * n64);
@@ -1796,6 +1947,57 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
+  } else if (kind == 4 || kind == 5) {  // -------------------------- SF4 / SF3
+    // SF4: buckets by the slim seeds, slots by the extended seeds (as SFF).
+    // SF3: g = h_i(key) over w' = z w (slim seeds), bucket g mod w, slot g / w.
+    const int kb = bits_for((uint64_t)z);
+    const bool fold = kind == 5;
+    HashArgs<D> h = fold ? make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)wp, z, kb, L, 0)
+                         : make_hash<D>(ks, ops, n64, slim_seeds, fat_seeds, (uint64_t)w, z, kb, L, 0);
+    h.fold_w = (uint32_t)w;
+    if (fold) { note_launch(); hash_emit_k<D, 3><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
+    else { note_launch(); hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    const uint64_t cells = (uint64_t)D * w * z;
+    uint32_t* fat_grp = fat;
+    if (fold) {
+      { note_launch(); fold_gather_k<<<grid_for((int64_t)cells, 256, sms * 8), 256, 0, st>>>(fat, L.fat_snap, D, (uint32_t)w, (uint32_t)z); }
+      // the scan writes only the groups this batch touches
+      cudaMemcpyAsync(L.fat_perm, L.fat_snap, cells * 4, cudaMemcpyDeviceToDevice, st);
+      fat_grp = L.fat_perm;
+    } else {
+      cudaMemcpyAsync(L.fat_snap, fat, cells * 4, cudaMemcpyDeviceToDevice, st);
+    }
+    ScanOut so{L.fat_snap, fat_grp, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, 3, true>(z, L.k_out, L.v_out, N, kb, L.tiles, so, st)) return r;
+    if (fold) {
+      { note_launch(); fold_scatter_k<<<grid_for((int64_t)cells, 256, sms * 8), 256, 0, st>>>(L.fat_perm, fat, D, (uint32_t)w, (uint32_t)z); }
+      HashArgs<D> hf = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)wp, 1, 0, L, 0);
+      { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
+    } else {
+      { note_launch(); fat_undo_k<D, 0><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(h, fat, (uint32_t)z); }
+    }
+    if (int r = run_engine<D, 3>(L, slim, slim_seeds, w, ks, n, kb, inc, st)) return r;
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
+  } else if (kind == 6) {  // ------------------------------------------ SF2
+    // flat fat: per-op b_min (as SF1, deletes allowed); deletion sub-sketch on
+    // the slim cells: a second, slim-sorted scan carries its counts
+    HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 0);
+    { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
+    cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
+    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
+    if (int r = run_scan_z<true, 1, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
+    HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
+    { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
+    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    cudaMemcpyAsync(L.fat_snap, dsub, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
+    ScanOut sd{L.fat_snap, dsub, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<true, 3, true>(1, L.k_out, L.v_out, N, 0, L.tiles, sd, st)) return r;
+    { note_launch(); fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hs, dsub, 1u); }
+    if (int r = run_engine<D, 3>(L, slim, slim_seeds, w, ks, n, 0, inc, st, true)) return r;
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
@@ -1818,23 +2020,23 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, const uint64_t
   return check_launch("sf_parallel");
 }
 
-int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, const uint64_t* slim_seeds, const uint64_t* fat_seeds, int d,
-                   int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
-                   int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st) {
+int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
+                   const uint64_t* fat_seeds, int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
+                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st) {
   Layout L = carve(ws, ws_bytes, kind, d, w, wp, z, n);
   if (!L.ok || ws == nullptr) {
     set_error("workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
     return 1;
   }
   switch (d) {
-    case 1: return sf_parallel_d<1>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 2: return sf_parallel_d<2>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 3: return sf_parallel_d<3>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 4: return sf_parallel_d<4>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 5: return sf_parallel_d<5>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 6: return sf_parallel_d<6>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 7: return sf_parallel_d<7>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 8: return sf_parallel_d<8>(kind, slim, fat, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 1: return sf_parallel_d<1>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 2: return sf_parallel_d<2>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 3: return sf_parallel_d<3>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 4: return sf_parallel_d<4>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 5: return sf_parallel_d<5>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 6: return sf_parallel_d<6>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 7: return sf_parallel_d<7>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 8: return sf_parallel_d<8>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
   }
   set_error("parallel engine: unsupported d=%d", d);
   return 1;

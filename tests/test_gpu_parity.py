@@ -167,3 +167,38 @@ def test_sff_long_runs(oracle, seed, w, del_p):
         status, idx = apply_batches(sk, ops, keys, sequential=sequential)
         assert (status, idx) == st[:2]
         assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+
+
+@pytest.mark.parametrize("variant,wp", [("sf2", 16384), ("sf3", 16384), ("sf4", None)])
+@pytest.mark.parametrize("alpha", [0.8, 1.2])
+def test_sum_trigger_variants_at_scale(oracle, variant, wp, alpha):
+    """SF2 / SF3 / SF4 on the parallel engine (bucket or fold-group sums, the
+    deletion sub-sketch) against the oracle on a cfg-3 style stream."""
+    c = W.cfg3(seed=5, n_ins=1_000_000, v=50_000, alpha=alpha)
+    compare_cfg(oracle, variant, 4, 4096, 4, wp, 5, c["ops"], c["keys"], c["keys"].astype(np.uint64),
+                c["distinct"])
+
+
+@pytest.mark.parametrize("variant", ["sf2", "sf3", "sf4"])
+@pytest.mark.parametrize("seed,w,del_p", [(1, 64, 0.3), (3, 32, 0.49), (5, 16, 0.4)])
+def test_sum_trigger_long_runs(oracle, variant, seed, w, del_p):
+    ops, keys = long_run_stream(seed, w, n_bg=400, blocks=12, block_len=3000, del_p=del_p)
+    wp = 4 * w if variant in ("sf2", "sf3") else None
+    for sequential in (False, True):
+        o, st = oracle_run(oracle, variant, 4, w, 4, wp, seed, ops, keys.astype(np.uint64))
+        sk = make_sketch(variant, 4, w, 4, wp, seed)
+        status, idx = apply_batches(sk, ops, keys, sequential=sequential)
+        assert (status, idx) == st[:2]
+        assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat, o.dsub)
+
+
+@pytest.mark.parametrize("variant", ["sf2", "sf3", "sf4"])
+def test_sum_trigger_prefix_semantics(oracle, variant):
+    """A phantom delete deep inside a batch: the prefix applies, the failing
+    op leaves no trace, on the parallel engine."""
+    c = W.cfg3(seed=9, n_ins=200_000, v=5000, alpha=1.0)
+    ops, keys = c["ops"].copy(), c["keys"].copy()
+    keys[150_000] = np.uint32(0xDEADBEEF)
+    ops[150_000] = 1
+    wp = 4096 if variant in ("sf2", "sf3") else None
+    compare_cfg(oracle, variant, 4, 1024, 4, wp, 9, ops, keys, keys.astype(np.uint64), c["distinct"])

@@ -3,7 +3,8 @@ and query throughput through the public API, each checked bit-exact against
 the CPU oracle (test infrastructure), with the rate also expressed as a
 fraction of the measured random-gather roofline (profiles/gather_peaks.json).
 
-Usage: python tools/config_sweep.py [cfg ...]   (cfg in 1 2 3 4 5; default all)
+Usage: python tools/config_sweep.py [cfg ...]   (cfg in 1 2 3 4 5 v; default 1-5;
+       v = SF2/SF3/SF4 on the cfg-3 stream)
 Prints one JSON line per measurement; profiles/<round>/config_sweep.jsonl
 keeps the committed copy."""
 import json
@@ -121,6 +122,16 @@ def cfg3():
                    c["keys"].astype(np.uint64), 8, "gather_4MiB_Gps", c["distinct"], c["distinct"].astype(np.uint64))
 
 
+def variants():
+    """SF2 / SF3 / SF4 on the cfg-3 stream (alpha = 1.0):
+    not a BASELINE config, reported beside it."""
+    c = W.cfg3(seed=2017, alpha=1.0)
+    for v, wp in (("sf2", 262144), ("sf3", 262144), ("sf4", None)):
+        build_case("cfg3-stream " + v, v, P.SketchParams(d=4, w=65536, z=4, w_prime=wp, master_seed=2017), c["ops"],
+                   c["keys"], c["keys"].astype(np.uint64), 8, "gather_4MiB_Gps", c["distinct"],
+                   c["distinct"].astype(np.uint64))
+
+
 def cfg4():
     c = W.cfg4(seed=2017)
     recs = c["records"]
@@ -161,5 +172,5 @@ def cfg5():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
     for w_ in which:
-        {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5}[w_]()
+        {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "v": variants}[w_]()
         torch.cuda.empty_cache()
