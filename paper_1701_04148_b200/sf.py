@@ -4,11 +4,13 @@ Same classes, attributes and methods as the reference (``sf.py:50-258``);
 state lives in CUDA tensors and every update/query runs in the sm_100a
 kernels behind ``libsfsketch_cuda.so``:
 
-  SF1  flat fat (d, w'); no deletion           -> parallel engine
-  SF2  flat fat + deletion sub-sketch          -> sequential device engine
-  SF3  flat fat of width z*w folded onto w     -> sequential device engine
-  SF4  bucketed fat (d, w, z), sum trigger     -> sequential device engine
-  SFF  bucketed fat (d, w, z), max clamp       -> parallel engine
+  SF1  flat fat (d, w'); no deletion           -> parallel engine (max-raise runs)
+  SF2  flat fat + deletion sub-sketch          -> parallel engine (sum trigger, op-by-op runs)
+  SF3  flat fat of width z*w folded onto w     -> parallel engine (sum trigger, fold groups as buckets)
+  SF4  bucketed fat (d, w, z), sum trigger     -> parallel engine (sum trigger)
+  SFF  bucketed fat (d, w, z), max clamp       -> parallel engine (max clamp)
+
+  (d > 8, z > 8, or ``sequential=True`` use the exact one-thread device engine)
 
 Attributes tests read (``slim.counters``, ``slim.increment_counts``,
 ``slim.insertions_seen``, ``fat.counters``, ``deletion_sub.counters``,
