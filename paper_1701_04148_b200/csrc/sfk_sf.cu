@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
     const uint32_t t = v >> (kb + 1);
     const uint32_t op = (v >> kb) & 1u;
     const uint32_t row = c / o.row_cells;
+    uint32_t rec_own = 0, rec_oth = 0;  // observations carried in the link record
     if (HAS_FAT) {
       const uint32_t k = v & ((1u << kb) - 1u);
       uint32_t init[Z];
@@ -341,10 +342,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
             if (q2 != (int)k) sum += (uint64_t)((int64_t)init[q2] + run.v[q2]);
           others = (uint32_t)min(sum, (uint64_t)U32MAX);
         }
-        if (WRITE_LINKS) {  // links and observations interleaved: one 16-B store
-          const uint32_t prev = (e > run.head) ? prev_t : NONE32;
-          reinterpret_cast<uint4*>(o.links)[(size_t)t * o.D + row] =
-              make_uint4(e - run.head, prev, (uint32_t)post_own, others);
+        if (WRITE_LINKS) {
+          rec_own = (uint32_t)post_own;
+          rec_oth = others;
         } else {
           o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
         }
@@ -366,9 +366,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
         for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
       }
     }
-    if (WRITE_LINKS && !(HAS_FAT && (WRITE_OBS == 2 || WRITE_OBS == 3))) {
+    if (WRITE_LINKS) {
+      // One 32-B record per (op, row): rank in the cell, previous op,
+      // observations, the cell and the op's sorted position (row 0: its
+      // row-0 order index). Whole-sector scattered stores: a 16-B store into
+      // a sector written at another time costs L2 a DRAM fill.
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
-      o.links[(size_t)t * o.D + row] = make_uint2(e - run.head, prev);
+      uint4* rec = reinterpret_cast<uint4*>(o.links) + ((size_t)t * o.D + row) * 2;
+      rec[0] = make_uint4(e - run.head, prev, rec_own, rec_oth);
+      rec[1] = make_uint4(c, e, 0u, 0u);
     }
     prev_t = t;
   }
@@ -387,14 +393,33 @@ struct RunArgs {
   KeySrc keys;
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
-  uint32_t* headflag;      // [t]
-  uint32_t* head_e0;       // [t]
+  uint32_t* headflag;      // [t] (written by runs_head_k)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
   uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
   Ctl* ctl;
 };
 
+// Run heads in stream order (coalesced over t): op t continues the run
+// before it when all its d cells were last touched by the same op, of the
+// same key (the closed forms need the same key, not just the same cells).
+template <int D>
+__global__ void __launch_bounds__(256) runs_head_k(RunArgs<D> a) {
+  const uint32_t tstar = a.ctl->fail_t;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
+    const bool valid = t < tstar;
+    uint32_t prev[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) prev[i] = a.links[((size_t)t * D + i) * 4].y;
+    bool cont = valid && prev[0] != NONE32;
+#pragma unroll
+    for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
+    if (cont) cont = load_key(a.keys, prev[0]) == load_key(a.keys, t);
+    a.headflag[t] = (valid && !cont) ? 1u : 0u;
+  }
+}
+
+// Per op in row-0 order: flags, b_min (SF1/SF2), delete bits, run boundaries.
 template <int D>
 __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
   const uint32_t tstar = a.ctl->fail_t;
@@ -404,14 +429,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const uint32_t t = v >> (a.kb + 1);
     const uint32_t op = (v >> a.kb) & 1u;
     const bool valid = t < tstar;
-    uint32_t prev[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) prev[i] = a.links[((size_t)t * D + i) * a.lstride].y;
-    bool cont = valid && prev[0] != NONE32;
-#pragma unroll
-    for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
-    // the same d cells is not enough for the closed forms: require the same key
-    if (cont) cont = load_key(a.keys, prev[0]) == load_key(a.keys, t);
+    const bool cont = valid && !a.headflag[t];
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
     if (a.obs) {
       uint32_t b = U32MAX;
@@ -424,11 +442,8 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
       const unsigned bits = __ballot_sync(__activemask(), op != 0);
       if ((threadIdx.x & 31) == 0) a.delbits[e >> 5] = bits;
     }
-    const bool head = valid && !cont;
-    a.bnd[e] = (valid && cont) ? 0u : 1u;
+    a.bnd[e] = cont ? 0u : 1u;
     a.isdel[e] = op;
-    a.headflag[t] = head ? 1u : 0u;
-    a.head_e0[t] = e;
     if (valid && op == 0) ++ins;
   }
   // n_ins: warp reduce then one atomic per warp
@@ -455,7 +470,6 @@ template <int D>
 struct BuildArgs {
   const uint32_t* headflag;
   const uint32_t* ridx;
-  const uint32_t* head_e0;
   const uint8_t* opflags;
   const uint32_t* bidx;     // exclusive prefix count of boundaries (row-0 order)
   const uint32_t* bpos;     // position of the k-th boundary; bpos[K] = n
@@ -463,7 +477,7 @@ struct BuildArgs {
   const uint32_t* delbits;  // SFF
   const uint2* obs2;        // SFF
   const uint2* links;
-  int lstride;              // 2 when links and obs2 are interleaved in one uint4 per (t, row)
+  int lstride;              // 4 when links, obs2 and the cell share one 32-B record per (t, row)
   uint32_t n;
   KeySrc keys;
   Seeds<D> seeds;
@@ -487,7 +501,7 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     if (t == a.n - 1) a.ctl->n_runs = a.ridx[t] + a.headflag[t];
     if (!a.headflag[t]) continue;
     const uint32_t r = a.ridx[t];
-    const uint32_t e0 = a.head_e0[t];
+    const uint32_t e0 = a.links[((size_t)t * D) * 4 + 2].y;  // row-0 position of op t
     // the run ends at the next boundary (row-0 order)
     const uint32_t e_end = a.bpos[a.bidx[e0] + 1];
     const uint32_t L = e_end - e0;
@@ -502,11 +516,10 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
       if (sh) b |= a.delbits[(e0 >> 5) + 1] << (32u - sh);
       rec.bits0 = L >= 32 ? b : (b & ((1u << L) - 1u));
     }
-    const uint64_t key = load_key(a.keys, t);
     const bool head_del = a.opflags[e0] & 1u;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      rec.cells[i] = (uint32_t)i * a.w + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+      rec.cells[i] = a.links[((size_t)t * D + i) * 4 + 2].x;
       rec.rank[i] = a.links[((size_t)t * D + i) * a.lstride].x;
       if (a.obs2) {
         const uint2 ob = a.obs2[((size_t)t * D + i) * a.lstride];
@@ -1609,7 +1622,6 @@ struct Layout {
   uint32_t* opdata;
   uint32_t* headflag;
   uint32_t *bnd, *bidx, *bpos, *isdel, *delpre;
-  uint32_t* head_e0;
   uint32_t* ridx;
   uint32_t *run_e0, *run_info, *run_t;
   void* recs;
@@ -1659,7 +1671,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
     }
   }
   const bool engine = kind != 3;
-  L.links = cv.take<uint2>(engine ? (deletes ? 2 * N : N) : 1);
+  L.links = cv.take<uint2>(engine ? 4 * N : 1);
   L.opflags = cv.take<uint8_t>(engine ? n : 1);
   L.opdata = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);
   L.headflag = cv.take<uint32_t>(engine ? n : 1);
@@ -1668,7 +1680,6 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.bpos = cv.take<uint32_t>(engine ? n + 2 : 1);
   L.isdel = cv.take<uint32_t>(engine ? n + 1 : 1);
   L.delpre = cv.take<uint32_t>(engine ? n + 1 : 1);
-  L.head_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
   L.run_e0 = cv.take<uint32_t>(engine ? n : 1);
   L.run_info = cv.take<uint32_t>(engine ? n : 1);
@@ -1802,17 +1813,17 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.kb = kb;
   ra.n = n;
   ra.links = L.links;
-  ra.lstride = MODE >= 2 ? 2 : 1;
+  ra.lstride = 4;
   ra.obs = (MODE == 0 || b_opdata) ? L.obs : nullptr;
   ra.keys = ks;
   ra.opflags = L.opflags;
   ra.opdata = L.opdata;
   ra.headflag = L.headflag;
-  ra.head_e0 = L.head_e0;
   ra.delbits = MODE >= 2 ? L.delbits : nullptr;
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
   ra.ctl = L.ctl;
+  { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.headflag, L.ridx, (int)n, st);
@@ -1828,7 +1839,6 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   BuildArgs<D> ba;
   ba.headflag = L.headflag;
   ba.ridx = L.ridx;
-  ba.head_e0 = L.head_e0;
   ba.opflags = L.opflags;
   ba.bidx = L.bidx;
   ba.bpos = L.bpos;
@@ -1836,7 +1846,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.delbits = MODE >= 2 ? L.delbits : nullptr;
   ba.obs2 = MODE >= 2 ? L.links + 1 : nullptr;
   ba.links = L.links;
-  ba.lstride = MODE >= 2 ? 2 : 1;
+  ba.lstride = 4;
   ba.n = n;
   ba.keys = ks;
   for (int i = 0; i < D; ++i) ba.seeds.s[i] = slim_seeds[i];
