@@ -13,7 +13,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsfsketch_cuda.so")
+LIB_PATH = os.environ.get("SFK_LIB_PATH") or os.path.join(_HERE, "_lib", "libsfsketch_cuda.so")  # env: A/B builds
 CSRC = os.path.join(_HERE, "csrc")
 
 KEY_U64, KEY_U32, KEY_RECORD = 0, 1, 2

@@ -17,8 +17,9 @@
 //     the per-row partial counters meet over DSMEM, where CTA r takes the min
 //     for its quarter of the tile and stores the int64 estimates. Rows wider
 //     than 16 bits are stored as u16 codes: small values as is, large ones
-//     (>= 0xF000) as an index into a per-CTA overflow array of exact u32
-//     values, so estimates stay exact (see OVF_BASE).
+//     (>= 0xF800, a few hot cells) as their rank among all rows' large values,
+//     which the owner decodes from a local table, so estimates stay exact
+//     (see OVF_BASE and rank_codes_setup).
 #include <cooperative_groups.h>
 
 #include "sfk_common.cuh"
@@ -167,12 +168,39 @@ __device__ __forceinline__ uint32_t row_index(uint64_t key, uint64_t seed, const
   return (uint32_t)fmod64(mix64(key ^ seed), M);
 }
 
+// finalize64(key ^ seed) mod 2^k for a 32-bit key, in 32-bit halves: the
+// high word of key ^ seed is the seed's, so the first xor-shift's high half
+// and its share of the first multiply are per-CTA constants (U32Hash).
+struct U32Hash {
+  uint32_t slo;  // low word of the seed
+  uint32_t c1;   // seed_hi << 2: the high bits shifted into the low word by x >> 30
+  uint32_t c2;   // (seed_hi ^ seed_hi >> 30) * lo32(K1): the high-word term of x * K1
+};
+__host__ __device__ __forceinline__ U32Hash make_u32hash(uint64_t seed) {
+  const uint32_t hi = (uint32_t)(seed >> 32);
+  return U32Hash{(uint32_t)seed, hi << 2, (hi ^ (hi >> 30)) * 0x1CE4E5B9u};
+}
+__device__ __forceinline__ uint32_t row_index_u32(uint32_t key, const U32Hash& h, uint32_t mask) {
+  const uint32_t lo = key ^ h.slo;
+  const uint32_t lo1 = lo ^ (lo >> 30) ^ h.c1;
+  // x *= 0xBF58476D1CE4E5B9
+  const uint64_t w1 = (uint64_t)lo1 * 0x1CE4E5B9u + ((uint64_t)h.c2 << 32);
+  const uint32_t lo2 = (uint32_t)w1, hi2 = (uint32_t)(w1 >> 32) + lo1 * 0xBF58476Du;
+  // x ^= x >> 27
+  const uint32_t lo3 = lo2 ^ __funnelshift_r(lo2, hi2, 27), hi3 = hi2 ^ (hi2 >> 27);
+  // x *= 0x94D049BB133111EB
+  const uint64_t w2 = (uint64_t)lo3 * 0x133111EBu;
+  const uint32_t lo4 = (uint32_t)w2, hi4 = (uint32_t)(w2 >> 32) + lo3 * 0x94D049BBu + hi3 * 0x133111EBu;
+  // low word of x ^ (x >> 31)
+  return (lo4 ^ __funnelshift_r(lo4, hi4, 31)) & mask;
+}
+
 // u16 row encoding: values below OVF_BASE are stored as is; a larger value
 // gets the code OVF_BASE + s and its exact u32 value in overflow slot s of
 // its row; OVF_NONE marks a large value that found no slot (re-read from
 // global memory). Codes order below every large value, so a min over codes
-// that is < OVF_BASE is the exact min. Every CTA keeps a copy of all D rows'
-// overflow tables (a few hot cells each), so decoding stays in local smem.
+// that is < OVF_BASE is the exact min. At setup the codes become ranks among
+// all rows' large values (a few hot cells), so decoding is one local load.
 constexpr uint32_t OVF_BASE = 0xF800u;
 constexpr uint32_t OVF_NONE = 0xFFFFu;
 constexpr int OVF_SLOTS = (int)(OVF_NONE - OVF_BASE);  // 2047 per row
@@ -184,6 +212,55 @@ __device__ __forceinline__ uint64_t key_at(const KeySrc& k, int64_t t) {
   if (KK == SFK_KEY_U32) return (uint64_t)__ldg(static_cast<const unsigned int*>(k.p) + t);
   if (KK == SFK_KEY_U64) return __ldg(static_cast<const unsigned long long*>(k.p) + t);
   return record_key(static_cast<const uint8_t*>(k.p) + t * (int64_t)k.rec, k.rec);
+}
+
+// Setup of the u16 rank codes (kept out of line so it does not perturb the
+// main loop's register allocation): rank every large value among all rows'
+// large values (read over DSMEM) and re-encode this row's codes as
+// OVF_BASE + rank; codes then order like the values across rows, so the
+// owner decodes only the minimum code, with one local load. Exhausted
+// tables keep per-row slot codes. Returns whether the rank codes apply.
+template <int D, typename CT, int NT>
+__device__ __noinline__ int rank_codes_setup(CT* row, uint32_t* ovf, uint32_t* merged, uint32_t* own_rank, int64_t w,
+                                             uint32_t r) {
+  const uint32_t* tab[D];
+  int cnt[D], total = 0;
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    tab[q] = cg::this_cluster().map_shared_rank(ovf, q);
+    const int raw = (int)tab[q][OVF_SLOTS];
+    ok = ok && raw <= OVF_SLOTS;
+    cnt[q] = min(raw, OVF_SLOTS);
+    total += cnt[q];
+  }
+  ok = ok && total <= OVF_SLOTS;
+  if (ok) {
+    for (int idx = threadIdx.x; idx < total; idx += NT) {
+      int q = 0, s = idx;
+#pragma unroll
+      for (int qq = 0; qq < D - 1; ++qq)
+        if (s >= cnt[q]) s -= cnt[q], ++q;
+      const uint32_t v = tab[q][s];
+      int rank = 0;
+#pragma unroll 1
+      for (int q2 = 0; q2 < D; ++q2)
+        for (int s2 = 0; s2 < cnt[q2]; ++s2) rank += tab[q2][s2] < v;
+      merged[rank] = v;
+      if (q == (int)r) own_rank[s] = (uint32_t)rank;
+    }
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < w; k += NT) {
+      const uint32_t cde = row[k];
+      if (cde >= OVF_BASE && cde != OVF_NONE) row[k] = (CT)(OVF_BASE + own_rank[cde - OVF_BASE]);
+    }
+  } else {
+    // exhausted: every large value re-reads its u32 counter from global memory
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < w; k += NT)
+      if ((uint32_t)row[k] >= OVF_BASE) row[k] = (CT)OVF_NONE;
+  }
+  return ok ? 1 : 0;
 }
 
 // Row-partitioned cluster query. A cluster of D CTAs; CTA r holds slim row r
@@ -211,9 +288,12 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
   const uint32_t r = cg::this_cluster().block_rank();
   CT* row = reinterpret_cast<CT*>(smem_raw);
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
+  // u16 rows: this row's overflow table (values + count, read by the peers
+  // during setup) and the cluster-wide rank table (rank -> value)
   uint32_t* ovf = reinterpret_cast<uint32_t*>(smem_raw + row_bytes);
-  CT* recv = reinterpret_cast<CT*>(smem_raw + row_bytes + (U16 ? D * OVF_STRIDE * 4 : 0));
-  uint32_t* my_ovf = ovf + r * OVF_STRIDE;
+  uint32_t* merged = ovf + OVF_STRIDE;
+  CT* recv = reinterpret_cast<CT*>(smem_raw + row_bytes + (U16 ? 2 * OVF_STRIDE * 4 : 0));
+  uint32_t* my_ovf = ovf;
   int& novf = *reinterpret_cast<int*>(my_ovf + OVF_SLOTS);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(recv + (size_t)QNB * D * Q);
   // bars[0..QNB) = full, bars[QNB..2QNB) = empty
@@ -245,6 +325,8 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
 #pragma unroll
   for (int i = 1; i < D; ++i)
     if (i == (int)r) seed = seeds.s[i];
+  const U32Hash h32 = make_u32hash(seed);
+  const uint32_t mask32 = (uint32_t)wm.mask;
   const uint32_t recv_a = smem_addr(recv), bars_a = smem_addr(bars);
   uint32_t peer_recv[D], peer_full[D];
 #pragma unroll
@@ -253,15 +335,9 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
     peer_full[q] = mapa_u32(bars_a, q);
   }
   cluster_sync_all();  // rows staged, barriers initialised cluster-wide
-  if (U16) {  // copy the peers' overflow tables
-#pragma unroll 1
-    for (int q = 0; q < D; ++q) {
-      if (q == (int)r) continue;
-      const uint32_t* pt = cg::this_cluster().map_shared_rank(ovf + q * OVF_STRIDE, q);
-      const int cnt = min(pt[OVF_SLOTS], OVF_SLOTS);
-      for (int s = threadIdx.x; s < cnt; s += NT) ovf[q * OVF_STRIDE + s] = pt[s];
-    }
-    __syncthreads();
+  if (U16) {
+    (void)rank_codes_setup<D, CT, NT>(row, ovf, merged, reinterpret_cast<uint32_t*>(recv), w, r);
+    cluster_sync_all();  // peers done reading this table; recv scratch free
   }
 
   const int64_t ntiles = (n + TILE - 1) / TILE;
@@ -310,10 +386,10 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
       if (VEC && base + TILE <= n) {
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
-          c[j][0] = row[row_index<POW2>(VEC ? kk[j].x : 0u, seed, wm)];
-          c[j][1] = row[row_index<POW2>(VEC ? kk[j].y : 0u, seed, wm)];
-          c[j][2] = row[row_index<POW2>(VEC ? kk[j].z : 0u, seed, wm)];
-          c[j][3] = row[row_index<POW2>(VEC ? kk[j].w : 0u, seed, wm)];
+          c[j][0] = row[POW2 ? row_index_u32(VEC ? kk[j].x : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].x : 0u, seed, wm)];
+          c[j][1] = row[POW2 ? row_index_u32(VEC ? kk[j].y : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].y : 0u, seed, wm)];
+          c[j][2] = row[POW2 ? row_index_u32(VEC ? kk[j].z : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].z : 0u, seed, wm)];
+          c[j][3] = row[POW2 ? row_index_u32(VEC ? kk[j].w : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].w : 0u, seed, wm)];
         }
       } else {
 #pragma unroll
@@ -369,43 +445,22 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
           for (int p = 1; p < D; ++p) m[u] = min(m[u], cc[p][u]);
         }
         if (U16) {
-          // keys whose every row holds a large value: decode all of their
-          // codes in one batch of predicated local loads
-          bool need[4], any = false;
+          // codes below OVF_NONE are ranks across all rows: the minimum code
+          // decodes alone; OVF_NONE (overflow tables exhausted) re-reads the
+          // key's d u32 counters
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            need[u] = m[u] >= OVF_BASE && t + u < n;
-            any |= need[u];
-          }
-          if (any) {
-            uint32_t v[D][4];
-            bool none = false;
-#pragma unroll
-            for (int p = 0; p < D; ++p)
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const bool slot = need[u] && cc[p][u] != OVF_NONE;
-                v[p][u] = slot ? ovf[p * OVF_STRIDE + (cc[p][u] - OVF_BASE)] : U32MAX;
-                none |= need[u] && !slot;
-              }
-            if (none) {  // overflow slots exhausted for some row: exact global re-read
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (!need[u]) continue;
+            if (m[u] >= OVF_BASE) {
+              if (m[u] != OVF_NONE) {
+                m[u] = merged[m[u] - OVF_BASE];
+              } else if (t + u < n) {
                 const uint64_t key = key_at<KK>(keys, t + u);
+                uint32_t mm = U32MAX;
 #pragma unroll
                 for (int p = 0; p < D; ++p)
-                  if (cc[p][u] == OVF_NONE)
-                    v[p][u] = __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm));
+                  mm = min(mm, __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm)));
+                m[u] = mm;
               }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (!need[u]) continue;
-              uint32_t mm = v[0][u];
-#pragma unroll
-              for (int p = 1; p < D; ++p) mm = min(mm, v[p][u]);
-              m[u] = mm;
             }
           }
         }
@@ -436,7 +491,7 @@ static int try_cluster_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, i
   constexpr int NT = 512;
   constexpr int Q = ((TILE + D - 1) / D + 3) & ~3;
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
-  const size_t smem = row_bytes + (sizeof(CT) == 2 ? D * OVF_STRIDE * 4 : 0) + (size_t)QNB * D * Q * sizeof(CT) +
+  const size_t smem = row_bytes + (sizeof(CT) == 2 ? 2 * OVF_STRIDE * 4 : 0) + (size_t)QNB * D * Q * sizeof(CT) +
                       2 * QNB * 8;
   if (smem + 1024 > (size_t)optin) return -1;
   auto kern = min_query_cluster<D, CT, TILE, NT, KK, VEC, POW2>;

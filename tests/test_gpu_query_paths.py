@@ -67,18 +67,25 @@ def test_query_paths_u32_keys(oracle, d, w, hi, path, n):
     np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
-def test_cluster_hot_keys_take_the_exact_regather(oracle):
-    """Keys whose every row counter is >= 65535 (the hot keys of a Zipf
-    stream) must come back with their exact u32 minimum."""
+@pytest.mark.parametrize("n_hot,distinct_vals", [(300, 0), (300, 7), (1000, 0)])
+def test_cluster_hot_keys_take_the_exact_regather(oracle, n_hot, distinct_vals):
+    """Keys whose every row counter is large (the hot keys of a Zipf stream)
+    must come back with their exact u32 minimum: through the cluster-wide
+    rank codes (few large cells, ties across rows when distinct_vals > 0)
+    or, when the overflow tables run out, through the per-row decode."""
     d, w = 4, 65536
-    rng = np.random.default_rng(3)
+    rng = np.random.default_rng(3 + n_hot + distinct_vals)
     seeds = seed_array(2017, 0, d)
     keys = rng.integers(0, 1 << 32, size=300_000, dtype=np.uint64).astype(np.uint32)
     c = rng.integers(0, 60000, size=(d, w), dtype=np.uint64).astype(np.uint32)
-    hot = keys[:1000].astype(np.uint64)
+    hot = keys[:n_hot].astype(np.uint64)
+    pool = 63488 + rng.integers(0, 1 << 20, size=max(distinct_vals, 1)).astype(np.uint32)
     for i in range(d):
         idx = oracle.min_query(np.arange(w, dtype=np.uint32)[None, :].repeat(1, 0), seeds[i:i + 1], hot)
-        c[i, idx] = 65535 + rng.integers(0, 1 << 20, size=idx.size).astype(np.uint32)
+        if distinct_vals:
+            c[i, idx] = rng.choice(pool, size=idx.size)
+        else:
+            c[i, idx] = 63488 + rng.integers(0, 1 << 20, size=idx.size).astype(np.uint32)
     ct = torch.from_numpy(c).cuda()
     kt = torch.from_numpy(keys).cuda()
     out = torch.empty(keys.size, dtype=torch.int64, device="cuda")
@@ -86,7 +93,7 @@ def test_cluster_hot_keys_take_the_exact_regather(oracle):
     got = out.cpu().numpy()
     want = oracle.min_query(c, seeds, keys.astype(np.uint64))
     np.testing.assert_array_equal(got, want)
-    assert (got[:1000] >= 65535).all()
+    assert (got[:n_hot] >= 63488).all()
 
 
 @pytest.mark.parametrize("path", [L2, CLUSTER])
