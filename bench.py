@@ -405,6 +405,15 @@ def run_ours(args):
                         "runs_per_launch": int(runs), "peak_source": hbm_src,
                         "note": "latency-bound: runs wait on the slim cells their predecessors write; "
                                 "see DESIGN.md for the critical-path depth"}
+        hl = os.path.join(ROOT, "profiles", "hop_latency.json")
+        if os.path.exists(hl) and args.alpha == 1.0:
+            with open(hl) as fh:
+                h = json.load(fh)
+            floor_ms = h["cfg3_alpha1_critical_hops"] * h["hop_ns_idle"] * 1e-6
+            rf["engine"]["latency_roofline"] = {
+                "critical_hops": h["cfg3_alpha1_critical_hops"], "hop_ns_floor": h["hop_ns_idle"],
+                "floor_ms": round(floor_ms, 3), "frac": round(floor_ms / eng_ms, 4),
+                "source": "profiles/hop_latency.json (tools/hop_latency.cu ping-pong; tools/trace_engine.py hops)"}
     dominant = "engine" if "engine" in rf and eng_ms > query_ms else "query"
     roofline = dict(rf[dominant])
     roofline["dominant"] = dominant
