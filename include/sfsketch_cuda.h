@@ -121,6 +121,16 @@ int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_
 int sfk_query_path(int mode);
 int sfk_query_last_path(void);
 
+/* Two-phase form of sfk_min_query (no reference counterpart; same
+ * estimates). sfk_query_index writes each key's bucket index for every row
+ * as uint16 (w <= 65536): idx[r * n + t] = h_r(key_t). It reads no counters,
+ * so it may run while the sketch is still being updated on another stream.
+ * sfk_min_query_idx then computes out[t] = min_r counters[r, idx[r * n + t]]. */
+int sfk_query_index(const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind, int rec_len, int64_t n,
+                    uint16_t* idx, void* stream);
+int sfk_min_query_idx(const uint32_t* counters, int d, int64_t w, const uint16_t* idx, int64_t n, int64_t* out,
+                      void* stream);
+
 /* Replaces _kernels.cm_apply (_kernels.py:62-88), called from
  * CmSketch.apply_ops (baselines.py:72-78). */
 size_t sfk_cm_workspace_size(int d, int64_t w, int64_t n);

@@ -43,6 +43,8 @@ EXPORTS = (
     "sfk_engine_trace",
     "sfk_query_path",
     "sfk_query_last_path",
+    "sfk_query_index",
+    "sfk_min_query_idx",
 )
 
 _lib = None
@@ -87,6 +89,8 @@ def load_library() -> ctypes.CDLL:
     L.sfk_engine_last_ms.restype = ctypes.c_float
     L.sfk_engine_trace.argtypes = [P, SZ]
     L.sfk_query_path.argtypes = [I]
+    L.sfk_query_index.argtypes = [P, I, I64, P, I, I, I64, P, P]
+    L.sfk_min_query_idx.argtypes = [P, I, I64, P, I64, P, P]
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]
     _lib = L
     return L

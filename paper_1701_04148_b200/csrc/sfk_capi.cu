@@ -48,6 +48,8 @@ int sm_count() {
 int launch_min_query(const uint32_t*, const uint64_t*, int, int64_t, KeySrc, int64_t, int64_t*, cudaStream_t);
 int launch_mix_batch(const uint64_t*, int64_t, uint64_t*, cudaStream_t);
 int query_path(int mode);
+int launch_query_index(const uint64_t*, int, int64_t, KeySrc, int64_t, uint16_t*, cudaStream_t);
+int launch_min_query_idx(const uint32_t*, int, int64_t, const uint16_t*, int64_t, int64_t*, cudaStream_t);
 int query_last_path();
 int launch_load_keys(KeySrc, int64_t, uint64_t*, cudaStream_t);
 int launch_gen_query_keys(uint64_t, const uint32_t*, const uint32_t*, uint32_t, const double*, int64_t, int64_t,
@@ -145,6 +147,21 @@ int sfk_engine_stats(unsigned long long* out8, int reset) { return engine_stats(
 int sfk_engine_timing(int on) { return engine_timing(on); }
 
 int sfk_query_path(int mode) { return query_path(mode); }
+
+int sfk_query_index(const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind, int rec_len, int64_t n,
+                    uint16_t* idx, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  return launch_query_index(seeds, d, w, KeySrc{keys, key_kind, rec_len}, n, idx, (cudaStream_t)stream);
+}
+
+int sfk_min_query_idx(const uint32_t* counters, int d, int64_t w, const uint16_t* idx, int64_t n, int64_t* out,
+                      void* stream) {
+  if (d < 1 || d > MAXSEEDS || w < 1) {
+    set_error("bad sketch shape d=%d w=%lld", d, (long long)w);
+    return 1;
+  }
+  return launch_min_query_idx(counters, d, w, idx, n, out, (cudaStream_t)stream);
+}
 
 int sfk_query_last_path(void) { return query_last_path(); }
 

@@ -207,6 +207,10 @@ constexpr int OVF_SLOTS = (int)(OVF_NONE - OVF_BASE);  // 2047 per row
 constexpr int OVF_STRIDE = OVF_SLOTS + 1;               // + the slot count
 constexpr int QNB = 2;                                 // receive buffers per CTA
 
+// internal key kind: precomputed u16 row indices (sfk_query_index), row r's
+// stream at p + r * n
+constexpr int KEY_IDX16 = 3;
+
 template <int KK>
 __device__ __forceinline__ uint64_t key_at(const KeySrc& k, int64_t t) {
   if (KK == SFK_KEY_U32) return (uint64_t)__ldg(static_cast<const unsigned int*>(k.p) + t);
@@ -349,8 +353,18 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
   const uint32_t* k32 = static_cast<const uint32_t*>(keys.p);
 
   uint4 kn[VEC ? VPT : 1];
+  const uint16_t* i16 = KK == KEY_IDX16 ? static_cast<const uint16_t*>(keys.p) + (int64_t)r * n : nullptr;
   auto prefetch = [&](int64_t it) {
-    if (VEC && it < T) {
+    if (VEC && KK == KEY_IDX16 && it < T) {  // four u16 row indices per 8-B load
+      const int64_t base = (cid + it * nclusters) * TILE;
+      const uint2* src2 = reinterpret_cast<const uint2*>(i16 + base) + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int64_t t = base + 4 * threadIdx.x + (int64_t)j * 4 * NT;
+        const uint2 v = (t + 3 < n) ? __ldcs(src2 + j * NT) : make_uint2(0, 0);
+        kn[j] = make_uint4(v.x, v.y, 0, 0);
+      }
+    } else if (VEC && it < T) {
       const int64_t base = (cid + it * nclusters) * TILE;
       const uint4* src4 = reinterpret_cast<const uint4*>(k32 + base) + threadIdx.x;
       if (base + TILE <= n) {
@@ -386,6 +400,13 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
       if (VEC && base + TILE <= n) {
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
+          if (KK == KEY_IDX16) {
+            c[j][0] = row[kk[j].x & 0xFFFFu];
+            c[j][1] = row[kk[j].x >> 16];
+            c[j][2] = row[kk[j].y & 0xFFFFu];
+            c[j][3] = row[kk[j].y >> 16];
+            continue;
+          }
           c[j][0] = row[POW2 ? row_index_u32(VEC ? kk[j].x : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].x : 0u, seed, wm)];
           c[j][1] = row[POW2 ? row_index_u32(VEC ? kk[j].y : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].y : 0u, seed, wm)];
           c[j][2] = row[POW2 ? row_index_u32(VEC ? kk[j].z : 0u, h32, mask32) : row_index<POW2>(VEC ? kk[j].z : 0u, seed, wm)];
@@ -397,7 +418,9 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
           const int64_t t = base + 4 * threadIdx.x + j * 4 * NT;
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            c[j][u] = (t + u < n) ? (uint32_t)row[row_index<POW2>(key_at<KK>(keys, t + u), seed, wm)] : 0u;
+            c[j][u] = (t + u < n) ? (KK == KEY_IDX16 ? (uint32_t)row[i16[t + u]]
+                                                     : (uint32_t)row[row_index<POW2>(key_at<KK>(keys, t + u), seed, wm)])
+                                  : 0u;
         }
       }
 #pragma unroll
@@ -454,11 +477,17 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
               if (m[u] != OVF_NONE) {
                 m[u] = merged[m[u] - OVF_BASE];
               } else if (t + u < n) {
-                const uint64_t key = key_at<KK>(keys, t + u);
                 uint32_t mm = U32MAX;
+                if (KK == KEY_IDX16) {
+                  const uint16_t* ix = static_cast<const uint16_t*>(keys.p);
 #pragma unroll
-                for (int p = 0; p < D; ++p)
-                  mm = min(mm, __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm)));
+                  for (int p = 0; p < D; ++p) mm = min(mm, __ldg(counters + (int64_t)p * w + ix[(int64_t)p * n + t + u]));
+                } else {
+                  const uint64_t key = key_at<KK>(keys, t + u);
+#pragma unroll
+                  for (int p = 0; p < D; ++p)
+                    mm = min(mm, __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm)));
+                }
                 m[u] = mm;
               }
             }
@@ -620,6 +649,129 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
   { note_launch(); min_query_l2<D, 4><<<blocks, 256, 0, st>>>(counters, sd, wm, w, ks, n, out); }
   g_query_last = 1;
   return check_launch("min_query_l2");
+}
+
+
+// ---- two-phase query: row indices now, gathers later ------------------------
+// sfk_query_index writes, for each key t and row r, its bucket index as u16
+// at idx[r * n + t] (needs w <= 65536). sfk_min_query_idx then gathers and
+// takes the min from those indices; the cluster kernel runs with
+// KK = KEY_IDX16 and reads 2 B per key and row instead of hashing. The index
+// pass reads 4 B and writes 2d B per key; it does not need the counters, so
+// it can run while the sketch is still being built.
+template <int D>
+__global__ void __launch_bounds__(256) query_index_k(Seeds<D> seeds, Mod wm, KeySrc keys, int64_t n,
+                                                     uint16_t* __restrict__ idx, int vec_ok) {
+  U32Hash h[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) h[i] = make_u32hash(seeds.s[i]);
+  const uint32_t mask = (uint32_t)wm.mask;
+  const bool fast = vec_ok && keys.kind == SFK_KEY_U32 && wm.pow2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; t < n; t += stride) {
+    if (fast && t + 3 < n) {
+      const uint4 k = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(keys.p) + t));
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const uint32_t a0 = row_index_u32(k.x, h[i], mask), a1 = row_index_u32(k.y, h[i], mask);
+        const uint32_t a2 = row_index_u32(k.z, h[i], mask), a3 = row_index_u32(k.w, h[i], mask);
+        __stcs(reinterpret_cast<uint2*>(idx + (int64_t)i * n + t), make_uint2(a0 | (a1 << 16), a2 | (a3 << 16)));
+      }
+    } else {
+      for (int u = 0; u < 4 && t + u < n; ++u) {
+        const uint64_t key = load_key(keys, t + u);
+#pragma unroll
+        for (int i = 0; i < D; ++i) idx[(int64_t)i * n + t + u] = (uint16_t)fmod64(mix64(key ^ seeds.s[i]), wm);
+      }
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) min_query_idx_l2(const uint32_t* __restrict__ counters, int64_t w,
+                                                        const uint16_t* __restrict__ idx, int64_t n,
+                                                        int64_t* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = U32MAX;
+#pragma unroll
+    for (int i = 0; i < D; ++i) m = min(m, __ldg(counters + (int64_t)i * w + idx[(int64_t)i * n + t]));
+    out[t] = (int64_t)m;
+  }
+}
+
+template <int D>
+static int launch_index_d(const uint64_t* seeds_host, int64_t w, KeySrc ks, int64_t n, uint16_t* idx, cudaStream_t st) {
+  Seeds<D> sd;
+  for (int i = 0; i < D; ++i) sd.s[i] = seeds_host[i];
+  const int vec_ok = ks.kind == SFK_KEY_U32 && (reinterpret_cast<uintptr_t>(ks.p) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(idx) & 7) == 0 && (n & 3) == 0;
+  { note_launch(); query_index_k<D><<<grid_for((n + 3) / 4, 256, sm_count() * 8), 256, 0, st>>>(sd, make_mod((uint64_t)w), ks, n, idx, vec_ok); }
+  return check_launch("query_index");
+}
+
+template <int D>
+static int launch_query_idx_d(const uint32_t* counters, int64_t w, const uint16_t* idx, int64_t n, int64_t* out,
+                              cudaStream_t st) {
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  Seeds<D> sd{};
+  const Mod wm = make_mod((uint64_t)w);
+  const KeySrc ks{idx, KEY_IDX16, 0};
+  const bool vec = (reinterpret_cast<uintptr_t>(idx) & 7) == 0 && (n & 3) == 0;
+  if (D >= 2 && D <= 8 && g_query_path != 1 && n >= (int64_t(1) << 21)) {
+    int rc = vec ? try_cluster_k<D, uint16_t, 8192, KEY_IDX16, true, true>(counters, sd, wm, w, ks, n, out, st, optin)
+                 : try_cluster_k<D, uint16_t, 8192, KEY_IDX16, false, true>(counters, sd, wm, w, ks, n, out, st, optin);
+    if (rc >= 0) return rc;
+  }
+  { note_launch(); min_query_idx_l2<D><<<grid_for(n, 256, sm_count() * 8), 256, 0, st>>>(counters, w, idx, n, out); }
+  g_query_last = 1;
+  return check_launch("min_query_idx_l2");
+}
+
+int launch_query_index(const uint64_t* seeds_host, int d, int64_t w, KeySrc ks, int64_t n, uint16_t* idx,
+                       cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (w > 65536) {
+    set_error("sfk_query_index: w=%lld exceeds the u16 index range", (long long)w);
+    return 1;
+  }
+  switch (d) {
+    case 1: return launch_index_d<1>(seeds_host, w, ks, n, idx, st);
+    case 2: return launch_index_d<2>(seeds_host, w, ks, n, idx, st);
+    case 3: return launch_index_d<3>(seeds_host, w, ks, n, idx, st);
+    case 4: return launch_index_d<4>(seeds_host, w, ks, n, idx, st);
+    case 5: return launch_index_d<5>(seeds_host, w, ks, n, idx, st);
+    case 6: return launch_index_d<6>(seeds_host, w, ks, n, idx, st);
+    case 7: return launch_index_d<7>(seeds_host, w, ks, n, idx, st);
+    case 8: return launch_index_d<8>(seeds_host, w, ks, n, idx, st);
+  }
+  set_error("sfk_query_index: unsupported d=%d", d);
+  return 1;
+}
+
+int launch_min_query_idx(const uint32_t* counters, int d, int64_t w, const uint16_t* idx, int64_t n, int64_t* out,
+                         cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (w > 65536) {
+    set_error("sfk_min_query_idx: w=%lld exceeds the u16 index range", (long long)w);
+    return 1;
+  }
+  switch (d) {
+    case 1: return launch_query_idx_d<1>(counters, w, idx, n, out, st);
+    case 2: return launch_query_idx_d<2>(counters, w, idx, n, out, st);
+    case 3: return launch_query_idx_d<3>(counters, w, idx, n, out, st);
+    case 4: return launch_query_idx_d<4>(counters, w, idx, n, out, st);
+    case 5: return launch_query_idx_d<5>(counters, w, idx, n, out, st);
+    case 6: return launch_query_idx_d<6>(counters, w, idx, n, out, st);
+    case 7: return launch_query_idx_d<7>(counters, w, idx, n, out, st);
+    case 8: return launch_query_idx_d<8>(counters, w, idx, n, out, st);
+  }
+  set_error("sfk_min_query_idx: unsupported d=%d", d);
+  return 1;
 }
 
 int launch_min_query(const uint32_t* counters, const uint64_t* seeds_host, int d,

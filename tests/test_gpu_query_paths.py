@@ -136,3 +136,60 @@ def test_auto_path_picks_cluster_for_cfg5_shape():
     out = torch.empty(n, dtype=torch.int64, device="cuda")
     assert run_query(c, seeds, keys, _lib.KEY_U32, 0, n, out, 0) == CLUSTER
     assert int(out.max()) == 0
+
+
+def two_phase(counters, seeds, keys_t, kind, n, out_t, stream=None, gather_stream=None):
+    L = _lib.lib()
+    d, w = counters.shape
+    idx = torch.empty(d * max(n, 1), dtype=torch.uint16, device="cuda")
+    s1 = _lib.stream_ptr(stream)
+    _lib.check(L.sfk_query_index(seeds.ctypes.data_as(ctypes.c_void_p), d, w, keys_t.data_ptr(), kind, 0, n,
+                                 idx.data_ptr(), s1), "sfk_query_index")
+    if gather_stream is not None:
+        gather_stream.wait_stream(stream)
+    _lib.check(L.sfk_min_query_idx(counters.data_ptr(), d, w, idx.data_ptr(), n, out_t.data_ptr(),
+                                   _lib.stream_ptr(gather_stream)), "sfk_min_query_idx")
+    torch.cuda.synchronize()
+    return L.sfk_query_last_path()
+
+
+@pytest.mark.parametrize("d,w,hi", [(4, 65536, 1 << 17), (4, 65536, 70000), (3, 40000, 1 << 20), (2, 1024, 1 << 32),
+                                    (5, 65536, 1000)])
+@pytest.mark.parametrize("n", [1, 4097, 3_000_001, 4_194_304])
+def test_two_phase_query_matches_oracle(oracle, d, w, hi, n):
+    """sfk_query_index + sfk_min_query_idx == min_query (_kernels.py:229-241)."""
+    rng = np.random.default_rng(d + w + n)
+    c = table(rng, d, w, hi)
+    seeds = seed_array(31 + d, 0, d)
+    keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    two_phase(torch.from_numpy(c).cuda(), seeds, torch.from_numpy(keys).cuda(), _lib.KEY_U32, n, out)
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, keys.astype(np.uint64)))
+
+
+def test_two_phase_index_overlaps_a_build(oracle):
+    """The index pass reads no counters: it may run on another stream while
+    the sketch is being built; the gathers after the build see the final slim."""
+    import paper_1701_04148_b200 as P
+    from paper_1701_04148_b200 import workloads as W
+
+    c = W.cfg3(seed=4, n_ins=2_000_000, v=100_000, alpha=1.0)
+    sk = P.SfSketch(P.SketchParams(d=4, w=65536, z=4, master_seed=4), "sff")
+    q = W.query_keys(9, c["distinct"], 1.0, 0, 4_000_000)
+    qt = torch.from_numpy(q).cuda()
+    ops, keys = torch.from_numpy(c["ops"]).cuda(), torch.from_numpy(c["keys"]).cuda()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    L = _lib.lib()
+    idx = torch.empty(4 * q.size, dtype=torch.uint16, device="cuda")
+    _lib.check(L.sfk_query_index(sk._slim_seeds.ctypes.data_as(ctypes.c_void_p), 4, 65536, qt.data_ptr(),
+                                 _lib.KEY_U32, 0, q.size, idx.data_ptr(), _lib.stream_ptr(side)), "index")
+    sk.apply_ops(ops, keys)  # current stream, concurrently
+    torch.cuda.current_stream().wait_stream(side)
+    out = torch.empty(q.size, dtype=torch.int64, device="cuda")
+    _lib.check(L.sfk_min_query_idx(sk.slim.counters.data_ptr(), 4, 65536, idx.data_ptr(), q.size, out.data_ptr(),
+                                   _lib.stream_ptr()), "gather")
+    np.testing.assert_array_equal(out.cpu().numpy(), sk.query_many(qt).cpu().numpy())
+    o = oracle.OracleSketch("sff", 4, 65536, 4, None, 4)
+    o.apply_ops(c["ops"], c["keys"].astype(np.uint64))
+    np.testing.assert_array_equal(out.cpu().numpy()[:200_000], o.query_many(q[:200_000].astype(np.uint64)))
