@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(1024) segscan_tiles_k(SegState<Z>* __restrict_
 struct ScanOut {
   const uint32_t* fat_init;  // snapshot of the fat (cell-major, Z per cell)
   uint32_t* fat_out;         // final fat (written at segment ends)
-  uint32_t* obs;             // [t*D + row]: post own count (insert) / bucket max (delete)
+  uint32_t* obs;             // WRITE_OBS 1: [t*D + row] post own count / bucket max; 4: [t] min over rows (b_min)
   uint2* obs2;               // [t*D + row]: {own slot count after the op, max of the other slots}
   uint2* links;              // [t*D + row]: {rank of the op in its cell, previous op on the cell or NONE}
   uint32_t n;                // ops
@@ -349,6 +349,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
           o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
         }
       }
+      if (WRITE_OBS == 4) {
+        // b_min of op t = min over its d rows of the post-op own fat count:
+        // one 4-B atomicMin per (op, row) into a per-op word (a scattered
+        // 4-B store per (op, row) would cost L2 a DRAM fill per sector)
+        atomicMin(o.obs + t, (uint32_t)min(post_own, (int64_t)U32MAX));
+      }
       if (WRITE_OBS == 1) {
         uint32_t ob;
         if (op == 0) {
@@ -389,7 +395,7 @@ struct RunArgs {
   uint32_t n;
   const uint2* links;      // {rank in cell, prev op} per (t, row), every lstride-th uint2
   int lstride;
-  const uint32_t* obs;     // SF1: post-insert own fat count per (t, row); null otherwise
+  const uint32_t* obs;     // SF1/SF2: b_min per op [t] (segscan WRITE_OBS 4); null otherwise
   KeySrc keys;
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
@@ -431,12 +437,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const bool valid = t < tstar;
     const bool cont = valid && !a.headflag[t];
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
-    if (a.obs) {
-      uint32_t b = U32MAX;
-#pragma unroll
-      for (int i = 0; i < D; ++i) b = min(b, a.obs[(size_t)t * D + i]);
-      a.opdata[e] = b;
-    }
+    if (a.obs) a.opdata[e] = a.obs[t];  // per-op b_min (segscan WRITE_OBS 4)
     if (a.delbits) {
       // e advances in warp-aligned strides, so the ballot covers one word
       const unsigned bits = __ballot_sync(__activemask(), op != 0);
@@ -1657,7 +1658,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
   L.fat_perm = cv.take<uint32_t>(kind == 5 ? fat_cells : 1);
   const bool need_obs = kind == 1 || kind == 6;
-  L.obs = cv.take<uint32_t>(need_obs ? N : 1);
+  L.obs = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);  // per-op b_min
   L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
   L.delbits = cv.take<uint32_t>(deletes ? n / 32 + 16 : 1);
   L.wsum = cv.take<uint32_t>(kind == 0 ? n / 32 + 32 : 1);
@@ -1948,7 +1949,8 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
-    if (int r = run_scan_z<true, 1, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
+    if (int r = run_scan_z<true, 4, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
@@ -1997,7 +1999,8 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
-    if (int r = run_scan_z<true, 1, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
+    if (int r = run_scan_z<true, 4, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }

@@ -1,5 +1,5 @@
-# engine tuning sweep (diagnostics): critical-path trace per knob value
-for v in 0 2 8 32; do
-  echo "nap=$v"; SFK_ENGINE_NAP=$v SFK_ENGINE_TRACE=1 timeout 300 python tools/trace_engine.py 1.0 2>&1 | sed -n 1,2p
-done
-SFK_ENGINE_NAP=8 SFK_ENGINE_TRACE=1 timeout 300 python tools/trace_engine.py 0.5 2>&1 | sed -n 1,2p
+# build timing check (diagnostics)
+for a in 1.0; do timeout 300 python tools/one_build.py sff $a 3 2>&1 | grep "rep 2"; done
+timeout 300 python tools/one_build.py sf1 1.0 3 2>&1 | grep "rep 2"
+timeout 300 python tools/one_build.py sf1rec 1.2 2 2>&1 | grep "rep 1"
+timeout 300 python tools/one_build.py cu 1.0 3 2>&1 | grep "rep 2"
