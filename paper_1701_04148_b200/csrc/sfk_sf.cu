@@ -1769,10 +1769,28 @@ static int run_scan_z(int z, const uint32_t* keys, const uint32_t* vals, uint32_
   return 1;
 }
 
-static int sort_pairs(Layout& L, uint32_t N, int end_bit, cudaStream_t st) {
+// Stable sort of the (cell, t|op|slot) pairs by cell. The pairs of row i sit
+// at [i n, (i + 1) n) and every cell of row i lies in [i R, (i + 1) R) (R
+// cells per row), so when R is a power of two each row sorts on its own over
+// log2(R) bits: for cfg 3 two 8-bit onesweep passes instead of three for the
+// 18-bit cells of all rows together.
+static int sort_pairs(Layout& L, uint32_t N, uint32_t rows, uint64_t row_cells, cudaStream_t st) {
   size_t bytes = L.cub_tmp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N, 0,
-                                                  std::max(end_bit, 1), st);
+  cudaError_t e = cudaSuccess;
+  const int row_bits = bits_for(row_cells);
+  const int all_bits = bits_for((uint64_t)rows * row_cells);
+  const bool per_row = rows > 1 && (row_cells & (row_cells - 1)) == 0 && (row_bits + 7) / 8 < (all_bits + 7) / 8;
+  if (per_row) {
+    const uint32_t n = N / rows;
+    for (uint32_t i = 0; i < rows && e == cudaSuccess; ++i) {
+      const size_t o = (size_t)i * n;
+      e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in + o, L.k_out + o, L.v_in + o, L.v_out + o, (int)n, 0,
+                                          std::max(row_bits, 1), st);
+    }
+  } else {
+    e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N, 0,
+                                        std::max(all_bits, 1), st);
+  }
   if (e != cudaSuccess) {
     set_error("radix sort: %s", cudaGetErrorString(e));
     return (int)e;
@@ -1935,7 +1953,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     const int kb = bits_for((uint64_t)z);
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, fat_seeds, (uint64_t)w, z, kb, L, 0);
     { note_launch(); hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     const size_t fat_bytes = (size_t)D * w * z * 4;
     cudaMemcpyAsync(L.fat_snap, fat, fat_bytes, cudaMemcpyDeviceToDevice, st);
     ScanOut so{L.fat_snap, fat, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
@@ -1946,7 +1964,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
   } else if (kind == 1) {  // ------------------------------------------ SF1
     HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
     cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
@@ -1954,7 +1972,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
@@ -1969,7 +1987,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     h.fold_w = (uint32_t)w;
     if (fold) { note_launch(); hash_emit_k<D, 3><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
     else { note_launch(); hash_emit_k<D, 0><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     const uint64_t cells = (uint64_t)D * w * z;
     uint32_t* fat_grp = fat;
     if (fold) {
@@ -1996,7 +2014,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     // the slim cells: a second, slim-sorted scan carries its counts
     HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * wp), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
     cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
@@ -2004,7 +2022,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     cudaMemcpyAsync(L.fat_snap, dsub, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sd{L.fat_snap, dsub, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<true, 3, true>(1, L.k_out, L.v_out, N, 0, L.tiles, sd, st)) return r;
@@ -2014,7 +2032,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
@@ -2022,7 +2040,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
   } else {  // ------------------------------------------------------- CM exact
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(h); }
-    if (int r = sort_pairs(L, N, bits_for((uint64_t)D * w), st)) return r;
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     cudaMemcpyAsync(L.fat_snap, slim, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut so{L.fat_snap, slim, nullptr, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<true, 0, false>(1, L.k_out, L.v_out, N, 0, L.tiles, so, st)) return r;
