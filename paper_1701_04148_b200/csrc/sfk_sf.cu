@@ -1072,10 +1072,51 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
       }
       const uint32_t off = k.e & 31u, avail = min(min(32u - off, k.rem), budget);
       const uint32_t bits = a.delbits[k.e >> 5] >> off;
+      if (a.b_opdata) {
+        // SF2: the word's 32 b_min values in one batch of 16-B loads (one
+        // memory latency per word instead of one per insert), then the ops
+        // with static register indices
+        uint32_t ob[32];
+        const uint4* src = reinterpret_cast<const uint4*>(a.opdata + (k.e & ~31u));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 v = __ldg(src + q);
+          ob[4 * q] = v.x; ob[4 * q + 1] = v.y; ob[4 * q + 2] = v.z; ob[4 * q + 3] = v.w;
+        }
+        const uint32_t wb = bits << off;  // delete bits at their word positions
+#pragma unroll
+        for (uint32_t jj = 0; jj < 32u; ++jj) {
+          if (jj < off || jj >= off + avail) continue;
+          if (!((wb >> jj) & 1u)) {
+            k.x += 1u;
+            if (k.m < ob[jj]) {
+#pragma unroll
+              for (int i = 0; i < D; ++i)
+                if (c[i] == k.m) c[i] += 1u, raised[i] += 1u;
+              k.m += 1u;
+            }
+          } else {
+            k.x -= 1u;
+            uint32_t m = U32MAX;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const int64_t T = (int64_t)A[i] + (int64_t)(int32_t)k.x + (int64_t)O[i];
+              if ((int64_t)c[i] > T) c[i] -= 1u;
+              m = min(m, c[i]);
+            }
+            k.m = m;
+          }
+        }
+        k.e += avail;
+        k.rem -= avail;
+        budget -= avail;
+        ws[2] += 1;
+        continue;
+      }
       for (uint32_t j = 0; j < avail; ++j) {
         if (!((bits >> j) & 1u)) {  // insert
           k.x += 1u;
-          const uint32_t b = a.b_opdata ? a.opdata[k.e + j] : k.A0 + k.x;
+          const uint32_t b = k.A0 + k.x;
           if (k.m < b) {
 #pragma unroll
             for (int i = 0; i < D; ++i)
