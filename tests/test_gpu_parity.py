@@ -202,3 +202,28 @@ def test_sum_trigger_prefix_semantics(oracle, variant):
     ops[150_000] = 1
     wp = 4096 if variant in ("sf2", "sf3") else None
     compare_cfg(oracle, variant, 4, 1024, 4, wp, 9, ops, keys, keys.astype(np.uint64), c["distinct"])
+
+
+@pytest.mark.parametrize("variant", ["sf2", "sf3", "sf4", "sff"])
+@pytest.mark.parametrize("d,w,z", [(1, 97, 2), (2, 64, 1), (3, 50, 8), (8, 33, 3), (4, 1000, 5)])
+def test_deleting_variants_shapes(oracle, variant, d, w, z):
+    """Every deleting variant on the parallel engine across d, odd widths and
+    slot counts (z up to 8), against the oracle and the sequential engine."""
+    rng = np.random.default_rng(d * 131 + w * 7 + z)
+    distinct = rng.integers(0, 1 << 32, size=300, dtype=np.uint64).astype(np.uint32)
+    ops, keys, counts = [], [], {}
+    for _ in range(40_000):
+        k = int(distinct[min(int(rng.zipf(1.3)) - 1, distinct.size - 1)])
+        if counts.get(k, 0) and rng.random() < 0.35:
+            ops.append(1); counts[k] -= 1
+        else:
+            ops.append(0); counts[k] = counts.get(k, 0) + 1
+        keys.append(k)
+    ops, keys = np.array(ops, np.uint8), np.array(keys, np.uint32)
+    wp = z * w if variant in ("sf2", "sf3") else None
+    o, st = oracle_run(oracle, variant, d, w, z, wp, d + z, ops, keys.astype(np.uint64))
+    for sequential in (False, True):
+        sk = make_sketch(variant, d, w, z, wp, d + z)
+        status, idx = apply_batches(sk, ops, keys, batches=3, sequential=sequential)
+        assert (status, idx) == st[:2]
+        assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat, o.dsub)
