@@ -387,6 +387,180 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
   if (HAS_FAT && local_fail != NONE32) atomicMin(&o.ctl->fail_t, local_fail);
 }
 
+
+// ---------------------------------------------------------------- SF1: ignorable (op, row) pairs
+// An SF1 slim cell never drops below the batch net count of any key that maps
+// to it: inserts only raise cells, and a key's own inserts keep the min of its
+// d cells at or above its count (b_min >= its count, and each insert raises a
+// min below b_min by one). So when an earlier op of the batch on the same cell
+// belongs to a key whose count then was >= this op's b_min, the cell is >=
+// b_min at this op's turn: it is neither a min below b_min nor raised, and the
+// op's outcome does not depend on it. Such (op, row) pairs leave the cell's
+// sequence: the engine neither waits for nor publishes them. Row 0 is never
+// dropped, so runs stay contiguous in row-0 order.
+
+// per-op count of its key among the batch's ops up to and including it
+__global__ void iota_k(uint32_t* __restrict__ t, uint32_t n) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) t[j] = j;
+}
+__global__ void key_heads_k(const uint64_t* __restrict__ ks, uint32_t n, uint32_t* __restrict__ headpos) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    headpos[j] = (j == 0 || ks[j] != ks[j - 1]) ? j : 0u;
+}
+// packed per op: {key count << 32 | b_min}, one 8-B gather for the ignore scan
+__global__ void key_count_k(const uint32_t* __restrict__ headpos, const uint32_t* __restrict__ ts, uint32_t n,
+                            const uint32_t* __restrict__ bmin, unsigned long long* __restrict__ cb) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t t = ts[j];
+    cb[t] = ((unsigned long long)(j - headpos[j] + 1u) << 32) | bmin[t];
+  }
+}
+
+struct SegMax {
+  uint32_t flag, v;
+};
+struct SegMaxOp {
+  __device__ __forceinline__ SegMax operator()(const SegMax& a, const SegMax& b) const {
+    return SegMax{a.flag | b.flag, b.flag ? b.v : max(a.v, b.v)};
+  }
+};
+
+// ignore flags in sorted (cell) order: within a 2048-element tile, the
+// segmented prefix max of the key counts of earlier ops on the cell (a valid
+// lower bound of the cell; earlier tiles are simply not consulted)
+__global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __restrict__ keys,
+                                                            const uint32_t* __restrict__ vals, uint32_t N,
+                                                            uint32_t row_cells,
+                                                            const unsigned long long* __restrict__ cb,
+                                                            const Ctl* __restrict__ ctl, uint8_t* __restrict__ ign) {
+  typedef cub::BlockScan<SegMax, SCAN_THREADS> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const uint32_t tstar = ctl->fail_t;
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  SegMax agg{0u, 0u};
+  SegMaxOp op;
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e < N) {
+      const uint32_t t = vals[e] >> 1;
+      const SegMax el{(e == 0 || keys[e - 1] != keys[e]) ? 1u : 0u, (uint32_t)(cb[t] >> 32)};
+      agg = q == 0 ? el : op(agg, el);
+    }
+  }
+  SegMax run;
+  BS(tmp).ExclusiveScan(agg, run, SegMax{0u, 0u}, op);
+  if (threadIdx.x == 0) run = SegMax{0u, 0u};
+#pragma unroll 1
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e >= N) break;
+    const uint32_t c = keys[e], t = vals[e] >> 1;
+    const bool head = e == 0 || keys[e - 1] != c;
+    const uint32_t lb = head ? 0u : run.v;
+    const unsigned long long kb = cb[t];
+    ign[e] = (c >= row_cells && t < tstar && lb >= (uint32_t)kb) ? 1u : 0u;
+    run = op(run, SegMax{head ? 1u : 0u, (uint32_t)(kb >> 32)});
+  }
+}
+
+// filtered links: for every element, the number of non-ignored elements
+// before it in its cell (its rank in the cell's filtered sequence) and the
+// last non-ignored op before it; a segmented scan (reduce / tile carry /
+// apply) like segscan, over {segment-head flag, count, last op}
+struct SegCnt {
+  uint32_t flag, cnt, last;
+};
+struct SegCntOp {
+  __device__ __forceinline__ SegCnt operator()(const SegCnt& a, const SegCnt& b) const {
+    if (b.flag) return b;
+    return SegCnt{a.flag, a.cnt + b.cnt, b.last != NONE32 ? b.last : a.last};
+  }
+};
+__device__ __forceinline__ SegCnt segcnt_elem(const uint32_t* keys, const uint32_t* vals, const uint8_t* ign,
+                                              uint32_t e) {
+  const bool keep = !ign[e];
+  return SegCnt{(e == 0 || keys[e - 1] != keys[e]) ? 1u : 0u, keep ? 1u : 0u, keep ? (vals[e] >> 1) : NONE32};
+}
+__global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __restrict__ keys,
+                                                             const uint32_t* __restrict__ vals,
+                                                             const uint8_t* __restrict__ ign, uint32_t N,
+                                                             SegCnt* __restrict__ tile_agg) {
+  typedef cub::BlockScan<SegCnt, SCAN_THREADS> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  SegCntOp op;
+  SegCnt agg{0u, 0u, NONE32};
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e < N) agg = op(agg, segcnt_elem(keys, vals, ign, e));
+  }
+  // ordered (non-commutative): the block's inclusive scan, last thread's value
+  SegCnt inc, tot;
+  BS(tmp).InclusiveScan(agg, inc, op, tot);
+  if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) filt_tiles_k(SegCnt* __restrict__ tile_agg, uint32_t ntiles) {
+  // one block: exclusive scan of the tile aggregates in place
+  typedef cub::BlockScan<SegCnt, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ SegCnt carry;
+  SegCntOp op;
+  if (threadIdx.x == 0) carry = SegCnt{0u, 0u, NONE32};
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
+    const uint32_t k = b0 + threadIdx.x;
+    const SegCnt v = k < ntiles ? tile_agg[k] : SegCnt{0u, 0u, NONE32};
+    SegCnt ex, total;
+    BS(tmp).ExclusiveScan(v, ex, SegCnt{0u, 0u, NONE32}, op, total);
+    const SegCnt c0 = carry;
+    __syncthreads();
+    if (k < ntiles) tile_agg[k] = op(c0, ex);
+    if (threadIdx.x == 0) carry = op(c0, total);
+    __syncthreads();
+  }
+}
+// rewrites each element's 32-B link record: filtered rank and predecessor for
+// kept pairs; ignored pairs get prev = IGN_MARK (never a run continuation)
+constexpr uint32_t IGN_MARK = 0xFFFFFFFEu;
+__global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __restrict__ keys,
+                                                            const uint32_t* __restrict__ vals,
+                                                            const uint8_t* __restrict__ ign, uint32_t N, uint32_t D,
+                                                            uint32_t row_cells, const SegCnt* __restrict__ carry,
+                                                            uint4* __restrict__ links) {
+  typedef cub::BlockScan<SegCnt, SCAN_THREADS> BS;
+  __shared__ typename BS::TempStorage tmp;
+  SegCntOp op;
+  const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  SegCnt agg{0u, 0u, NONE32};
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e < N) agg = op(agg, segcnt_elem(keys, vals, ign, e));
+  }
+  SegCnt run;
+  BS(tmp).ExclusiveScan(agg, run, SegCnt{0u, 0u, NONE32}, op);
+  if (threadIdx.x == 0) run = SegCnt{0u, 0u, NONE32};
+  run = op(carry[blockIdx.x], run);
+#pragma unroll 1
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    if (e >= N) break;
+    const uint32_t c = keys[e], t = vals[e] >> 1, row = c / row_cells;
+    const SegCnt el = segcnt_elem(keys, vals, ign, e);
+    const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
+    uint4* rec = links + ((size_t)t * D + row) * 2;
+    if (ign[e]) {
+      rec[0] = make_uint4(0u, IGN_MARK, 0u, 0u);
+    } else {
+      rec[0] = make_uint4(before.cnt, before.last, 0u, 0u);
+    }
+    rec[1] = make_uint4(c, e, 0u, 0u);
+    run = op(run, el);
+  }
+}
+
 // ---------------------------------------------------------------- 4. runs
 template <int D>
 struct RunArgs {
@@ -400,6 +574,7 @@ struct RunArgs {
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
   uint32_t* headflag;      // [t] (written by runs_head_k)
+  int has_ign;             // SF1 ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
   uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
@@ -414,12 +589,22 @@ __global__ void __launch_bounds__(256) runs_head_k(RunArgs<D> a) {
   const uint32_t tstar = a.ctl->fail_t;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
     const bool valid = t < tstar;
-    uint32_t prev[D];
+    uint32_t prev[D], mask = 0;
 #pragma unroll
-    for (int i = 0; i < D; ++i) prev[i] = a.links[((size_t)t * D + i) * 4].y;
+    for (int i = 0; i < D; ++i) {
+      prev[i] = a.links[((size_t)t * D + i) * 4].y;
+      if (prev[i] == IGN_MARK) mask |= 1u << i;  // (SF1) a dropped pair: not in the cell's sequence
+    }
     bool cont = valid && prev[0] != NONE32;
 #pragma unroll
-    for (int i = 1; i < D; ++i) cont = cont && (prev[i] == prev[0]);
+    for (int i = 1; i < D; ++i) cont = cont && ((mask >> i) & 1u || prev[i] == prev[0]);
+    if (cont && a.has_ign) {  // the run's ops must drop the same rows
+      uint32_t pm = 0;
+#pragma unroll
+      for (int i = 1; i < D; ++i)
+        if (a.links[((size_t)prev[0] * D + i) * 4].y == IGN_MARK) pm |= 1u << i;
+      cont = pm == mask;
+    }
     if (cont) cont = load_key(a.keys, prev[0]) == load_key(a.keys, t);
     a.headflag[t] = (valid && !cont) ? 1u : 0u;
   }
@@ -511,6 +696,11 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     rec.e0 = e0;
     rec.info = L | (hasdel << 31);
     rec.bits0 = 0;
+    if (!a.delbits) {  // SF1 / CU: the rows this run's ops drop (IGN_MARK links)
+#pragma unroll
+      for (int i = 1; i < D; ++i)
+        if (a.links[((size_t)t * D + i) * a.lstride].y == IGN_MARK) rec.bits0 |= 1u << i;
+    }
     if (a.delbits && hasdel) {
       const uint32_t sh = e0 & 31u;
       uint32_t b = a.delbits[e0 >> 5] >> sh;
@@ -1407,6 +1597,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
             if (MODE >= 2) A[i] = rec.A[i], O[i] = rec.O[i];
           }
           pend = (1u << D) - 1u;
+          if (MODE <= 1) pend &= ~bits0;  // SF1: rows this run drops (never row 0)
           has = true;
         } else {
           exhausted = true;
@@ -1428,6 +1619,11 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
         }
       if (!pend) {  // all cells acquired: start the replay
         if (a.trace) a.trace[3ull * rid + 1] = gtimer();
+        if (MODE <= 1) {
+#pragma unroll
+          for (int i = 1; i < D; ++i)
+            if ((bits0 >> i) & 1u) c[i] = U32MAX;  // a dropped row: neither the min nor raised
+        }
         k.m = c[0];
 #pragma unroll
         for (int i = 1; i < D; ++i) k.m = min(k.m, c[i]);
@@ -1448,7 +1644,8 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
         const uint32_t L = info & 0x7fffffffu;
 #pragma unroll
         for (int i = 0; i < D; ++i)
-          st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
+          if (MODE > 1 || !((bits0 >> i) & 1u))
+            st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
         has = false;
         ++st_runs;
         if (a.trace) a.trace[3ull * rid + 2] = gtimer();
@@ -1637,6 +1834,14 @@ static size_t scan_temp_bytes(uint32_t n) {
   return bytes;
 }
 
+static size_t key_sort_temp_bytes(uint32_t n) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)n, 0, 64);
+  cub::DeviceScan::InclusiveScan(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, cub::Max(), (int)n);
+  return std::max(a, b);
+}
+
 static int bits_for(uint64_t v) {  // bits needed to represent values < v
   int b = 0;
   while (b < 64 && (1ull << b) < v) ++b;
@@ -1665,7 +1870,10 @@ struct Layout {
   uint32_t* headflag;
   uint32_t *bnd, *bidx, *bpos, *isdel, *delpre;
   uint32_t* ridx;
-  uint32_t *run_e0, *run_info, *run_t;
+  uint64_t *k64a, *k64b;          // SF1 ignore pass: materialised keys, sorted
+  uint32_t *ta, *tb, *headpos;     //   op ids, sorted op ids, key segment heads
+  uint8_t* ign;                    //   dropped (op, row) flags in cell order
+  void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
   unsigned long long* slim64;
   Ctl* ctl;
@@ -1687,6 +1895,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.k_out = cv.take<uint32_t>(N);
   L.v_out = cv.take<uint32_t>(N);
   L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n + 1));
+  if (kind == 1) L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, key_sort_temp_bytes((uint32_t)n));
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
@@ -1723,9 +1932,16 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.isdel = cv.take<uint32_t>(engine ? n + 1 : 1);
   L.delpre = cv.take<uint32_t>(engine ? n + 1 : 1);
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
-  L.run_e0 = cv.take<uint32_t>(engine ? n : 1);
-  L.run_info = cv.take<uint32_t>(engine ? n : 1);
-  L.run_t = cv.take<uint32_t>(engine ? n : 1);
+  {
+    const bool sf1 = kind == 1;
+    L.k64a = cv.take<uint64_t>(sf1 ? n : 1);
+    L.k64b = cv.take<uint64_t>(sf1 ? n : 1);
+    L.ta = cv.take<uint32_t>(sf1 ? n : 1);
+    L.tb = cv.take<uint32_t>(sf1 ? n : 1);
+    L.headpos = cv.take<uint32_t>(sf1 ? n : 1);
+    L.ign = cv.take<uint8_t>(sf1 ? N : 1);
+    L.ftiles = cv.take<char>(sf1 ? ((N + SCAN_TILE - 1) / SCAN_TILE + 1) * 16 : 1);
+  }
   L.recs = cv.take<char>(engine ? (uint64_t)n * (12 + 16 * (uint64_t)d) : 1);
   L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
   L.total = cv.off + 256;
@@ -1866,7 +2082,7 @@ static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uin
 // pairs (k_out/v_out), the links and the observations exist.
 template <int D, int MODE>
 static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int64_t w, KeySrc ks, uint32_t n, int kb,
-                      int64_t* inc, cudaStream_t st, bool b_opdata = false) {
+                      int64_t* inc, cudaStream_t st, bool b_opdata = false, bool has_ign = false) {
   const int sms = sm_count();
   RunArgs<D> ra;
   ra.vals0 = L.v_out;
@@ -1882,6 +2098,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.delbits = MODE >= 2 ? L.delbits : nullptr;
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
+  ra.has_ign = has_ign ? 1 : 0;
   ra.ctl = L.ctl;
   { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
@@ -1982,6 +2199,33 @@ __global__ void fold_scatter_k(const uint32_t* __restrict__ grp, uint32_t* __res
   }
 }
 
+
+int launch_load_keys(KeySrc ks, int64_t n, uint64_t* out, cudaStream_t st);  // sfk_query.cu
+
+// SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
+static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st) {
+  const int sms = sm_count();
+  if (int r = launch_load_keys(ks, n, L.k64a, st)) return r;
+  { note_launch(); iota_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.ta, n); }
+  size_t bytes = L.cub_tmp_bytes;
+  const int kbits = ks.kind == SFK_KEY_U32 ? 32 : 64;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k64a, L.k64b, L.ta, L.tb, (int)n, 0, kbits, st);
+  if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
+  { note_launch(); key_heads_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, n, L.headpos); }
+  bytes = L.cub_tmp_bytes;
+  e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
+  if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
+  unsigned long long* cb = reinterpret_cast<unsigned long long*>(L.k64a);  // free after the key sort
+  { note_launch(); key_count_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.headpos, L.tb, n, L.obs, cb); }
+  const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign); }
+  SegCnt* ft = static_cast<SegCnt*>(L.ftiles);
+  { note_launch(); filt_reduce_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, ft); }
+  { note_launch(); filt_tiles_k<<<1, 1024, 0, st>>>(ft, ntiles); }
+  { note_launch(); filt_apply_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, ft, reinterpret_cast<uint4*>(L.links)); }
+  return check_launch("sf1_ignore");
+}
+
 template <int D>
 static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
                          const uint64_t* fat_seeds, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
@@ -2014,9 +2258,14 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
-    ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
-    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
+    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob
+    if (ign) {  // the filtered scan writes every link record itself
+      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st)) return r;
+    } else {
+      ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+      if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    }
+    if (int r = run_engine<D, 0>(L, slim, slim_seeds, w, ks, n, 0, inc, st, false, ign)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else if (kind == 4 || kind == 5) {  // -------------------------- SF4 / SF3
     // SF4: buckets by the slim seeds, slots by the extended seeds (as SFF).

@@ -227,3 +227,25 @@ def test_deleting_variants_shapes(oracle, variant, d, w, z):
         status, idx = apply_batches(sk, ops, keys, batches=3, sequential=sequential)
         assert (status, idx) == st[:2]
         assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat, o.dsub)
+
+
+@pytest.mark.parametrize("d,w,wp,batches", [(4, 64, 256, 1), (4, 128, 4096, 3), (2, 32, 64, 2), (8, 200, 1000, 1),
+                                            (4, 12800, 4194304, 1)])
+def test_sf1_dropped_pairs(oracle, d, w, wp, batches):
+    """SF1 drops (op, row >= 1) pairs whose cell provably exceeds the op's
+    b_min (a hot key's count on the cell). Hot keys mixed with many cold keys
+    on narrow rows make such pairs common; state must stay bit-exact, across
+    batches, against the oracle and the sequential engine."""
+    rng = np.random.default_rng(d * 7 + w + batches)
+    hot = rng.integers(0, 1 << 32, size=5, dtype=np.uint64).astype(np.uint32)
+    cold = rng.integers(0, 1 << 32, size=20000, dtype=np.uint64).astype(np.uint32)
+    n = 200_000
+    pick_hot = rng.random(n) < 0.5
+    keys = np.where(pick_hot, hot[rng.integers(0, hot.size, n)], cold[rng.integers(0, cold.size, n)]).astype(np.uint32)
+    ops = np.zeros(n, np.uint8)
+    o, st = oracle_run(oracle, "sf1", d, w, 1, wp, 3, ops, keys.astype(np.uint64))
+    for sequential in (False, True):
+        sk = make_sketch("sf1", d, w, 1, wp, 3)
+        status, idx = apply_batches(sk, ops, keys, batches=batches, sequential=sequential)
+        assert (status, idx) == st[:2]
+        assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)

@@ -1,4 +1,7 @@
-# build timing check (diagnostics)
-for a in 1.0; do timeout 300 python tools/one_build.py sff $a 3 2>&1 | grep "rep 2"; done
-timeout 300 python tools/one_build.py cu 1.0 3 2>&1 | grep "rep 2"
-timeout 300 python tools/one_build.py sf1 1.0 3 2>&1 | grep "rep 2"
+# SF1 timing with / without the ignore pass (diagnostics)
+for m in 0 1; do
+  if [ $m = 1 ]; then export SFK_NO_SF1_IGNORE=1; else unset SFK_NO_SF1_IGNORE; fi
+  echo "no_ignore=$m"
+  timeout 300 python tools/one_build.py sf1 1.0 3 2>&1 | grep "rep 2"
+  timeout 600 python tools/one_build.py sf1rec 1.2 2 2>&1 | grep "rep 1"
+done
