@@ -437,30 +437,38 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   __shared__ typename BS::TempStorage tmp;
   const uint32_t tstar = ctl->fail_t;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  // this thread's elements, loaded once: cell, head flag, op, {count, b_min}
+  uint32_t cc[SCAN_ITEMS], tt[SCAN_ITEMS];
+  unsigned long long kb[SCAN_ITEMS];
+  bool hd[SCAN_ITEMS];
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const uint32_t e = base + q;
+    cc[q] = e < N ? keys[e] : U32MAX;
+    tt[q] = e < N ? vals[e] >> 1 : 0u;
+    hd[q] = e < N && (e == 0 || (q ? cc[q - 1] : keys[e - 1]) != cc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? cb[tt[q]] : 0ull;
   SegMax agg{0u, 0u};
   SegMaxOp op;
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const uint32_t e = base + q;
-    if (e < N) {
-      const uint32_t t = vals[e] >> 1;
-      const SegMax el{(e == 0 || keys[e - 1] != keys[e]) ? 1u : 0u, (uint32_t)(cb[t] >> 32)};
+    if (base + q < N) {
+      const SegMax el{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)};
       agg = q == 0 ? el : op(agg, el);
     }
   }
   SegMax run;
   BS(tmp).ExclusiveScan(agg, run, SegMax{0u, 0u}, op);
   if (threadIdx.x == 0) run = SegMax{0u, 0u};
-#pragma unroll 1
+#pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t e = base + q;
     if (e >= N) break;
-    const uint32_t c = keys[e], t = vals[e] >> 1;
-    const bool head = e == 0 || keys[e - 1] != c;
-    const uint32_t lb = head ? 0u : run.v;
-    const unsigned long long kb = cb[t];
-    ign[e] = (c >= row_cells && t < tstar && lb >= (uint32_t)kb) ? 1u : 0u;
-    run = op(run, SegMax{head ? 1u : 0u, (uint32_t)(kb >> 32)});
+    const uint32_t lb = hd[q] ? 0u : run.v;
+    ign[e] = (cc[q] >= row_cells && tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
+    run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
   }
 }
 
