@@ -60,6 +60,12 @@ def lib():
         L.orc_sf_bucket_apply.restype = _I
         L.orc_oracle_slim_apply.argtypes = [_P, _P, _I, _I64, _P, _P, _I64, _P, _P, _P]
         L.orc_oracle_slim_apply.restype = _I
+        L.orc_count_apply.argtypes = [_P, _P, _I, _I64, _P, _P, _I64, _P, _P]
+        L.orc_count_apply.restype = _I
+        L.orc_count_query.argtypes = [_P, _P, _I, _I64, _P, _I64, _P]
+        L.orc_cml_apply.argtypes = [_P, _P, _I, _I64, _P, _P, _I64, ctypes.c_double, ctypes.c_uint64, _I64, _P, _P]
+        L.orc_cml_apply.restype = _I
+        L.orc_cml_min_exp.argtypes = [_P, _P, _I, _I64, _P, _I64, _P]
         _lib = L
     return _lib
 
@@ -198,6 +204,53 @@ def oracle_slim_apply(slim, seeds, keys, true_counts, inc_counts):
     st = lib().orc_oracle_slim_apply(_ptr(slim), _ptr(seeds), d, w, _ptr(keys), _ptr(true_counts),
                                      keys.shape[0], _ptr(inc_counts), ctypes.byref(oi), ctypes.byref(ni))
     return _apply_tail(st, oi, ni)
+
+
+def count_apply(counters, seeds, ops, keys):
+    """_kernels.py:118-146 (mutates the int32 counters)."""
+    ops, keys, seeds = _u8(ops), _u64(keys), _u64(seeds)
+    d, w = counters.shape
+    oi, ni = _I64(), _I64()
+    st = lib().orc_count_apply(_ptr(counters), _ptr(seeds), d, w, _ptr(ops), _ptr(keys), ops.shape[0],
+                               ctypes.byref(oi), ctypes.byref(ni))
+    return _apply_tail(st, oi, ni)
+
+
+def count_query(counters, seeds, keys) -> np.ndarray:
+    """_kernels.py:149-179."""
+    keys, seeds = _u64(keys), _u64(seeds)
+    d, w = counters.shape
+    out = np.empty(keys.shape[0], dtype=np.int64)
+    lib().orc_count_query(_ptr(counters), _ptr(seeds), d, w, _ptr(keys), keys.shape[0], _ptr(out))
+    return out
+
+
+def cml_apply(exps, seeds, ops, keys, base, rng_seed, start_pos):
+    """_kernels.py:182-211 (mutates the uint16 exponents)."""
+    ops, keys, seeds = _u8(ops), _u64(keys), _u64(seeds)
+    d, w = exps.shape
+    oi, ni = _I64(), _I64()
+    st = lib().orc_cml_apply(_ptr(exps), _ptr(seeds), d, w, _ptr(ops), _ptr(keys), ops.shape[0], float(base),
+                             int(rng_seed) & 0xFFFFFFFFFFFFFFFF, int(start_pos), ctypes.byref(oi), ctypes.byref(ni))
+    return _apply_tail(st, oi, ni)
+
+
+def cml_min_exp(exps, seeds, keys) -> np.ndarray:
+    """_kernels.py:214-226."""
+    keys, seeds = _u64(keys), _u64(seeds)
+    d, w = exps.shape
+    out = np.empty(keys.shape[0], dtype=np.int64)
+    lib().orc_cml_min_exp(_ptr(exps), _ptr(seeds), d, w, _ptr(keys), keys.shape[0], _ptr(out))
+    return out
+
+
+def cml_value(exponent, base: float) -> np.ndarray:
+    """baselines.py:174-179: round((base**c - 1) / (base - 1)), ties away from zero."""
+    import math
+
+    c = np.asarray(exponent, dtype=np.float64)
+    vals = np.expm1(c * math.log(base)) / (base - 1.0)
+    return np.floor(vals + 0.5).astype(np.int64)
 
 
 class OracleSketch:

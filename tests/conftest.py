@@ -36,3 +36,15 @@ def oracle():
 
     orc.lib()
     return orc
+
+
+BASELINES = os.path.join(GOLDEN, "baselines")
+
+
+def baseline_fixture_names(prefix=""):
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(BASELINES, prefix + "*.npz")))
+
+
+def load_baseline_fixture(name):
+    with np.load(os.path.join(BASELINES, name + ".npz"), allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}

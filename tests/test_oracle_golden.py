@@ -87,3 +87,62 @@ def test_oracle_u32_keys_zero_extend(oracle):
     sk, _, _ = replay_oracle(oracle, fx)
     q32 = fx["query_keys"].astype(np.uint32)
     np.testing.assert_array_equal(sk.query_many(q32, threads=2), fx["query"])
+
+
+# ---------------------------------------------------------------- Count / CML / oracle-assisted
+from conftest import baseline_fixture_names, load_baseline_fixture  # noqa: E402
+
+
+def _splits(n, batches):
+    b = np.linspace(0, n, batches + 1).astype(int)
+    return list(zip(b[:-1], b[1:]))
+
+
+@pytest.mark.parametrize("name", baseline_fixture_names())
+def test_oracle_matches_reference_baseline_fixture(oracle, name):
+    """Count (_kernels.py:118-179), CML (_kernels.py:182-226, baselines.py:174-179)
+    and the oracle-assisted slim (_kernels.py:387-411) against the reference's
+    own outputs (tests/golden/make_golden_baselines.py)."""
+    fx = load_baseline_fixture(name)
+    kind, d, w = str(fx["kind"]), int(fx["d"]), int(fx["w"])
+    seeds = oracle.seed_array(int(fx["master_seed"]), 0, d)
+    keys = fx["keys"].astype(np.uint64)
+    qk = fx["query_keys"].astype(np.uint64)
+    status, idx, seen = 0, -1, 0
+    if kind == "count":
+        c = fx["pre_counters"].copy()
+        for a, b in _splits(len(keys), int(fx["batches"])):
+            st, oi, ni = oracle.count_apply(c, seeds, fx["ops"][a:b], keys[a:b])
+            seen += ni
+            if st:
+                status, idx = st, a + oi
+                break
+        np.testing.assert_array_equal(c, fx["counters"])
+        np.testing.assert_array_equal(oracle.count_query(c, seeds, qk), fx["query"])
+        np.testing.assert_array_equal(oracle.count_query(c, seeds, qk), fx["collector_query"])
+    elif kind == "cml":
+        e = fx["pre_exponents"].copy()
+        base, rs = float(fx["base"]), int(fx["rng_seed"])
+        for a, b in _splits(len(keys), int(fx["batches"])):
+            st, oi, ni = oracle.cml_apply(e, seeds, fx["ops"][a:b], keys[a:b], base, rs, seen)
+            seen += ni
+            if st:
+                status, idx = st, a + oi
+                break
+        np.testing.assert_array_equal(e, fx["exponents"])
+        with np.errstate(over="ignore", invalid="ignore"):
+            np.testing.assert_array_equal(oracle.cml_value(oracle.cml_min_exp(e, seeds, qk), base), fx["query"])
+    else:
+        slim = fx["pre_slim"].copy()
+        inc = np.zeros(d, np.int64)
+        for a, b in _splits(len(keys), int(fx["batches"])):
+            st, oi, ni = oracle.oracle_slim_apply(slim, seeds, keys[a:b], fx["true_counts"][a:b], inc)
+            seen += ni
+            if st:
+                status, idx = st, a + oi
+                break
+        np.testing.assert_array_equal(slim, fx["slim"])
+        np.testing.assert_array_equal(inc, fx["inc"])
+        np.testing.assert_array_equal(oracle.min_query(slim, seeds, qk), fx["query"])
+    assert (status, idx) == (int(fx["status"]), int(fx["op_index"]))
+    assert seen == int(fx["seen"])
