@@ -161,10 +161,52 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub,
                  size_t workspace_bytes, int flags, void* stream);
 
 /* Replaces _kernels.oracle_slim_apply (_kernels.py:387-411), called from
- * SfSketch.oracle_assisted_apply (sf.py:199-229). */
+ * SfSketch.oracle_assisted_apply (sf.py:199-229). true_counts: int64[n] on
+ * the device. The ordered engine replays the batch (gate: m <
+ * np.uint64(true count)); a batch holding a count that is negative or above
+ * 2^32 - 1 while a slim cell could reach 2^32 - 1 (checked on the device)
+ * runs in the exact sequential engine. */
+size_t sfk_oracle_workspace_size(int d, int64_t w, int64_t n);
 int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t w, const void* keys,
                           int key_kind, int rec_len, const int64_t* true_counts, int64_t n,
-                          int64_t* inc_counts, int64_t* result, void* stream);
+                          int64_t* inc_counts, int64_t* result, void* workspace, size_t workspace_bytes,
+                          int flags, void* stream);
+
+/* Replaces _kernels.count_apply (_kernels.py:118-146), called from
+ * CountSketch.apply_ops (baselines.py:115-119). counters: int32 (d, w).
+ * result = {status, op_index, n_ins} (no tallies: the reference keeps none).
+ * Batches that cannot reach +-2^31 (checked on the device) are one pass of
+ * warp-aggregated atomics; the others run in the exact sequential engine. */
+size_t sfk_count_workspace_size(int d, int64_t w, int64_t n);
+int sfk_count_apply(int32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops,
+                    const void* keys, int key_kind, int rec_len, int64_t n, int64_t* result,
+                    void* workspace, size_t workspace_bytes, int flags, void* stream);
+/* Replaces _kernels.count_query (_kernels.py:149-179): median of the d
+ * sign-corrected reads (even d: mean of the central pair, half away from
+ * zero), clamped at 0, as int64. */
+int sfk_count_query(const int32_t* counters, const uint64_t* seeds, int d, int64_t w, const void* keys,
+                    int key_kind, int rec_len, int64_t n, int64_t* out, void* stream);
+
+/* Replaces _kernels.cml_apply (_kernels.py:182-211), called from
+ * CmlSketch.apply_ops (baselines.py:219-231). exps: uint16 (d, w).
+ * gate: device float64[65536], gate[c] = base ** -c as the host's libm pow
+ * computes it (numba's float ** lowers to the same call). start_pos = the
+ * sketch's insertions_seen before the batch (the coin-flip stream index).
+ * Runs in the ordered engine when the gate is non-increasing and the 0xFFFF
+ * exponent cannot be raised within the batch (gate[65535] == 0, or the
+ * largest exponent + n < 0xFFFF; checked on the device), else in the exact
+ * sequential engine. */
+size_t sfk_cml_workspace_size(int d, int64_t w, int64_t n);
+int sfk_cml_apply(uint16_t* exps, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops,
+                  const void* keys, int key_kind, int rec_len, int64_t n, const double* gate,
+                  uint64_t rng_seed, int64_t start_pos, int64_t* result, void* workspace,
+                  size_t workspace_bytes, int flags, void* stream);
+/* Replaces _kernels.cml_min_exp (_kernels.py:214-226) and, when value_table
+ * (device int64[65536], the reference's cml_value of every exponent) is
+ * given, the decode of CmlSketch.query_many (baselines.py:236-238). */
+int sfk_cml_query(const uint16_t* exps, const uint64_t* seeds, int d, int64_t w, const void* keys,
+                  int key_kind, int rec_len, int64_t n, const int64_t* value_table, int64_t* out,
+                  void* stream);
 
 
 #ifdef __cplusplus

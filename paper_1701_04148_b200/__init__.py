@@ -2,14 +2,15 @@
 reference ``sfsketch`` package's sketch API.
 
 The public surface mirrors ``sfsketch/__init__.py``: ``SketchParams``,
-``SfSketch`` (sf1/sf2/sf3/sf4/sff), ``CmSketch``, ``CuSketch``,
+``SfSketch`` (sf1/sf2/sf3/sf4/sff), ``CmSketch``, ``CuSketch``, ``CountSketch``,
+``CmlSketch``,
 ``export_slim`` / ``import_slim`` / ``CollectorSketch``, the hash family and
 the exception taxonomy. State lives in CUDA tensors; every update and query
 runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI of
 ``include/sfsketch_cuda.h``. There is no CPU fallback.
 """
 
-from .baselines import CmSketch, CuSketch
+from .baselines import CmlSketch, CmSketch, CountSketch, CuSketch, cml_value
 from .errors import (
     ConfigurationError,
     ExportFormatError,
@@ -30,6 +31,9 @@ __version__ = "0.1.0"
 __all__ = [
     "CmSketch",
     "CuSketch",
+    "CountSketch",
+    "CmlSketch",
+    "cml_value",
     "SfSketch",
     "Variant",
     "SketchParams",

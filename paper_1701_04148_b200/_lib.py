@@ -34,7 +34,14 @@ EXPORTS = (
     "sfk_cu_apply",
     "sfk_sf_workspace_size",
     "sfk_sf_apply",
+    "sfk_oracle_workspace_size",
     "sfk_oracle_slim_apply",
+    "sfk_count_workspace_size",
+    "sfk_count_apply",
+    "sfk_count_query",
+    "sfk_cml_workspace_size",
+    "sfk_cml_apply",
+    "sfk_cml_query",
     "sfk_launch_count",
     "sfk_gen_query_keys",
     "sfk_engine_stats",
@@ -82,7 +89,17 @@ def load_library() -> ctypes.CDLL:
     L.sfk_sf_workspace_size.argtypes = [I, I, I64, I64, I, I64]
     L.sfk_sf_workspace_size.restype = SZ
     L.sfk_sf_apply.argtypes = [I, P, P, P, P, P, I, I64, I64, I, P, P, I, I, I64, P, P, P, SZ, I, P]
-    L.sfk_oracle_slim_apply.argtypes = [P, P, I, I64, P, I, I, P, I64, P, P, P]
+    L.sfk_oracle_workspace_size.argtypes = [I, I64, I64]
+    L.sfk_oracle_workspace_size.restype = SZ
+    L.sfk_oracle_slim_apply.argtypes = [P, P, I, I64, P, I, I, P, I64, P, P, P, SZ, I, P]
+    L.sfk_count_workspace_size.argtypes = [I, I64, I64]
+    L.sfk_count_workspace_size.restype = SZ
+    L.sfk_count_apply.argtypes = [P, P, I, I64, P, P, I, I, I64, P, P, SZ, I, P]
+    L.sfk_count_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
+    L.sfk_cml_workspace_size.argtypes = [I, I64, I64]
+    L.sfk_cml_workspace_size.restype = SZ
+    L.sfk_cml_apply.argtypes = [P, P, I, I64, P, P, I, I, I64, P, ctypes.c_uint64, I64, P, P, SZ, I, P]
+    L.sfk_cml_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P, P]
     L.sfk_launch_count.restype = ctypes.c_ulonglong
     L.sfk_engine_stats.argtypes = [P, I]
     L.sfk_engine_timing.argtypes = [I]

@@ -1,5 +1,6 @@
-"""Count-min and conservative-update baselines on the GPU (drop-in for the
-``CmSketch`` / ``CuSketch`` of ``sfsketch.baselines``, ``baselines.py:46-171``).
+"""The four baseline sketches on the GPU (drop-in for ``CmSketch``,
+``CountSketch``, ``CuSketch`` and ``CmlSketch`` of ``sfsketch.baselines``,
+``baselines.py:46-238``).
 
 * ``CmSketch.apply_ops``: when no op of the batch can fail (checked on the
   device from the counter extremes and the batch's insert/delete counts),
@@ -9,6 +10,13 @@
 * ``CuSketch.apply_ops``: the ordered dataflow engine with an unbounded cap
   (every insert raises its minimal counters), or the exact sequential device
   engine if the batch could reach a saturated minimum.
+* ``CountSketch``: signed +-1 per row; one pass of warp-aggregated atomics
+  when no counter can reach +-2^31 within the batch, else the sequential
+  engine. Query: the reference's signed median, in registers.
+* ``CmlSketch``: the ordered engine with each insert's coin flip turned into
+  a cap on the minimum exponent (``base ** -c`` tabulated on the host with
+  the same libm ``pow`` the reference's numba kernel calls). Query: the min
+  exponent decoded through a table of the reference's ``cml_value``.
 """
 
 from __future__ import annotations
@@ -18,7 +26,9 @@ import torch
 
 from . import _lib
 from ._ops import OP_DELETE, OP_INSERT, Scratch, device, normalize_stream, raise_for_status, single_op
-from .errors import UnsupportedOperationError
+import math
+
+from .errors import ConfigurationError, UnsupportedOperationError
 from .hashing import MASK64, seed_array
 from .params import SketchParams
 from .sf import query_min
@@ -100,3 +110,149 @@ class CuSketch(_CounterSketch):
 
     def delete(self, key: int) -> None:
         raise UnsupportedOperationError("conservative update cannot be reversed; deletion is unsupported")
+
+
+class CountSketch:
+    """Signed-median sketch: d arrays of w int32 counters (``baselines.py:90-128``).
+    Insert adds a per-row sign, delete subtracts it; query = median of the
+    sign-corrected reads (even d: mean of the central pair, half away from
+    zero), clamped at zero."""
+
+    kind = "c"
+    supports_deletion = True
+
+    def __init__(self, params: SketchParams):
+        self.params = params
+        self.counters = torch.zeros((params.d, params.w), dtype=torch.int32, device=device())
+        self._seeds = seed_array(params.master_seed, 0, params.d)
+        self.insertions_seen = 0
+        self._scratch = Scratch()
+
+    def insert(self, key: int) -> None:
+        self.apply_ops(*single_op(OP_INSERT, key))
+
+    def delete(self, key: int) -> None:
+        self.apply_ops(*single_op(OP_DELETE, key))
+
+    def apply_ops(self, ops, keys, *, sequential: bool = False) -> None:
+        ops_t, kb = normalize_stream(ops, keys)
+        L = _lib.lib()
+        p = self.params
+        result, ws = self._scratch.get(int(L.sfk_count_workspace_size(p.d, p.w, kb.n)))
+        rc = L.sfk_count_apply(self.counters.data_ptr(), self._seeds.ctypes.data, p.d, p.w, ops_t.data_ptr(),
+                               kb.ptr(), kb.kind, kb.rec_len, kb.n, result.data_ptr(), ws.data_ptr(), ws.numel(),
+                               _lib.FLAG_SEQUENTIAL if sequential else 0, _lib.stream_ptr())
+        _lib.check(rc, "sfk_count_apply")
+        status, bad, n_ins = Scratch.read(result)
+        self.insertions_seen += n_ins
+        raise_for_status(status, bad, kb)
+
+    def query(self, key: int) -> int:
+        return int(self.query_many(np.array([int(key) & MASK64], dtype=np.uint64))[0].item())
+
+    def query_many(self, keys) -> torch.Tensor:
+        return count_query(self.counters, self._seeds, keys)
+
+
+def count_query(counters: torch.Tensor, seeds: np.ndarray, keys) -> torch.Tensor:
+    """``_kernels.count_query`` (``_kernels.py:149-179``) on the GPU."""
+    from ._ops import normalize_keys
+
+    kb = normalize_keys(keys)
+    d, w = counters.shape
+    out = torch.empty(kb.n, dtype=torch.int64, device=counters.device)
+    if kb.n:
+        rc = _lib.lib().sfk_count_query(counters.data_ptr(), seeds.ctypes.data, d, w, kb.ptr(), kb.kind, kb.rec_len,
+                                        kb.n, out.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "sfk_count_query")
+    return out
+
+
+def cml_value(exponent, base: float):
+    """Point value of a log counter (``baselines.py:174-179``), host numpy,
+    the reference's formula: round((base**c - 1) / (base - 1)), ties away."""
+    c = np.asarray(exponent, dtype=np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        vals = np.expm1(c * math.log(base)) / (base - 1.0)
+        return np.floor(vals + 0.5).astype(np.int64)
+
+
+_CML_TABLES = {}
+
+
+def cml_tables(base: float, dev):
+    """Device tables for one base: gate[c] = base ** -c (the host libm pow the
+    reference's numba kernel calls) and value[c] = cml_value(c, base)."""
+    key = (float(base), str(dev))
+    if key not in _CML_TABLES:
+        b = float(base)
+        gate = np.array([b ** -float(c) for c in range(65536)], dtype=np.float64)
+        value = cml_value(np.arange(65536), b)
+        _CML_TABLES[key] = (torch.from_numpy(gate).to(dev), torch.from_numpy(value).to(dev))
+    return _CML_TABLES[key]
+
+
+def cml_query(exps: torch.Tensor, seeds: np.ndarray, keys, value_table=None) -> torch.Tensor:
+    """``_kernels.cml_min_exp`` (``_kernels.py:214-226``), decoded through
+    ``value_table`` when given."""
+    from ._ops import normalize_keys
+
+    kb = normalize_keys(keys)
+    d, w = exps.shape
+    out = torch.empty(kb.n, dtype=torch.int64, device=exps.device)
+    if kb.n:
+        vt = value_table.data_ptr() if value_table is not None else None
+        rc = _lib.lib().sfk_cml_query(exps.data_ptr(), seeds.ctypes.data, d, w, kb.ptr(), kb.kind, kb.rec_len, kb.n,
+                                      vt, out.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "sfk_cml_query")
+    return out
+
+
+class CmlSketch:
+    """Log-counter sketch: d arrays of w uint16 exponents (``baselines.py:182-238``).
+    Insert number n draws u = finalize64(rng_seed + (n+1) GOLDEN) and, with
+    probability base ** -c, raises every hashed cell still at the minimum
+    exponent c. No deletion."""
+
+    kind = "cml"
+    supports_deletion = False
+    DEFAULT_BASE = 1.08
+
+    def __init__(self, params: SketchParams, base: float = DEFAULT_BASE, rng_seed=None):
+        if not base > 1.0:
+            raise ConfigurationError(f"base must be > 1, got {base}")
+        self.params = params
+        self.base = float(base)
+        self.rng_seed = params.master_seed if rng_seed is None else int(rng_seed) & MASK64
+        self.exponents = torch.zeros((params.d, params.w), dtype=torch.uint16, device=device())
+        self._seeds = seed_array(params.master_seed, 0, params.d)
+        self.insertions_seen = 0
+        self._scratch = Scratch()
+
+    def insert(self, key: int) -> None:
+        self.apply_ops(*single_op(OP_INSERT, key))
+
+    def delete(self, key: int) -> None:
+        raise UnsupportedOperationError("log counters cannot be decremented; deletion is unsupported")
+
+    def apply_ops(self, ops, keys, *, sequential: bool = False) -> None:
+        ops_t, kb = normalize_stream(ops, keys)
+        L = _lib.lib()
+        p = self.params
+        gate, _ = cml_tables(self.base, self.exponents.device)
+        result, ws = self._scratch.get(int(L.sfk_cml_workspace_size(p.d, p.w, kb.n)))
+        rc = L.sfk_cml_apply(self.exponents.data_ptr(), self._seeds.ctypes.data, p.d, p.w, ops_t.data_ptr(), kb.ptr(),
+                             kb.kind, kb.rec_len, kb.n, gate.data_ptr(), self.rng_seed, self.insertions_seen,
+                             result.data_ptr(), ws.data_ptr(), ws.numel(), _lib.FLAG_SEQUENTIAL if sequential else 0,
+                             _lib.stream_ptr())
+        _lib.check(rc, "sfk_cml_apply")
+        status, bad, n_ins = Scratch.read(result)
+        self.insertions_seen += n_ins
+        raise_for_status(status, bad, kb)
+
+    def query(self, key: int) -> int:
+        return int(self.query_many(np.array([int(key) & MASK64], dtype=np.uint64))[0].item())
+
+    def query_many(self, keys) -> torch.Tensor:
+        _, value = cml_tables(self.base, self.exponents.device)
+        return cml_query(self.exponents, self._seeds, keys, value)

@@ -64,9 +64,19 @@ int engine_trace(unsigned long long* host_out, size_t runs);
 float engine_last_ms();
 int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
                    const uint64_t* fat_seeds, int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
-                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st);
+                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st,
+                   const ExtArgs* ext = nullptr);
 int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64_t cells, void* ws, size_t ws_bytes,
-                  Stats* host, cudaStream_t st);
+                  Stats* host, cudaStream_t st, uint32_t bias = 0);
+int count_fast(int32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
+               cudaStream_t st);
+int ext_query(int which, const void* table, const uint64_t* seeds, int d, int64_t w, KeySrc ks, int64_t n,
+              const int64_t* vtab, int64_t* out, cudaStream_t st);
+int gated_precheck(const int64_t* tc, int64_t n, const double* gate, const uint16_t* exps, const uint32_t* slim,
+                   int64_t cells, void* ws, size_t ws_bytes, bool* ok, cudaStream_t st);
+int launch_seq_ext(int kind, void* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks,
+                   int64_t n, const double* gate, uint64_t rng_seed, int64_t start_pos, int64_t* result,
+                   cudaStream_t st);
 int cm_fast(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks, int64_t n,
             cudaStream_t st);
 
@@ -300,12 +310,94 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
   });
 }
 
+size_t sfk_oracle_workspace_size(int d, int64_t w, int64_t n) {
+  if (d > MAXD) return 256;
+  return parallel_workspace_size(8, d, w, 0, 1, std::min<int64_t>(n, chunk_ops(d, 1)));
+}
+
 int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind,
                           int rec_len, const int64_t* true_counts, int64_t n, int64_t* inc_counts, int64_t* result,
-                          void* stream) {
+                          void* workspace, size_t workspace_bytes, int flags, void* stream) {
   if (check_common(d, w, key_kind, rec_len)) return 1;
-  return launch_seq_apply(4, 0, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr,
-                          KeySrc{keys, key_kind, rec_len}, true_counts, n, inc_counts, result, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  KeySrc all{keys, key_kind, rec_len};
+  bool ok = false;
+  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0)
+    if (int r = gated_precheck(true_counts, n, nullptr, nullptr, slim, (int64_t)d * w, workspace, workspace_bytes, &ok, st)) return r;
+  if (!ok)
+    return launch_seq_apply(4, 0, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr, all, true_counts, n,
+                            inc_counts, result, st);
+  return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    ExtArgs ext{nullptr, nullptr, 0, 0, true_counts + t0};
+    return parallel_apply(8, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr, ks, cnt, inc_counts, result,
+                          workspace, workspace_bytes, st, &ext);
+  });
+}
+
+// ---------------------------------------------------------------- Count / CML
+size_t sfk_count_workspace_size(int d, int64_t w, int64_t n) { return 4096; }
+
+int sfk_count_apply(int32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, const void* keys,
+                    int key_kind, int rec_len, int64_t n, int64_t* result, void* workspace, size_t workspace_bytes,
+                    int flags, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  KeySrc all{keys, key_kind, rec_len};
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+    return launch_seq_ext(5, counters, seeds, d, w, ops, all, n, nullptr, 0, 0, result, st);
+  return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    Stats s;
+    if (int r = collect_stats(ops + t0, cnt, reinterpret_cast<const uint32_t*>(counters), (int64_t)d * w, workspace,
+                              workspace_bytes, &s, st, 0x80000000u))
+      return r;
+    // every counter moves by at most one per op: no op can meet a bound
+    const int64_t cmax = (int64_t)(int32_t)(s.cmax ^ 0x80000000u), cmin = (int64_t)(int32_t)(s.cmin ^ 0x80000000u);
+    if (cmax + cnt <= 2147483647ll && cmin - cnt >= -2147483648ll) {
+      if (int r = count_fast(counters, seeds, d, w, ops + t0, ks, cnt, st)) return r;
+      { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_OK, -1, (int64_t)s.n_ins, nullptr, 0, 0); }
+      return check_launch("set_result");
+    }
+    return launch_seq_ext(5, counters, seeds, d, w, ops + t0, ks, cnt, nullptr, 0, 0, result, st);
+  });
+}
+
+int sfk_count_query(const int32_t* counters, const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind,
+                    int rec_len, int64_t n, int64_t* out, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  return ext_query(0, counters, seeds, d, w, KeySrc{keys, key_kind, rec_len}, n, nullptr, out, (cudaStream_t)stream);
+}
+
+size_t sfk_cml_workspace_size(int d, int64_t w, int64_t n) {
+  if (d > MAXD) return 256;
+  return parallel_workspace_size(7, d, w, 0, 1, std::min<int64_t>(n, chunk_ops(d, 1)));
+}
+
+int sfk_cml_apply(uint16_t* exps, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, const void* keys,
+                  int key_kind, int rec_len, int64_t n, const double* gate, uint64_t rng_seed, int64_t start_pos,
+                  int64_t* result, void* workspace, size_t workspace_bytes, int flags, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  if (gate == nullptr) { set_error("CML apply needs the gate table"); return 1; }
+  cudaStream_t st = (cudaStream_t)stream;
+  KeySrc all{keys, key_kind, rec_len};
+  bool ok = false;
+  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0)
+    if (int r = gated_precheck(nullptr, n, gate, exps, nullptr, (int64_t)d * w, workspace, workspace_bytes, &ok, st)) return r;
+  if (!ok) return launch_seq_ext(6, exps, seeds, d, w, ops, all, n, gate, rng_seed, start_pos, result, st);
+  return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
+    KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
+    // every op before this chunk was an insert (a failing chunk ends the batch)
+    ExtArgs ext{exps, gate, rng_seed, start_pos + t0, nullptr};
+    return parallel_apply(7, nullptr, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops + t0, ks, cnt, nullptr, result,
+                          workspace, workspace_bytes, st, &ext);
+  });
+}
+
+int sfk_cml_query(const uint16_t* exps, const uint64_t* seeds, int d, int64_t w, const void* keys, int key_kind,
+                  int rec_len, int64_t n, const int64_t* value_table, int64_t* out, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  return ext_query(1, exps, seeds, d, w, KeySrc{keys, key_kind, rec_len}, n, value_table, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -118,6 +118,15 @@ struct Stats {
   uint32_t cmax, cmin;
 };
 
+// per-op gate inputs of the gated engine kinds (sfk_sf.cu kinds 7 and 8)
+struct ExtArgs {
+  uint16_t* exps;              // CML exponents (d, w)
+  const double* gate;          // CML: gate[c] = base ** -c, 65536 entries, non-increasing
+  uint64_t rng_seed;           // CML coin-flip stream seed
+  int64_t start_pos;           // CML: inserts before this chunk
+  const int64_t* true_counts;  // oracle-assisted: exact post-insert counts
+};
+
 // counts every kernel this library launches itself (CUB's internal sort/scan
 // launches are not included); read through sfk_launch_count()
 void note_launch();

@@ -22,12 +22,17 @@ struct SeqArgs {
   const uint8_t* ops;
   KeySrc keys;
   const int64_t* true_counts;
+  uint16_t* exps;        // CML exponents
+  const double* gate;    // CML: gate[c] = base ** -c (libm pow, computed by the caller)
+  uint64_t rng_seed;     // CML coin-flip stream
+  int64_t start_pos;     // CML: inserts the sketch saw before this batch
   int64_t n;
   int64_t* inc;
   int64_t* result;
 };
 
-// kind: 0 CM, 1 CU, 2 SF flat (variant 1/2/3), 3 SF bucketed (mode 0/1/2), 4 oracle-assisted slim
+// kind: 0 CM, 1 CU, 2 SF flat (variant 1/2/3), 3 SF bucketed (mode 0/1/2), 4 oracle-assisted slim,
+//       5 Count (signed int32 counters), 6 CML (u16 exponents)
 __global__ void seq_apply_k(SeqArgs a, int kind, int variant) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int d = a.d;
@@ -38,7 +43,38 @@ __global__ void seq_apply_k(SeqArgs a, int kind, int variant) {
   for (int64_t t = 0; t < a.n; ++t) {
     const uint64_t key = load_key(a.keys, t);
     const int op = a.ops ? a.ops[t] : 0;
-    if (kind == 0) {  // cm_apply, _kernels.py:62-88
+    if (kind == 5) {  // count_apply, _kernels.py:118-146
+      int32_t* c = reinterpret_cast<int32_t*>(a.slim);
+      int dl[MAXSEEDS];
+      bool fail = false;
+      for (int i = 0; i < d; ++i) {
+        idx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        int s = (mix64(key ^ a.s_seeds.s[i] ^ 0xA5A5A5A5A5A5A5A5ull) & 1ull) ? -1 : 1;
+        if (op) s = -s;
+        const int32_t v = c[i * w + idx[i]];
+        if ((s > 0 && v == 2147483647) || (s < 0 && v == (-2147483647 - 1))) fail = true;
+        dl[i] = s;
+      }
+      if (fail) { status = SFK_SATURATED; bad = t; break; }
+      for (int i = 0; i < d; ++i) c[i * w + idx[i]] += dl[i];
+      if (op == 0) ++n_ins;
+    } else if (kind == 6) {  // cml_apply, _kernels.py:182-211
+      if (op != 0) { status = SFK_UNSUPPORTED; bad = t; break; }
+      uint32_t cmin = 0xFFFFu;
+      for (int i = 0; i < d; ++i) {
+        idx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
+        cmin = min(cmin, (uint32_t)a.exps[i * w + idx[i]]);
+      }
+      const uint64_t pos = (uint64_t)(a.start_pos + n_ins);
+      const uint64_t u = mix64(a.rng_seed + (pos + 1ull) * 0x9E3779B97F4A7C15ull);
+      const double uf = (double)(u >> 11) * (1.0 / 9007199254740992.0);
+      if (uf < a.gate[cmin]) {
+        if (cmin == 0xFFFFu) { status = SFK_SATURATED; bad = t; break; }
+        for (int i = 0; i < d; ++i)
+          if (a.exps[i * w + idx[i]] == cmin) a.exps[i * w + idx[i]] += 1;
+      }
+      ++n_ins;
+    } else if (kind == 0) {  // cm_apply, _kernels.py:62-88
       bool fail = false;
       for (int i = 0; i < d; ++i) {
         idx[i] = (int64_t)bucket(key, a.s_seeds.s[i], a.wm);
@@ -209,10 +245,40 @@ int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint3
   a.ops = ops;
   a.keys = ks;
   a.true_counts = true_counts;
+  a.exps = nullptr;
+  a.gate = nullptr;
+  a.rng_seed = 0;
+  a.start_pos = 0;
   a.n = n;
   a.inc = inc;
   a.result = result;
   { note_launch(); seq_apply_k<<<1, 32, 0, st>>>(a, kind, variant); }
+  return check_launch("seq_apply");
+}
+
+// Count (kind 5, counters = int32 table) and CML (kind 6, counters = u16 exponents)
+int launch_seq_ext(int kind, void* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks,
+                   int64_t n, const double* gate, uint64_t rng_seed, int64_t start_pos, int64_t* result,
+                   cudaStream_t st) {
+  SeqArgs a{};
+  a.slim = kind == 5 ? static_cast<uint32_t*>(counters) : nullptr;
+  a.exps = kind == 6 ? static_cast<uint16_t*>(counters) : nullptr;
+  for (int i = 0; i < d; ++i) a.s_seeds.s[i] = seeds[i];
+  a.d = d;
+  a.w = w;
+  a.wp = 1;
+  a.z = 1;
+  a.wm = make_mod((uint64_t)w);
+  a.wpm = make_mod(1);
+  a.zm = make_mod(1);
+  a.ops = ops;
+  a.keys = ks;
+  a.gate = gate;
+  a.rng_seed = rng_seed;
+  a.start_pos = start_pos;
+  a.n = n;
+  a.result = result;
+  { note_launch(); seq_apply_k<<<1, 32, 0, st>>>(a, kind, 0); }
   return check_launch("seq_apply");
 }
 

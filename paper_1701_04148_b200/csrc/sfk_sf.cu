@@ -1805,11 +1805,12 @@ __global__ void stats_ins_before_k(const uint8_t* __restrict__ ops, Stats* st) {
   for (int off = 16; off > 0; off >>= 1) ins += __shfl_down_sync(0xffffffffu, ins, off);
   if ((threadIdx.x & 31) == 0 && ins) atomicAdd(&st->ins_before_first_del, ins);
 }
-__global__ void stats_counters_k(const uint32_t* __restrict__ c, int64_t cells, Stats* st) {
+// bias = 0x80000000 maps int32 counters onto u32 order (Count sketch)
+__global__ void stats_counters_k(const uint32_t* __restrict__ c, int64_t cells, Stats* st, uint32_t bias) {
   uint32_t mx = 0, mn = U32MAX;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cells; k += (int64_t)gridDim.x * blockDim.x) {
-    mx = max(mx, c[k]);
-    mn = min(mn, c[k]);
+    mx = max(mx, c[k] ^ bias);
+    mn = min(mn, c[k] ^ bias);
   }
   for (int off = 16; off > 0; off >>= 1) {
     mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
@@ -1884,6 +1885,8 @@ struct Layout {
   void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
   unsigned long long* slim64;
+  uint8_t* zops;                   // oracle-assisted: an all-insert op stream
+  int64_t* inc_scratch;            // CML: the engine's per-row raise tallies (discarded)
   Ctl* ctl;
   Stats* stats;
   size_t total;
@@ -1891,7 +1894,9 @@ struct Layout {
 };
 
 // kind: 0 SFF (bucketed), 1 SF1 (flat), 2 CU, 3 CM exact, 4 SF4 (bucketed, sum
-// trigger), 5 SF3 (fold groups as buckets), 6 SF2 (flat fat + deletion sub-sketch)
+// trigger), 5 SF3 (fold groups as buckets), 6 SF2 (flat fat + deletion sub-sketch),
+// 7 CML (u16 exponents widened into fat_snap), 8 oracle-assisted slim
+// (7 and 8: insert-only gated min-raise with a per-op gate, op-by-op replay)
 static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
   Carver cv(base, cap);
   Layout L{};
@@ -1908,14 +1913,15 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
   const bool bucketed = kind == 0 || kind == 4 || kind == 5;
-  const bool deletes = bucketed || kind == 6;  // runs carry delete bits and (own, other) observations
+  const bool gated = kind == 7 || kind == 8;
+  const bool deletes = bucketed || kind == 6 || gated;  // runs carry delete bits (and observations)
   uint64_t fat_cells = 0;
   if (bucketed) fat_cells = (uint64_t)d * w * z;
   if (kind == 1 || kind == 6) fat_cells = std::max((uint64_t)d * wp, (uint64_t)d * w);
-  if (kind == 3) fat_cells = (uint64_t)d * w;
+  if (kind == 3 || kind == 7) fat_cells = (uint64_t)d * w;
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
   L.fat_perm = cv.take<uint32_t>(kind == 5 ? fat_cells : 1);
-  const bool need_obs = kind == 1 || kind == 6;
+  const bool need_obs = kind == 1 || kind == 6 || gated;
   L.obs = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);  // per-op b_min
   L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
   L.delbits = cv.take<uint32_t>(deletes ? n / 32 + 16 : 1);
@@ -1952,6 +1958,8 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   }
   L.recs = cv.take<char>(engine ? (uint64_t)n * (12 + 16 * (uint64_t)d) : 1);
   L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
+  L.zops = cv.take<uint8_t>(kind == 8 ? (uint64_t)n : 1);
+  L.inc_scratch = cv.take<int64_t>(MAXSEEDS);
   L.total = cv.off + 256;
   L.ok = cv.ok;
   return L;
@@ -2188,6 +2196,43 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
 }
 
 
+// CML gate (_kernels.py:200-204): insert number pos = start_pos + t draws
+// uf = (finalize64(rng_seed + (pos + 1) GOLDEN) >> 11) 2^-53 and raises when
+// uf < base ** -c for the min exponent c. With gate[c] = base ** -c
+// non-increasing (the caller checks), that is c < E_t where E_t = the first
+// c with gate[c] <= uf: a per-op cap like SF1's b_min. Ops t >= t* are never
+// replayed, and every op before t* is an insert, so pos = start_pos + t.
+__global__ void cml_gate_k(const double* __restrict__ gate, uint64_t rng_seed, int64_t start_pos, uint32_t n,
+                           uint32_t* __restrict__ obs) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint64_t pos = (uint64_t)(start_pos + (int64_t)t);
+    const uint64_t u = mix64(rng_seed + (pos + 1ull) * 0x9E3779B97F4A7C15ull);
+    const double uf = (double)(u >> 11) * (1.0 / 9007199254740992.0);
+    uint32_t lo = 0, hi = 65536;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(gate + mid) <= uf) hi = mid; else lo = mid + 1;
+    }
+    obs[t] = lo;
+  }
+}
+// oracle-assisted cap (_kernels.py:400-405): raise when m < np.uint64(true
+// count), so a negative count wraps to a cap above every u32 minimum; caps
+// above 2^32 - 1 clamp to it (exact: the precheck keeps every cell below it)
+__global__ void oracle_gate_k(const int64_t* __restrict__ tc, uint32_t n, uint32_t* __restrict__ obs) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint64_t v = (uint64_t)tc[t];
+    obs[t] = v >= (uint64_t)U32MAX ? U32MAX : (uint32_t)v;
+  }
+}
+__global__ void widen_u16_k(const uint16_t* __restrict__ src, uint32_t* __restrict__ dst, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) dst[c] = src[c];
+}
+__global__ void narrow_u16_k(const uint32_t* __restrict__ src, uint16_t* __restrict__ dst, uint32_t cells) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
+    dst[c] = (uint16_t)src[c];
+}
+
 // SF3 fat (d, w') with w' = z w: fold group of slim cell (i, j) = fat cells
 // j + m w, m < z. Regrouped as (i, j, m) so the bucketed scan applies.
 __global__ void fold_gather_k(const uint32_t* __restrict__ fat, uint32_t* __restrict__ grp, uint32_t d, uint32_t w,
@@ -2237,7 +2282,7 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
 template <int D>
 static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
                          const uint64_t* fat_seeds, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
-                         int64_t n64, int64_t* inc, int64_t* result, Layout& L, cudaStream_t st) {
+                         int64_t n64, int64_t* inc, int64_t* result, Layout& L, cudaStream_t st, const ExtArgs* ext) {
   const int sms = sm_count();
   const uint32_t n = (uint32_t)n64;
   const uint32_t N = (uint32_t)(D * n64);
@@ -2327,6 +2372,31 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hs, dsub, 1u); }
     if (int r = run_engine<D, 3>(L, slim, slim_seeds, w, ks, n, 0, inc, st, true)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
+  } else if (kind == 7 || kind == 8) {  // ----------------- CML / oracle-assisted
+    // insert-only gated min-raise on the slim-shaped table with a per-op
+    // cap (the CML coin flip as an exponent bound, or the true count); the
+    // cap is not monotone along a run, so runs replay op by op (MODE 3 with
+    // per-op data)
+    const uint32_t cells = (uint32_t)(D * w);
+    uint32_t* tab = slim;
+    const uint8_t* opk = ops;
+    if (kind == 7) {
+      { note_launch(); widen_u16_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(ext->exps, L.fat_snap, cells); }
+      tab = L.fat_snap;
+    } else {
+      cudaMemsetAsync(L.zops, 0, (size_t)n64, st);
+      opk = L.zops;
+    }
+    HashArgs<D> hs = make_hash<D>(ks, opk, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
+    { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
+    if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
+    ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+    if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    if (kind == 7) { note_launch(); cml_gate_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ext->gate, ext->rng_seed, ext->start_pos, n, L.obs); }
+    else { note_launch(); oracle_gate_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ext->true_counts, n, L.obs); }
+    if (int r = run_engine<D, 3>(L, tab, slim_seeds, w, ks, n, 0, kind == 7 ? L.inc_scratch : inc, st, true)) return r;
+    if (kind == 7) { note_launch(); narrow_u16_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.fat_snap, ext->exps, cells); }
+    { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, opk, 0, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
@@ -2351,21 +2421,26 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
 
 int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* slim_seeds,
                    const uint64_t* fat_seeds, int d, int64_t w, int64_t wp, int z, const uint8_t* ops, KeySrc ks,
-                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st) {
+                   int64_t n, int64_t* inc, int64_t* result, void* ws, size_t ws_bytes, cudaStream_t st,
+                   const ExtArgs* ext) {
   Layout L = carve(ws, ws_bytes, kind, d, w, wp, z, n);
   if (!L.ok || ws == nullptr) {
     set_error("workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
     return 1;
   }
+  if ((kind == 7 || kind == 8) && ext == nullptr) {
+    set_error("gated engine kind %d needs its per-op gate arguments", kind);
+    return 1;
+  }
   switch (d) {
-    case 1: return sf_parallel_d<1>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 2: return sf_parallel_d<2>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 3: return sf_parallel_d<3>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 4: return sf_parallel_d<4>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 5: return sf_parallel_d<5>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 6: return sf_parallel_d<6>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 7: return sf_parallel_d<7>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
-    case 8: return sf_parallel_d<8>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st);
+    case 1: return sf_parallel_d<1>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 2: return sf_parallel_d<2>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 3: return sf_parallel_d<3>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 4: return sf_parallel_d<4>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 5: return sf_parallel_d<5>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 6: return sf_parallel_d<6>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 7: return sf_parallel_d<7>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
+    case 8: return sf_parallel_d<8>(kind, slim, fat, dsub, slim_seeds, fat_seeds, w, wp, z, ops, ks, n, inc, result, L, st, ext);
   }
   set_error("parallel engine: unsupported d=%d", d);
   return 1;
@@ -2373,7 +2448,7 @@ int parallel_apply(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub, cons
 
 // CM/CU precheck statistics (host reads them back: one small sync)
 int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64_t cells, void* ws, size_t ws_bytes,
-                  Stats* host, cudaStream_t st) {
+                  Stats* host, cudaStream_t st, uint32_t bias) {
   Carver cv(ws, ws_bytes);
   cv.take<Ctl>(1);
   Stats* s = cv.take<Stats>(1);
@@ -2385,7 +2460,7 @@ int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64
   const int sms = sm_count();
   if (n > 0) { note_launch(); stats_ops_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, n, s); }
   if (n > 0) { note_launch(); stats_ins_before_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(ops, s); }
-  { note_launch(); stats_counters_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(counters, cells, s); }
+  { note_launch(); stats_counters_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(counters, cells, s, bias); }
   cudaMemcpyAsync(host, s, sizeof(Stats), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {

@@ -235,8 +235,11 @@ class SfSketch:
             np.array([int(key) & MASK64], dtype=np.uint64), np.array([true_freq], dtype=np.int64)
         )
 
-    def oracle_assisted_apply(self, keys, true_counts) -> None:
-        """Slim updates gated by exact post-insert counts (``sf.py:199-229``)."""
+    def oracle_assisted_apply(self, keys, true_counts, *, sequential: bool = False) -> None:
+        """Slim updates gated by exact post-insert counts (``sf.py:199-229``):
+        the ordered engine with the true count as each op's cap (op-by-op
+        replay), or the exact sequential engine when ``sequential`` or a count
+        exceeds 2^32 - 1."""
         if self._used_normal:
             raise UnsupportedOperationError(
                 "sketch already saw normal updates; oracle-assisted inserts would break it"
@@ -249,12 +252,14 @@ class SfSketch:
         tc = tc.to(device()).contiguous()
         if kb.n:
             self._used_oracle = True
-        result, _ = self._scratch.get(256)
         L = _lib.lib()
         p = self.params
+        ws_bytes = int(L.sfk_oracle_workspace_size(p.d, p.w, kb.n)) if not sequential else 256
+        result, ws = self._scratch.get(ws_bytes)
         rc = L.sfk_oracle_slim_apply(
             self.slim.counters.data_ptr(), self._slim_seeds.ctypes.data, p.d, p.w, kb.ptr(), kb.kind, kb.rec_len,
-            tc.data_ptr(), kb.n, self.slim.increment_counts.data_ptr(), result.data_ptr(), _lib.stream_ptr(),
+            tc.data_ptr(), kb.n, self.slim.increment_counts.data_ptr(), result.data_ptr(), ws.data_ptr(), ws.numel(),
+            _lib.FLAG_SEQUENTIAL if sequential else 0, _lib.stream_ptr(),
         )
         _lib.check(rc, "sfk_oracle_slim_apply")
         status, bad, n_ins = Scratch.read(result)
