@@ -3,8 +3,9 @@ and query throughput through the public API, each checked bit-exact against
 the CPU oracle (test infrastructure), with the rate also expressed as a
 fraction of the measured random-gather roofline (profiles/gather_peaks.json).
 
-Usage: python tools/config_sweep.py [cfg ...]   (cfg in 1 2 3 4 5 v; default 1-5;
-       v = SF2/SF3/SF4 on the cfg-3 stream)
+Usage: python tools/config_sweep.py [cfg ...]   (cfg in 1 2 3 4 5 v b; default 1-5;
+       v = SF2/SF3/SF4 on the cfg-3 stream; b = Count / CML on the cfg-2
+       stream and the oracle-assisted slim on the cfg-3 inserts)
 Prints one JSON line per measurement; profiles/<round>/config_sweep.jsonl
 keeps the committed copy."""
 import json
@@ -169,8 +170,90 @@ def cfg5():
         out.clear()
 
 
+def baselines():
+    """Count / CML on the cfg-2 stream (Count with
+    cfg-3-style deletes) and the oracle-assisted slim (rank 3) on the cfg-3
+    inserts with their exact post-insert counts: not BASELINE configs."""
+    p = P.SketchParams(d=4, w=65536, z=4, master_seed=2017)
+    seeds = P.hashing.seed_array(2017, 0, 4)
+    c2 = W.cfg2(seed=2017)
+    c3 = W.cfg3(seed=2017, alpha=1.0)
+    q = c2["distinct"][:1_000_000]
+    qd = torch.from_numpy(q).to(dev)
+    cases = [
+        ("count", c3["ops"], c3["keys"]),
+        ("cml", np.zeros(c2["keys"].size, np.uint8), c2["keys"]),
+    ]
+    for kind, ops, keys in cases:
+        ops_d, keys_d = torch.from_numpy(ops).to(dev), torch.from_numpy(keys).to(dev)
+        holder = {}
+
+        def run():
+            holder["sk"] = P.CountSketch(p) if kind == "count" else P.CmlSketch(p)
+            holder["sk"].apply_ops(ops_d, keys_d)
+
+        run()
+        ms = timed(run)
+        sk = holder["sk"]
+        t0 = time.perf_counter()
+        if kind == "count":
+            ref = np.zeros((4, 65536), np.int32)
+            st = orc.count_apply(ref, seeds, ops, keys.astype(np.uint64))
+            ok = np.array_equal(sk.counters.cpu().numpy(), ref)
+        else:
+            ref = np.zeros((4, 65536), np.uint16)
+            st = orc.cml_apply(ref, seeds, ops, keys.astype(np.uint64), 1.08, 2017, 0)
+            ok = np.array_equal(sk.exponents.cpu().numpy(), ref)
+        cpu_s = time.perf_counter() - t0
+        n = int(ops.size)
+        emit(cfg="cfg2-stream" if kind == "cml" else "cfg3-stream", op="build", kind=kind, ops=n, ms=round(ms, 3),
+             Mitems_s=round(n / (ms * 1e-3) / 1e6, 2), cpu_port_1thread_Mitems_s=round(n / cpu_s / 1e6, 2),
+             bit_exact_vs_oracle=bool(ok and st[0] == 0))
+        out = {}
+
+        def qq():
+            out["e"] = sk.query_many(qd)
+
+        qq()
+        qms = timed(qq)
+        if kind == "count":
+            want = orc.count_query(ref, seeds, q.astype(np.uint64))
+        else:
+            want = orc.cml_value(orc.cml_min_exp(ref, seeds, q.astype(np.uint64)), 1.08)
+        emit(cfg="cfg2-distinct", op="query", kind=kind, queries=int(q.size), ms=round(qms, 3),
+             Mitems_s=round(q.size / (qms * 1e-3) / 1e6, 2),
+             bit_exact_vs_oracle=bool(np.array_equal(out["e"].cpu().numpy(), want)))
+    # oracle-assisted: the cfg-3 inserts with exact running counts
+    keys = c3["keys"][c3["ops"] == 0]
+    _, inv = np.unique(keys, return_inverse=True)
+    order = np.argsort(inv, kind="stable")
+    s_ = inv[order]
+    head = np.concatenate([[True], s_[1:] != s_[:-1]])
+    starts = np.where(head)[0]
+    tc = np.empty(keys.size, np.int64)
+    tc[order] = np.arange(keys.size) - np.repeat(starts, np.diff(np.append(starts, keys.size))) + 1
+    keys_d, tc_d = torch.from_numpy(keys).to(dev), torch.from_numpy(tc).to(dev)
+    holder = {}
+
+    def orun():
+        holder["sk"] = P.SfSketch(p, "sff")
+        holder["sk"].oracle_assisted_apply(keys_d, tc_d)
+
+    orun()
+    ms = timed(orun)
+    ref = np.zeros((4, 65536), np.uint32)
+    inc = np.zeros(4, np.int64)
+    t0 = time.perf_counter()
+    st = orc.oracle_slim_apply(ref, seeds, keys.astype(np.uint64), tc, inc)
+    cpu_s = time.perf_counter() - t0
+    ok = st[0] == 0 and np.array_equal(holder["sk"].slim.counters.cpu().numpy(), ref)
+    emit(cfg="cfg3-inserts", op="oracle_assisted_apply", ops=int(keys.size), ms=round(ms, 3),
+         Mitems_s=round(keys.size / (ms * 1e-3) / 1e6, 2),
+         cpu_port_1thread_Mitems_s=round(keys.size / cpu_s / 1e6, 2), bit_exact_vs_oracle=bool(ok))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
     for w_ in which:
-        {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "v": variants}[w_]()
+        {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "v": variants, "b": baselines}[w_]()
         torch.cuda.empty_cache()
