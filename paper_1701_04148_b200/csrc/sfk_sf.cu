@@ -760,6 +760,8 @@ struct EngineArgs {
   unsigned long long* inc;     // int64[d] tallies (two's complement add)
   uint32_t budget;             // ops a lane replays per engine iteration before it yields
   int b_opdata;                // MODE 3: an insert's b_min comes from opdata (SF2) instead of A0 + x
+  const uint32_t* omax[2];     // insert-only per-op caps (CML, oracle-assisted): max cap per 32 / 1024 ops
+  const uint32_t* brk_pre;     // oracle-assisted: exclusive prefix count of ops whose cap does not exceed the previous op's
   unsigned long long* trace;   // diagnostics: per run {claim, ready, done} globaltimer ns (or null)
 };
 
@@ -1219,7 +1221,42 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     // run with every row in [0, K_i] (c_i >= A0 + x: not lagging), rows are
     // independent two-sided reflected walks and precomputed pieces apply
     uint32_t budget = a.budget;
+    if (a.brk_pre && k.rem == L && (L == 1 || a.brk_pre[e0 + L] == a.brk_pre[e0 + 1])) {
+      // caps strictly increase along the run (exact true counts of one key):
+      // once an op raises, every later op does (its cap exceeds the new
+      // minimum), so the first raising op by binary search, as SF1
+      uint32_t j = 0, hi = L;
+      while (j < hi) {
+        const uint32_t mid = (j + hi) >> 1;
+        if (a.opdata[e0 + mid] <= k.m) j = mid + 1; else hi = mid;
+      }
+      if (L - j) raise_to<D>(k.m + (L - j), c, raised);
+      k.x += L;
+      k.e += L;
+      k.rem = 0;
+      return true;
+    }
     while (k.rem && budget) {
+      if (a.omax[0]) {
+        // insert-only caps: an op raises only if m < its cap, so aligned
+        // blocks (1024 ops) and words (32 ops) whose largest cap is <= m
+        // change nothing but the insert count; skip them whole
+        const uint32_t* o0 = a.omax[0];
+        const uint32_t* o1 = a.omax[1];
+        while (k.rem && budget) {
+          if ((k.e & 1023u) == 0 && k.rem >= 1024u && __ldg(o1 + (k.e >> 10)) <= k.m) {
+            k.e += 1024u, k.rem -= 1024u, k.x += 1024u, budget -= min(budget, 32u), ++ws[3];
+            continue;
+          }
+          const uint32_t av = min(32u - (k.e & 31u), k.rem);
+          if (__ldg(o0 + (k.e >> 5)) <= k.m) {
+            k.e += av, k.rem -= av, k.x += av, budget -= min(budget, 8u), ++ws[3];
+            continue;
+          }
+          break;
+        }
+        if (!k.rem || !budget) break;
+      }
       if (!a.b_opdata && a.rmap[0] && L > 32u && (k.e & 31u) == 0) {
         const int64_t floor0 = (int64_t)(uint32_t)(k.A0 + k.x);
         int32_t v[D];
@@ -1886,6 +1923,8 @@ struct Layout {
   void* recs;
   unsigned long long* slim64;
   uint8_t* zops;                   // oracle-assisted: an all-insert op stream
+  uint32_t *omax0, *omax1;         // gated kinds: largest cap per 32 / 1024 ops
+  uint32_t *brk, *brkpre;          // oracle-assisted: cap-break flags and their prefix counts
   int64_t* inc_scratch;            // CML: the engine's per-row raise tallies (discarded)
   Ctl* ctl;
   Stats* stats;
@@ -1959,6 +1998,10 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.recs = cv.take<char>(engine ? (uint64_t)n * (12 + 16 * (uint64_t)d) : 1);
   L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
   L.zops = cv.take<uint8_t>(kind == 8 ? (uint64_t)n : 1);
+  L.omax0 = cv.take<uint32_t>(gated ? n / 32 + 2 : 1);
+  L.omax1 = cv.take<uint32_t>(gated ? n / 1024 + 2 : 1);
+  L.brk = cv.take<uint32_t>(kind == 8 ? n + 1 : 1);
+  L.brkpre = cv.take<uint32_t>(kind == 8 ? n + 1 : 1);
   L.inc_scratch = cv.take<int64_t>(MAXSEEDS);
   L.total = cv.off + 256;
   L.ok = cv.ok;
@@ -2094,11 +2137,37 @@ static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uin
   return h;
 }
 
+// brk[e] = 1 when op e's cap does not exceed op e-1's (row-0 order); brk[n] = 0
+__global__ void cap_break_k(const uint32_t* __restrict__ opdata, uint32_t n, uint32_t* __restrict__ brk) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= n; e += gridDim.x * blockDim.x)
+    brk[e] = (e == 0 || e == n) ? (e == 0 ? 1u : 0u) : (opdata[e] <= opdata[e - 1] ? 1u : 0u);
+}
+// per 32-op word (row-0 order) the largest cap, then per 1024 ops
+__global__ void opmax_word_k(const uint32_t* __restrict__ opdata, uint32_t n, uint32_t* __restrict__ omax0) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; e0 < n; e0 += gridDim.x * blockDim.x) {
+    const uint32_t e = e0 + lane;
+    uint32_t v = e < n ? opdata[e] : 0u;
+    for (int off = 16; off > 0; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) omax0[e0 >> 5] = v;
+  }
+}
+__global__ void opmax_block_k(const uint32_t* __restrict__ omax0, uint32_t nwords, uint32_t* __restrict__ omax1) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; w0 < nwords; w0 += gridDim.x * blockDim.x) {
+    const uint32_t w = w0 + lane;
+    uint32_t v = w < nwords ? omax0[w] : 0u;
+    for (int off = 16; off > 0; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) omax1[w0 >> 5] = v;
+  }
+}
+
 // The run/engine tail shared by SFF, SF1 and CU once the row-0 sorted slim
 // pairs (k_out/v_out), the links and the observations exist.
 template <int D, int MODE>
 static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int64_t w, KeySrc ks, uint32_t n, int kb,
-                      int64_t* inc, cudaStream_t st, bool b_opdata = false, bool has_ign = false) {
+                      int64_t* inc, cudaStream_t st, bool b_opdata = false, bool has_ign = false,
+                      bool cap_skip = false, bool cap_mono = false) {
   const int sms = sm_count();
   RunArgs<D> ra;
   ra.vals0 = L.v_out;
@@ -2157,6 +2226,24 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ea.delbits = L.delbits;
   ea.wsum = L.wsum;
   for (int lv = 0; lv < MAP_LEVELS; ++lv) ea.piece[lv] = nullptr, ea.rmap[lv] = nullptr;
+  ea.omax[0] = ea.omax[1] = nullptr;
+  if (cap_skip && !getenv("SFK_NO_CAP_SKIP")) {  // diagnostics knob: op-by-op only
+    const uint32_t nwords = (n + 31) / 32;
+    { note_launch(); opmax_word_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.opdata, n, L.omax0); }
+    { note_launch(); opmax_block_k<<<grid_for(nwords, 256, sms * 8), 256, 0, st>>>(L.omax0, nwords, L.omax1); }
+    ea.omax[0] = L.omax0;
+    ea.omax[1] = L.omax1;
+  }
+  ea.brk_pre = nullptr;
+  if (cap_mono && !getenv("SFK_NO_CAP_SKIP")) {
+    { note_launch(); cap_break_k<<<grid_for(n + 1, 256, sms * 8), 256, 0, st>>>(L.opdata, n, L.brk); }
+    size_t bytes2 = L.cub_tmp_bytes;
+    if (cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes2, L.brk, L.brkpre, (int)n + 1, st) != cudaSuccess) {
+      set_error("cap break scan failed");
+      return 1;
+    }
+    ea.brk_pre = L.brkpre;
+  }
   if (MODE == 2 || (MODE == 3 && !b_opdata)) {
     const uint32_t nwords = (n + 31) / 32;
     const int sum_mode = MODE == 3 ? 1 : 0;
@@ -2394,7 +2481,9 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     if (kind == 7) { note_launch(); cml_gate_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ext->gate, ext->rng_seed, ext->start_pos, n, L.obs); }
     else { note_launch(); oracle_gate_k<<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(ext->true_counts, n, L.obs); }
-    if (int r = run_engine<D, 3>(L, tab, slim_seeds, w, ks, n, 0, kind == 7 ? L.inc_scratch : inc, st, true)) return r;
+    if (int r = run_engine<D, 3>(L, tab, slim_seeds, w, ks, n, 0, kind == 7 ? L.inc_scratch : inc, st, true, false,
+                                 true, kind == 8))
+      return r;
     if (kind == 7) { note_launch(); narrow_u16_k<<<grid_for(cells, 256, sms * 8), 256, 0, st>>>(L.fat_snap, ext->exps, cells); }
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, opk, 0, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
