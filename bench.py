@@ -53,15 +53,30 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cm", action="store_true", help="skip the cfg-2 CM merge leg")
+    ap.add_argument("--shared-slim", action="store_true",
+                    help="N>1: build once on rank 0, broadcast the slim, shard the queries (strong scaling) "
+                         "instead of one independent replica per GPU (weak scaling, the default)")
     return ap.parse_args()
 
 
+def replicas(args, world):
+    return world > 1 and not args.shared_slim
+
+
 def workload_config(args, world):
+    if replicas(args, world):
+        par = ("replicas only: %d independent sketches, one per GPU (SF updates are order-dependent and do not "
+               "shard); rank r builds its own cfg-3 stream (seed %d + r) and answers its own %d queries; no "
+               "data-path collective" % (world, SEED, args.queries))
+    elif world > 1:
+        par = "build on rank 0 (order-dependent), slim broadcast, queries sharded over %d GPU(s)" % world
+    else:
+        par = "1 GPU"
     return {
         "workload": "cfg3 SFF build (10M inserts Zipf(%.1f)/1M + 2M interleaved deletes) + cfg5 %d point queries "
                     "(50%% present Zipf(%.1f), 50%% absent) on the built slim" % (args.alpha, args.queries, args.alpha_q),
         "d": D, "w": W, "z": Z, "ops": 12_000_000, "queries": args.queries,
-        "parallelism": "build on rank 0 (order-dependent), slim broadcast, queries sharded over %d GPU(s)" % world,
+        "parallelism": par,
         "l2": "query keys (4 B x Q) exceed L2; L2 flushed (256 MiB write) between steps",
         "seed": SEED,
     }
@@ -288,14 +303,20 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
 
-    stream = Wl.cfg3(seed=SEED, alpha=args.alpha)
+    rep = replicas(args, world)
+    # replicas: rank r is an independent sketch over its own stream and queries
+    rseed = SEED + rank if rep else SEED
+    stream = Wl.cfg3(seed=rseed, alpha=args.alpha)
     n_ops = int(stream["ops"].shape[0])
     ops_d = torch.from_numpy(stream["ops"]).to(dev)
     keys_d = torch.from_numpy(stream["keys"]).to(dev)
-    per = args.queries // world
-    q0 = rank * per
-    qn = per if rank < world - 1 else args.queries - q0
-    gen = Wl.DeviceQueryStream(SEED + 5, stream["distinct"], args.alpha_q)
+    if rep or world == 1:
+        q0, qn = 0, args.queries
+    else:
+        per = args.queries // world
+        q0 = rank * per
+        qn = per if rank < world - 1 else args.queries - q0
+    gen = Wl.DeviceQueryStream(rseed + 5, stream["distinct"], args.alpha_q)
     qkeys = gen.keys(q0, qn)
     qout = torch.empty(qn, dtype=torch.int64, device=dev)
     params = P.SketchParams(d=D, w=W, z=Z, master_seed=SEED)
@@ -315,12 +336,12 @@ def run_ours(args):
     def step():
         ev[0].record()
         eng = 0.0
-        if rank == 0:
+        if rank == 0 or rep:
             reset()
             sk.apply_ops(ops_d, keys_d)
             eng = float(L.sfk_engine_last_ms())
         ev[1].record()
-        if world > 1:
+        if world > 1 and not rep:
             sk.broadcast_slim_(src=0)
         ev[2].record()
         rc = L.sfk_min_query(sk.slim.counters.data_ptr(), sk._slim_seeds.ctypes.data, D, W, qkeys.data_ptr(),
@@ -366,7 +387,7 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, build_ms, bcast_ms, query_ms = (float(x) for x in t.tolist())
-    items = n_ops + args.queries
+    items = (n_ops + args.queries) * (world if rep else 1)  # whole job: every replica's ops and queries
     value = items / (step_ms * 1e-3) / 1e6
 
     hbm, hbm_src, gather = measured_peaks()
@@ -437,10 +458,10 @@ def run_ours(args):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            if rank == 0:
+            if rank == 0 or rep:
                 reset()
                 sk.apply_ops(ops_h, keys_h)  # H2D inside the API call
-            if world > 1:
+            if world > 1 and not rep:
                 sk.broadcast_slim_(src=0)
             query_min_host(sk.slim.counters, sk._slim_seeds, qk_h, qo_h)
             torch.cuda.synchronize()
@@ -452,8 +473,8 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": round(items / float(et.item()) / 1e6, 3), "unit": "Mitems/s",
-               "h2d_bytes_per_step": int(n_ops * 5 + args.queries * 4) if rank == 0 else int(qn * 4),
-               "d2h_bytes_per_step": int(args.queries * 8 + 24),
+               "h2d_bytes_per_step": int(n_ops * 5 + qn * 4) if (rank == 0 or rep) else int(qn * 4),
+               "d2h_bytes_per_step": int(qn * 8 + 24),
                "note": "apply_ops from pinned host ops/keys; queries through query_min_host (3-stream "
                        "H2D/kernel/D2H pipeline); wall clock, max over ranks"}
         # the estimates must equal the device-resident run's
@@ -482,7 +503,8 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mitems/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True,
+            "scaling": "weak" if (rep or world == 1) else "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
             "config": workload_config(args, world), "breakdown": breakdown, "roofline": roofline,
             "cpu_baseline": cpu, "e2e": e2e, "cm_merge": cm_leg, "gpu_launches": int(launches),
