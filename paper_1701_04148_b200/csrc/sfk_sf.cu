@@ -34,8 +34,6 @@
 // s raises give c_i' = max(c_i, m0 + s).
 #include <cub/cub.cuh>
 
-#include <cstring>
-
 #include "sfk_common.cuh"
 
 namespace sfk {
@@ -62,17 +60,6 @@ static uint32_t engine_budget() {
   return (uint32_t)v;
 }
 
-// SFK_ENGINE=flow selects the dataflow engine (flow_engine_k), =poll the
-// polling engine (poll_engine_k)
-static int engine_flow() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("SFK_ENGINE");
-    v = (s && strcmp(s, "flow") == 0) ? 1 : 0;
-  }
-  return v;
-}
-
 static int engine_blocks_per_sm() {
   static int v = -1;
   if (v < 0) {
@@ -97,7 +84,6 @@ struct Ctl {
   uint32_t qhead, qtail;     // engine ready queue
   uint32_t executed;         // engine runs finished
   uint32_t pad;
-  uint32_t ovf_head, ovf_tail;  // dataflow engine: overflow queue of ready DIRECT runs
 };
 
 // ---------------------------------------------------------------- 1. hash_emit
@@ -1734,320 +1720,6 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
   }
 }
 
-// ---------------------------------------------------------------- 5b. dataflow engine
-// The same runs and replay as poll_engine_k, scheduled by dependency counts
-// instead of polling. Per run S: its predecessor runs (the last run on each
-// of its cells), deduplicated, minus those implied by another predecessor
-// (one level of transitive reduction: P -> S is dropped when P is itself a
-// predecessor of another predecessor of S). pend[S] = the rest. A run that
-// finishes publishes its cells, then notifies each successor: one atomic
-// decrement, or none when it is the successor's only predecessor (DIRECT).
-// The lane that completes a successor's count executes it next itself (a
-// dependency chain stays in one lane with no polling round trip); further
-// ready successors go to a ticketed queue that idle lanes drain.
-constexpr uint32_t FLOW_DIRECT = 0x80000000u;
-
-template <int D>
-struct FlowArgs {
-  const RunRec<D>* recs;
-  const uint2* links;      // 32-B records per (t, row): {rank, prev}, {own, oth}, {cell, e}
-  const uint32_t* vals0;   // row-0 sorted vals: op id = v >> (kb + 1)
-  int kb;
-  const uint32_t* bnd;     // run boundaries (row-0 order) and their exclusive prefix / positions
-  const uint32_t* bidx;
-  const uint32_t* bpos;
-  const uint32_t* ridx;    // run id of a head op (exclusive prefix of head flags over t)
-  const Ctl* ctl;
-  int drop_rows;           // SF1: rows in bits0 are not in the run's cells' sequences
-  uint32_t* pred;          // [S * D + i]: distinct predecessor runs (NONE32 padded)
-  uint32_t* succ;          // [P * D + i]: successor run (| FLOW_DIRECT) notified through row i, or NONE32
-  uint32_t* pend;          // [S]: predecessors to wait for
-  uint32_t* src;           // [S]: 1 if pend == 0 (sources), scanned into queue slots
-};
-
-template <int D>
-__device__ __forceinline__ uint32_t flow_run_of_op(const FlowArgs<D>& f, uint32_t p) {
-  const uint32_t ep = f.links[((size_t)p * D) * 4 + 2].y;  // row-0 position of op p
-  const uint32_t b = f.bidx[ep] + f.bnd[ep] - 1u;          // index of the boundary that starts p's run
-  const uint32_t th = f.vals0[f.bpos[b]] >> (f.kb + 1);
-  return f.ridx[th];
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) flow_pred_k(FlowArgs<D> f) {
-  const uint32_t R = f.ctl->n_runs;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-    const RunRec<D>& rec = f.recs[r];
-    const uint32_t th = f.vals0[rec.e0] >> (f.kb + 1);
-    const uint32_t drop = f.drop_rows ? rec.bits0 : 0u;
-    uint32_t P[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      P[i] = NONE32;
-      if ((drop >> i) & 1u) continue;
-      const uint32_t p = f.links[((size_t)th * D + i) * 4].y;
-      if (p != NONE32 && p != 0xFFFFFFFEu) P[i] = flow_run_of_op<D>(f, p);
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      bool dup = false;
-#pragma unroll
-      for (int j = 0; j < i; ++j) dup = dup || P[j] == P[i];
-      f.pred[(size_t)r * D + i] = dup ? NONE32 : P[i];
-    }
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) flow_edge_k(FlowArgs<D> f) {
-  const uint32_t R = f.ctl->n_runs;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-    uint32_t Q[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) Q[i] = f.pred[(size_t)r * D + i];
-    bool keep[D];
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      bool red = false;
-      if (Q[i] != NONE32) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          if (j == i || Q[j] == NONE32) continue;
-#pragma unroll
-          for (int k = 0; k < D; ++k) red = red || f.pred[(size_t)Q[j] * D + k] == Q[i];
-        }
-      }
-      keep[i] = Q[i] != NONE32 && !red;
-      cnt += keep[i] ? 1u : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (keep[i]) f.succ[(size_t)Q[i] * D + i] = r | (cnt == 1 ? FLOW_DIRECT : 0u);
-    f.pend[r] = cnt;
-    f.src[r] = cnt != 1 ? 1u : 0u;  // claimed in stream order unless DIRECT
-  }
-}
-
-// the claim list: runs that are not DIRECT (several or no effective
-// predecessors), in run-id (stream) order, and the queue counters
-__global__ void flow_sources_k(const uint32_t* __restrict__ src, const uint32_t* __restrict__ pos, Ctl* ctl,
-                               uint32_t* __restrict__ slots) {
-  const uint32_t R = ctl->n_runs;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-    if (src[r]) slots[pos[r]] = r;
-    if (r == R - 1) {
-      ctl->qtail = pos[r] + src[r];
-      ctl->qhead = 0;
-      ctl->executed = 0;
-      ctl->ovf_head = 0;
-      ctl->ovf_tail = 0;
-    }
-  }
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-template <int D>
-struct FlowEngineArgs {
-  EngineArgs<D> e;
-  const uint32_t* succ;    // [P * D + i]: successor through row i (| FLOW_DIRECT) or NONE32
-  const uint32_t* claim;   // non-DIRECT runs in stream order (claimed by idle lanes)
-  uint32_t* ovf;           // overflow queue of DIRECT runs (a lane's FIFO was full)
-  Ctl* ctl;
-  int drop_rows;
-};
-
-constexpr int FLOW_FIFO = 4;  // per-lane queue of ready DIRECT runs (shared memory)
-constexpr bool FLOW_KEEP = true;  // (16-entry FIFO, all kept: 14.0 ms; 4 + shared queue: 27.2 ms)
-
-// Hybrid of the polling engine and dataflow: runs with several effective
-// predecessors are claimed in stream order and poll their cells (seq-checked
-// 64-bit words, as poll_engine_k); a run with a single effective predecessor
-// (DIRECT) is never claimed: the lane that finishes that predecessor queues
-// it and runs it next, so a chain of DIRECT runs executes in one lane with
-// no polling round trip. A DIRECT run's other predecessors finished before
-// its effective one started, so its cells are final when it starts (the seq
-// check still guards against late visibility). Deadlock-free: claimed runs
-// are taken in stream order and DIRECT runs never wait on a later run.
-template <int D, int MODE>
-__global__ void __launch_bounds__(256) flow_engine_k(FlowEngineArgs<D> fa) {
-  __shared__ uint32_t lut[256];
-  __shared__ uint8_t rlut[WMAX * 8 * 256];
-  __shared__ uint32_t fifo[FLOW_FIFO][256];
-  build_step_lut(lut);
-  if (MODE == 2) build_reflect_lut(rlut);
-  __syncthreads();
-  const EngineArgs<D>& a = fa.e;
-  const uint32_t lane = lane_id();
-  const uint32_t R = fa.ctl->n_runs;
-  const uint32_t NC = fa.ctl->qtail;  // claimable runs
-  bool has = false, exhausted = false;
-  uint32_t cur = NONE32, pend = 0, fh = 0, ft = 0;  // fifo head / tail (monotone counters)
-  uint32_t cells[D], rank[D], A[D], O[D], c[D], raised[D];
-  uint32_t e0 = 0, info = 0, bits0 = 0;
-#pragma unroll
-  for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0, A[i] = 0, O[i] = 0, c[i] = 0;
-  Cursor k{};
-  uint32_t ws[5] = {0, 0, 0, 0, 0};
-  unsigned long long st_cyc = 0, st_runs = 0, st_iters = 0;
-  uint32_t idle = 0, pool_base = 0, pool_cnt = 0;
-  while (true) {
-    ++st_iters;
-    // 1. a free lane takes its next run: its own FIFO, the overflow queue, or a claim
-    uint32_t take = NONE32;
-    if (!has && fh != ft) {
-      take = fifo[fh % FLOW_FIFO][threadIdx.x];
-      ++fh;
-    }
-    if (!has && take == NONE32) {
-      const uint32_t oh = ld_relaxed_u32(&fa.ctl->ovf_head);
-      if (oh < ld_relaxed_u32(&fa.ctl->ovf_tail) && atomicCAS(&fa.ctl->ovf_head, oh, oh + 1u) == oh) {
-        uint32_t v;
-        while ((v = ld_relaxed_u32(fa.ovf + oh)) == NONE32) {
-        }
-        take = v;
-      }
-    }
-    const unsigned need = __ballot_sync(0xffffffffu, !has && take == NONE32 && !exhausted);
-    if (need) {
-      const int leader = __ffs(need) - 1;
-      const uint32_t kneed = (uint32_t)__popc(need), pos = (uint32_t)__popc(need & lanemask_lt());
-      uint32_t r;
-      if (pool_cnt >= kneed) {
-        r = pool_base + pos;
-        pool_base += kneed;
-        pool_cnt -= kneed;
-      } else {
-        uint32_t nb = 0;
-        if ((int)lane == leader) nb = atomicAdd(&fa.ctl->qhead, CLAIM_POOL);
-        nb = __shfl_sync(0xffffffffu, nb, leader);
-        r = pos < pool_cnt ? pool_base + pos : nb + (pos - pool_cnt);
-        pool_base = nb + (kneed - pool_cnt);
-        pool_cnt = CLAIM_POOL - (kneed - pool_cnt);
-      }
-      if ((need >> lane) & 1u) {
-        if (r < NC) take = __ldg(fa.claim + r);
-        else exhausted = true;
-      }
-    }
-    if (take != NONE32) {
-      cur = take;
-      const RunRec<D>& rec = a.recs[cur];
-      e0 = rec.e0;
-      info = rec.info;
-      bits0 = rec.bits0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        cells[i] = rec.cells[i];
-        rank[i] = rec.rank[i];
-        if (MODE >= 2) A[i] = rec.A[i], O[i] = rec.O[i];
-      }
-      pend = (1u << D) - 1u;
-      if (fa.drop_rows) pend &= ~bits0;
-      has = true;
-    }
-    bool progressed = false, finished = false;
-    if (has && pend) {
-      unsigned long long wv[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-        if (pend & (1u << i)) wv[i] = ld_relaxed_u64(a.slim64 + cells[i]);
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-        if ((pend & (1u << i)) && (uint32_t)(wv[i] >> 32) == rank[i]) {
-          c[i] = (uint32_t)wv[i];
-          pend &= ~(1u << i);
-        }
-      if (!pend) {
-        if (fa.drop_rows) {
-#pragma unroll
-          for (int i = 1; i < D; ++i)
-            if ((bits0 >> i) & 1u) c[i] = U32MAX;
-        }
-        k.m = c[0];
-#pragma unroll
-        for (int i = 1; i < D; ++i) k.m = min(k.m, c[i]);
-        k.A0 = A[0];
-#pragma unroll
-        for (int i = 1; i < D; ++i) k.A0 = min(k.A0, A[i]);
-        k.x = 0;
-        k.e = e0;
-        k.rem = info & 0x7fffffffu;
-        k.ring = false;
-      }
-    }
-    if (has && !pend) {
-      const long long t0 = clock64();
-      const bool done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws, lut, rlut);
-      st_cyc += clock64() - t0;
-      progressed = true;
-      if (done) {
-        const uint32_t L = info & 0x7fffffffu;
-        const uint32_t drop = fa.drop_rows ? bits0 : 0u;
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-          if (!((drop >> i) & 1u))
-            st_relaxed_u64(a.slim64 + cells[i], ((unsigned long long)(rank[i] + L) << 32) | c[i]);
-        // the first DIRECT successor runs next in this lane; the others go to
-        // the shared queue so that independent successors run in parallel
-        bool kept = fh != ft;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          const uint32_t sv = __ldg(fa.succ + (size_t)cur * D + i);
-          if (sv == NONE32 || !(sv & FLOW_DIRECT)) continue;
-          const uint32_t sid = sv & ~FLOW_DIRECT;
-          if (!kept && FLOW_KEEP) {
-            fifo[ft % FLOW_FIFO][threadIdx.x] = sid;
-            ++ft;
-            kept = true;
-          } else {
-            st_relaxed_u32(fa.ovf + atomicAdd(&fa.ctl->ovf_tail, 1u), sid);
-          }
-        }
-        has = false;
-        finished = true;
-        ++st_runs;
-      }
-    }
-    const unsigned fin = __ballot_sync(0xffffffffu, finished);
-    if (fin && lane == (uint32_t)(__ffs(fin) - 1)) atomicAdd(&fa.ctl->executed, (uint32_t)__popc(fin));
-    if (__all_sync(0xffffffffu, !has && fh == ft && exhausted)) {
-      uint32_t ex = 0;
-      if (lane == 0) ex = ld_relaxed_u32(&fa.ctl->executed);
-      ex = __shfl_sync(0xffffffffu, ex, 0);
-      if (ex >= R) break;
-    }
-    if (__any_sync(0xffffffffu, progressed)) {
-      idle = 0;
-    } else if (++idle > 4) {
-      __nanosleep(min(idle * 4u, 32u));
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    unsigned long long r = raised[i];
-    for (int off = 16; off > 0; off >>= 1) r += __shfl_down_sync(0xffffffffu, r, off);
-    if (lane == 0 && r) atomicAdd(a.inc + i, r);
-  }
-  unsigned long long sv[8] = {ws[0], ws[1], ws[2], (unsigned long long)st_cyc, st_runs, lane == 0 ? st_iters : 0ull,
-                              ws[3], ws[4]};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    unsigned long long v = sv[q];
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0 && v) atomicAdd(&g_engine_stats[q], v);
-  }
-}
-
 __global__ void pack_slim_k(const uint32_t* __restrict__ slim, unsigned long long* __restrict__ s64, uint32_t cells) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) s64[c] = slim[c];
 }
@@ -2063,8 +1735,6 @@ __global__ void ctl_init_k(Ctl* ctl) {
   ctl->qhead = 0;
   ctl->qtail = 0;
   ctl->executed = 0;
-  ctl->ovf_head = 0;
-  ctl->ovf_tail = 0;
 }
 
 // undo the fat deltas of ops t >= t* (the fat was written for the whole
@@ -2255,9 +1925,6 @@ struct Layout {
   uint8_t* zops;                   // oracle-assisted: an all-insert op stream
   uint32_t *omax0, *omax1;         // gated kinds: largest cap per 32 / 1024 ops
   uint32_t *brk, *brkpre;          // oracle-assisted: cap-break flags and their prefix counts
-  uint32_t *fl_pred, *fl_succ;     // dataflow engine: per run D predecessor / successor run ids
-  uint32_t *fl_pend, *fl_src, *fl_pos, *fl_slots;  //   pending counts, claim flags / positions, claim list
-  uint32_t* fl_ovf;                //   overflow queue of ready DIRECT runs
   int64_t* inc_scratch;            // CML: the engine's per-row raise tallies (discarded)
   Ctl* ctl;
   Stats* stats;
@@ -2333,13 +2000,6 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.zops = cv.take<uint8_t>(kind == 8 ? (uint64_t)n : 1);
   L.omax0 = cv.take<uint32_t>(gated ? n / 32 + 2 : 1);
   L.omax1 = cv.take<uint32_t>(gated ? n / 1024 + 2 : 1);
-  L.fl_pred = cv.take<uint32_t>(engine ? (uint64_t)n * d : 1);
-  L.fl_succ = cv.take<uint32_t>(engine ? (uint64_t)n * d : 1);
-  L.fl_pend = cv.take<uint32_t>(engine ? n : 1);
-  L.fl_src = cv.take<uint32_t>(engine ? n + 1 : 1);
-  L.fl_pos = cv.take<uint32_t>(engine ? n + 1 : 1);
-  L.fl_slots = cv.take<uint32_t>(engine ? n : 1);
-  L.fl_ovf = cv.take<uint32_t>(engine ? n : 1);
   L.brk = cv.take<uint32_t>(kind == 8 ? n + 1 : 1);
   L.brkpre = cv.take<uint32_t>(kind == 8 ? n + 1 : 1);
   L.inc_scratch = cv.take<int64_t>(MAXSEEDS);
@@ -2612,44 +2272,8 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
     }
     ea.trace = g_trace;
   }
-  const bool flow = engine_flow() != 0;
-  if (flow) {
-    FlowArgs<D> fa;
-    fa.recs = static_cast<const RunRec<D>*>(L.recs);
-    fa.links = L.links;
-    fa.vals0 = L.v_out;
-    fa.kb = kb;
-    fa.bnd = L.bnd;
-    fa.bidx = L.bidx;
-    fa.bpos = L.bpos;
-    fa.ridx = L.ridx;
-    fa.ctl = L.ctl;
-    fa.drop_rows = MODE <= 1 ? 1 : 0;
-    fa.pred = L.fl_pred;
-    fa.succ = L.fl_succ;
-    fa.pend = L.fl_pend;
-    fa.src = L.fl_src;
-    cudaMemsetAsync(L.fl_succ, 0xFF, (size_t)n * D * 4, st);
-    cudaMemsetAsync(L.fl_ovf, 0xFF, (size_t)n * 4, st);
-    cudaMemsetAsync(L.fl_src, 0, (size_t)(n + 1) * 4, st);
-    { note_launch(); flow_pred_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(fa); }
-    { note_launch(); flow_edge_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(fa); }
-    size_t fb = L.cub_tmp_bytes;
-    if (cub::DeviceScan::ExclusiveSum(L.cub_tmp, fb, L.fl_src, L.fl_pos, (int)n + 1, st) != cudaSuccess) {
-      set_error("flow source scan failed");
-      return 1;
-    }
-    { note_launch(); flow_sources_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.fl_src, L.fl_pos, L.ctl, L.fl_slots); }
-  }
   if (g_time_engine) cudaEventRecord(g_ev[0], st);
-  if (flow) {
-    FlowEngineArgs<D> fe{ea, L.fl_succ, L.fl_slots, L.fl_ovf, L.ctl, MODE <= 1 ? 1 : 0};
-    note_launch();
-    flow_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(fe);
-  } else {
-    note_launch();
-    poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea);
-  }
+  { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea); }
   if (g_time_engine) {
     cudaEventRecord(g_ev[1], st);
     g_ev_pending = true;
