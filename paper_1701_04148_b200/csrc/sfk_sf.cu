@@ -45,6 +45,15 @@ constexpr int ENGINE_BLOCKS_PER_SM = 1;
 // default replay budget: a long run never stalls the other lanes of its warp
 // for more than ~this many ops
 constexpr uint32_t REPLAY_BUDGET = 1024;
+// SFF runs with deletes of at most this many ops replay op by op (uniform code)
+#ifndef SFK_SHORT_RUN_MAX
+#define SFK_SHORT_RUN_MAX 32
+#endif
+#ifndef SFK_SHORT_ALL
+#define SFK_SHORT_ALL 0
+#endif
+constexpr bool SHORT_RUNS = SFK_SHORT_RUN_MAX > 0;
+constexpr uint32_t SHORT_RUN_MAX = SFK_SHORT_RUN_MAX;
 // engine run claiming: run ids per warp atomic, and how far ahead of a claim
 // the run records are prefetched into L2
 constexpr uint32_t CLAIM_POOL = 64;
@@ -1376,6 +1385,38 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
       ws[2] += 1;
     }
     return k.rem == 0;
+  }
+  if (SHORT_RUNS && (SFK_SHORT_ALL || (info >> 31)) && L <= SHORT_RUN_MAX && k.rem == L) {
+    // short run (its delete bits are all in bits0): op by op
+    // with the same few instructions in every lane, so a warp's lanes that
+    // became ready together replay in lockstep instead of serialising the
+    // word-replay paths. Insert: own counts A_i + x, gate m < A0 + x, raise
+    // the rows at m. Delete: c_i = min(c_i, max(A_i + x, O_i)).
+    uint32_t m = k.m, x = k.x;
+    for (uint32_t j = 0; j < L; ++j) {
+      if (!((bits0 >> j) & 1u)) {
+        x += 1u;
+        if (m < k.A0 + x) {
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            if (c[i] == m) c[i] += 1u, raised[i] += 1u;
+          m += 1u;
+        }
+      } else {
+        x -= 1u;
+        m = U32MAX;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          c[i] = min(c[i], max(A[i] + x, O[i]));
+          m = min(m, c[i]);
+        }
+      }
+    }
+    k.m = m;
+    k.x = x;
+    k.e += L;
+    k.rem = 0;
+    return true;
   }
   if (!(info >> 31)) {  // insert-only SFF run: the j-th insert raises iff m0 < A0 + j
     const int64_t jstar = max((int64_t)k.m - (int64_t)k.A0 + 1, (int64_t)1);

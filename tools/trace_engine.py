@@ -82,8 +82,10 @@ def main():
     r = int(np.argmax(done))
     hops = 0
     tot = {"replay": 0, "detect": 0, "claim_wait": 0}
+    path = []
     while True:
         hops += 1
+        path.append(r)
         tot["replay"] += done[r] - ready[r]
         gate = dep_done[r]
         if claim[r] > gate:  # the run was claimed after its inputs were ready
@@ -98,6 +100,14 @@ def main():
     print(f"critical path: {hops} hops; replay {tot['replay'] / 1e6:.2f} ms, dependency detect "
           f"{tot['detect'] / 1e6:.2f} ms ({tot['detect'] / max(hops, 1):.0f} ns/hop), claim wait "
           f"{tot['claim_wait'] / 1e6:.2f} ms")
+    path = np.array(path)
+    pl = rlen[path]
+    prep = (done - ready)[path]
+    for lo, hi in ((1, 2), (2, 8), (8, 32), (32, 256), (256, 1024), (1024, 1 << 40)):
+        sel = (pl >= lo) & (pl < hi)
+        if sel.any():
+            print(f"critical-path runs with {lo}..{hi - 1} ops: {int(sel.sum())} runs, {int(pl[sel].sum())} ops, "
+                  f"replay {prep[sel].sum() / 1e6:.3f} ms ({prep[sel].sum() / max(pl[sel].sum(), 1):.1f} ns/op)")
     for lo in (32, 1000, 10000):
         sel = rlen >= lo
         if sel.any():
