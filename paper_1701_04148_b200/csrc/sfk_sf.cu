@@ -49,6 +49,9 @@ constexpr uint32_t REPLAY_BUDGET = 1024;
 #ifndef SFK_SHORT_RUN_MAX
 #define SFK_SHORT_RUN_MAX 32
 #endif
+#ifndef SFK_DROP_ROW0
+#define SFK_DROP_ROW0 1
+#endif
 #ifndef SFK_SHORT_ALL
 #define SFK_SHORT_ALL 0
 #endif
@@ -476,8 +479,28 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
     const uint32_t e = base + q;
     if (e >= N) break;
     const uint32_t lb = hd[q] ? 0u : run.v;
-    ign[e] = (cc[q] >= row_cells && tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
+    ign[e] = ((SFK_DROP_ROW0 || cc[q] >= row_cells) && tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
     run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
+  }
+}
+
+// CU: per op, 1 + an upper bound of its minimum (_kernels.py:100-113): a
+// cell starts the batch at its current value and every op on it raises it by
+// at most one, so min_i (value_i + ops before this one on cell i) bounds it.
+// Stored where the ignore scan reads b_min: row i drops when its lower bound
+// (the largest batch count of a key seen earlier on the cell) exceeds it.
+template <int D>
+__global__ void cu_cap_k(const uint2* __restrict__ links, const uint32_t* __restrict__ slim, uint32_t n,
+                         uint32_t* __restrict__ obs) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    unsigned long long ub = ~0ull;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint32_t rank = links[((size_t)t * D + i) * 4].x;
+      const uint32_t cell = links[((size_t)t * D + i) * 4 + 2].x;
+      ub = min(ub, (unsigned long long)__ldg(slim + cell) + rank);
+    }
+    obs[t] = (uint32_t)min(ub + 1ull, (unsigned long long)U32MAX);
   }
 }
 
@@ -591,7 +614,9 @@ struct RunArgs {
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
   uint32_t* headflag;      // [t] (written by runs_head_k)
-  int has_ign;             // SF1 ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
+  int has_ign;             // SF1 / CU ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
+  const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
+  const uint32_t* kprev;   // key order: the previous op of the same key (NONE32 for a key's first op)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
   uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
@@ -610,21 +635,40 @@ __global__ void __launch_bounds__(256) runs_head_k(RunArgs<D> a) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       prev[i] = a.links[((size_t)t * D + i) * 4].y;
-      if (prev[i] == IGN_MARK) mask |= 1u << i;  // (SF1) a dropped pair: not in the cell's sequence
+      if (prev[i] == IGN_MARK) mask |= 1u << i;  // a dropped pair: not in the cell's sequence
     }
-    bool cont = valid && prev[0] != NONE32;
+    // every kept row's previous op is the same op p
+    uint32_t p = NONE32;
+    bool cont = valid && mask != (1u << D) - 1u;
 #pragma unroll
-    for (int i = 1; i < D; ++i) cont = cont && ((mask >> i) & 1u || prev[i] == prev[0]);
+    for (int i = 0; i < D; ++i) {
+      if ((mask >> i) & 1u) continue;
+      if (prev[i] == NONE32) cont = false;
+      else if (p == NONE32) p = prev[i];
+      else if (prev[i] != p) cont = false;
+    }
+    cont = cont && p != NONE32;
     if (cont && a.has_ign) {  // the run's ops must drop the same rows
       uint32_t pm = 0;
 #pragma unroll
-      for (int i = 1; i < D; ++i)
-        if (a.links[((size_t)prev[0] * D + i) * 4].y == IGN_MARK) pm |= 1u << i;
+      for (int i = 0; i < D; ++i)
+        if (a.links[((size_t)p * D + i) * 4].y == IGN_MARK) pm |= 1u << i;
       cont = pm == mask;
     }
-    if (cont) cont = load_key(a.keys, prev[0]) == load_key(a.keys, t);
+    if (cont) {
+      // key order: p must be the key's previous op, so a run is a contiguous
+      // stretch of its key's ops; row-0 order: the same key
+      cont = a.kprev ? a.kprev[t] == p : load_key(a.keys, p) == load_key(a.keys, t);
+    }
     a.headflag[t] = (valid && !cont) ? 1u : 0u;
   }
+}
+
+// key order: the previous op of the same key, from the key-sorted op list
+__global__ void key_prev_k(const uint64_t* __restrict__ ks, const uint32_t* __restrict__ tb, uint32_t n,
+                           uint32_t* __restrict__ kprev) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    kprev[tb[j]] = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
 }
 
 // Per op in row-0 order: flags, b_min (SF1/SF2), delete bits, run boundaries.
@@ -633,10 +677,12 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
   const uint32_t tstar = a.ctl->fail_t;
   uint32_t ins = 0;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.n; e += gridDim.x * blockDim.x) {
-    const uint32_t v = a.vals0[e];
-    const uint32_t t = v >> (a.kb + 1);
-    const uint32_t op = (v >> a.kb) & 1u;
+    // position e: row-0 order, or key order (SF1 / CU with dropped rows: every
+    // valid op is an insert there, a delete being the failing op)
+    const uint32_t v = a.order ? 0u : a.vals0[e];
+    const uint32_t t = a.order ? a.order[e] : v >> (a.kb + 1);
     const bool valid = t < tstar;
+    const uint32_t op = a.order ? (valid ? 0u : 1u) : (v >> a.kb) & 1u;
     const bool cont = valid && !a.headflag[t];
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
     if (a.obs) a.opdata[e] = a.obs[t];  // per-op b_min (segscan WRITE_OBS 4)
@@ -687,6 +733,7 @@ struct BuildArgs {
   Mod wm;
   uint32_t w;
   RunRec<D>* recs;
+  const uint32_t* order;    // key order (see RunArgs)
   Ctl* ctl;
 };
 
@@ -700,11 +747,13 @@ __global__ void boundary_pos_k(const uint32_t* __restrict__ bnd, const uint32_t*
 
 template <int D>
 __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
-    if (t == a.n - 1) a.ctl->n_runs = a.ridx[t] + a.headflag[t];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
+    if (j == a.n - 1) a.ctl->n_runs = a.ridx[j] + a.headflag[j];
+    const uint32_t t = a.order ? a.order[j] : j;
     if (!a.headflag[t]) continue;
     const uint32_t r = a.ridx[t];
-    const uint32_t e0 = a.links[((size_t)t * D) * 4 + 2].y;  // row-0 position of op t
+    // the head's position in the run order (row 0 or key order)
+    const uint32_t e0 = a.order ? j : a.links[((size_t)t * D) * 4 + 2].y;
     // the run ends at the next boundary (row-0 order)
     const uint32_t e_end = a.bpos[a.bidx[e0] + 1];
     const uint32_t L = e_end - e0;
@@ -715,7 +764,7 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     rec.bits0 = 0;
     if (!a.delbits) {  // SF1 / CU: the rows this run's ops drop (IGN_MARK links)
 #pragma unroll
-      for (int i = 1; i < D; ++i)
+      for (int i = 0; i < D; ++i)
         if (a.links[((size_t)t * D + i) * a.lstride].y == IGN_MARK) rec.bits0 |= 1u << i;
     }
     if (a.delbits && hasdel) {
@@ -1683,14 +1732,18 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
             if (MODE >= 2) A[i] = rec.A[i], O[i] = rec.O[i];
           }
           pend = (1u << D) - 1u;
-          if (MODE <= 1) pend &= ~bits0;  // SF1: rows this run drops (never row 0)
-          has = true;
+          if (MODE <= 1) pend &= ~bits0;  // SF1 / CU: rows this run drops
+          // a run that drops every row neither reads nor writes the slim (its
+          // ops cannot raise): nothing to replay
+          has = MODE > 1 || pend != 0;
         } else {
           exhausted = true;
         }
       }
     }
-    if (__all_sync(0xffffffffu, !has)) break;  // no lane holds a run and none can get one
+    // no lane holds a run and none can get one (a lane may also be between
+    // runs after claiming one that drops every row)
+    if (__all_sync(0xffffffffu, !has && exhausted)) break;
     bool progressed = false;
     if (has && pend) {
       unsigned long long wv[D];
@@ -1707,7 +1760,7 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
         if (a.trace) a.trace[3ull * rid + 1] = gtimer();
         if (MODE <= 1) {
 #pragma unroll
-          for (int i = 1; i < D; ++i)
+          for (int i = 0; i < D; ++i)
             if ((bits0 >> i) & 1u) c[i] = U32MAX;  // a dropped row: neither the min nor raised
         }
         k.m = c[0];
@@ -1959,6 +2012,7 @@ struct Layout {
   uint32_t* ridx;
   uint64_t *k64a, *k64b;          // SF1 ignore pass: materialised keys, sorted
   uint32_t *ta, *tb, *headpos;     //   op ids, sorted op ids, key segment heads
+  uint32_t* kprev;                 //   previous op of the same key
   uint8_t* ign;                    //   dropped (op, row) flags in cell order
   void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
@@ -1988,7 +2042,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.k_out = cv.take<uint32_t>(N);
   L.v_out = cv.take<uint32_t>(N);
   L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n + 1));
-  if (kind == 1) L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, key_sort_temp_bytes((uint32_t)n));
+  if (kind == 1 || kind == 2) L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, key_sort_temp_bytes((uint32_t)n));
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
@@ -2001,7 +2055,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   if (kind == 3 || kind == 7) fat_cells = (uint64_t)d * w;
   L.fat_snap = cv.take<uint32_t>(fat_cells ? fat_cells : 1);
   L.fat_perm = cv.take<uint32_t>(kind == 5 ? fat_cells : 1);
-  const bool need_obs = kind == 1 || kind == 6 || gated;
+  const bool need_obs = kind == 1 || kind == 2 || kind == 6 || gated;
   L.obs = cv.take<uint32_t>(need_obs ? (uint64_t)n : 1);  // per-op b_min
   L.obs2 = cv.take<uint2>(1);  // SFF interleaves its observations with the links
   L.delbits = cv.take<uint32_t>(deletes ? n / 32 + 16 : 1);
@@ -2027,7 +2081,8 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.delpre = cv.take<uint32_t>(engine ? n + 1 : 1);
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
   {
-    const bool sf1 = kind == 1;
+    const bool sf1 = kind == 1 || kind == 2;  // SF1 and CU: the ignore pass
+    L.kprev = cv.take<uint32_t>(sf1 ? n : 1);
     L.k64a = cv.take<uint64_t>(sf1 ? n : 1);
     L.k64b = cv.take<uint64_t>(sf1 ? n : 1);
     L.ta = cv.take<uint32_t>(sf1 ? n : 1);
@@ -2225,6 +2280,8 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
   ra.has_ign = has_ign ? 1 : 0;
+  ra.order = has_ign ? L.tb : nullptr;
+  ra.kprev = has_ign ? L.kprev : nullptr;
   ra.ctl = L.ctl;
   { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
@@ -2256,6 +2313,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.wm = make_mod((uint64_t)w);
   ba.w = (uint32_t)w;
   ba.recs = static_cast<RunRec<D>*>(L.recs);
+  ba.order = has_ign ? L.tb : nullptr;
   ba.ctl = L.ctl;
   { note_launch(); runs_build_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ba); }
   const uint32_t cells = (uint32_t)(D * w);
@@ -2393,6 +2451,7 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k64a, L.k64b, L.ta, L.tb, (int)n, 0, kbits, st);
   if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
   { note_launch(); key_heads_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, n, L.headpos); }
+  { note_launch(); key_prev_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, L.tb, n, L.kprev); }
   bytes = L.cub_tmp_bytes;
   e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
   if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
@@ -2533,7 +2592,15 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
-    if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st)) return r;
+    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob (shared with SF1)
+    if (ign) {
+      // a CU cell is >= the batch count of every key on it, and <= its value
+      // before the batch + the ops on it so far: an op drops the rows whose
+      // lower bound exceeds that upper bound of its own minimum
+      { note_launch(); cu_cap_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(L.links, slim, n, L.obs); }
+      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st)) return r;
+    }
+    if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st, false, ign)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
   } else {  // ------------------------------------------------------- CM exact
     HashArgs<D> h = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
