@@ -304,6 +304,7 @@ struct ScanOut {
 
 // WRITE_OBS: 0 none, 1 obs (b_min / bucket max), 2 obs2 (own count, max of the others),
 //            3 obs2 (own count, sum of the others clamped to 2^32 - 1: the SF2/SF3/SF4 trigger)
+//            5 obs (CU drop pass: 1 + an upper bound of each op's minimum; fat_init = the slim)
 template <int Z, bool HAS_FAT, int WRITE_OBS, bool WRITE_LINKS>
 __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ vals, uint32_t N, int kb,
@@ -383,6 +384,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
 #pragma unroll
         for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
       }
+    }
+    if (WRITE_OBS == 5) {
+      // CU: 1 + (the cell's value before the batch + the ops before this one
+      // on it), min over the op's rows = 1 + an upper bound of its minimum
+      const unsigned long long ub = (unsigned long long)__ldg(o.fat_init + c) + (e - run.head) + 1ull;
+      atomicMin(o.obs + t, (uint32_t)min(ub, (unsigned long long)U32MAX));
     }
     if (WRITE_LINKS) {
       // One 32-B record per (op, row): rank in the cell, previous op,
@@ -481,26 +488,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
     const uint32_t lb = hd[q] ? 0u : run.v;
     ign[e] = ((SFK_DROP_ROW0 || cc[q] >= row_cells) && tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
     run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
-  }
-}
-
-// CU: per op, 1 + an upper bound of its minimum (_kernels.py:100-113): a
-// cell starts the batch at its current value and every op on it raises it by
-// at most one, so min_i (value_i + ops before this one on cell i) bounds it.
-// Stored where the ignore scan reads b_min: row i drops when its lower bound
-// (the largest batch count of a key seen earlier on the cell) exceeds it.
-template <int D>
-__global__ void cu_cap_k(const uint2* __restrict__ links, const uint32_t* __restrict__ slim, uint32_t n,
-                         uint32_t* __restrict__ obs) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    unsigned long long ub = ~0ull;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      const uint32_t rank = links[((size_t)t * D + i) * 4].x;
-      const uint32_t cell = links[((size_t)t * D + i) * 4 + 2].x;
-      ub = min(ub, (unsigned long long)__ldg(slim + cell) + rank);
-    }
-    obs[t] = (uint32_t)min(ub + 1ull, (unsigned long long)U32MAX);
   }
 }
 
@@ -2590,14 +2577,17 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
-    ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
-    if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
     const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob (shared with SF1)
-    if (ign) {
+    if (!ign) {
+      ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
+      if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
+    } else {  // the filtered scan writes every link record itself
       // a CU cell is >= the batch count of every key on it, and <= its value
       // before the batch + the ops on it so far: an op drops the rows whose
       // lower bound exceeds that upper bound of its own minimum
-      { note_launch(); cu_cap_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(L.links, slim, n, L.obs); }
+      ScanOut su{slim, nullptr, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
+      cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
+      if (int r = run_scan<1, false, 5, false>(L.k_out, L.v_out, N, 0, L.tiles, su, st)) return r;
       if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st)) return r;
     }
     if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st, false, ign)) return r;

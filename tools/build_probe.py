@@ -18,7 +18,11 @@ alpha = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 cfg = sys.argv[3] if len(sys.argv) > 3 else "3"
 L = _lib.lib()
 dev = torch.device("cuda", 0)
-if cfg == "4":
+if variant == "cu":
+    c = W.cfg2(seed=2017)
+    ops, keys = torch.from_numpy(c["ops"]).to(dev), torch.from_numpy(c["keys"]).to(dev)
+    params = P.SketchParams(d=4, w=65536, master_seed=2017)
+elif cfg == "4":
     c = W.cfg4(seed=2017)
     ops, keys = torch.from_numpy(c["ops"]).to(dev), torch.from_numpy(c["records"]).to(dev)
     params = P.SketchParams(d=4, w=12800, w_prime=4194304, master_seed=2017)
@@ -29,7 +33,7 @@ else:
 ts, es = [], []
 L.sfk_engine_timing(1)
 for r in range(6):
-    sk = P.SfSketch(params, variant)
+    sk = P.CuSketch(params) if variant == "cu" else P.SfSketch(params, variant)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
