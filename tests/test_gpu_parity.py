@@ -249,3 +249,37 @@ def test_sf1_dropped_pairs(oracle, d, w, wp, batches):
         status, idx = apply_batches(sk, ops, keys, batches=batches, sequential=sequential)
         assert (status, idx) == st[:2]
         assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+
+
+@pytest.mark.parametrize("kind", ["sf1", "cu"])
+@pytest.mark.parametrize("d,w,preset", [(4, 64, "zero"), (4, 256, "random"), (3, 50, "skewed"), (8, 128, "random")])
+def test_dropped_pairs_any_start_state(oracle, kind, d, w, preset):
+    """The drop rules of SF1 (lower bound >= b_min) and CU (lower bound >
+    upper bound of the op's minimum, from the cells' values before the batch)
+    hold from any starting state: preset slim / fat counters, hot keys over
+    narrow rows, several batches, every row droppable (row 0 included)."""
+    rng = np.random.default_rng(d * 100 + w + len(preset))
+    hot = rng.integers(0, 1 << 32, size=4, dtype=np.uint64).astype(np.uint32)
+    cold = rng.integers(0, 1 << 32, size=5000, dtype=np.uint64).astype(np.uint32)
+    n = 120_000
+    keys = np.where(rng.random(n) < 0.4, hot[rng.integers(0, hot.size, n)],
+                    cold[rng.integers(0, cold.size, n)]).astype(np.uint32)
+    ops = np.zeros(n, np.uint8)
+    wp = 4 * w if kind == "sf1" else None
+    o = oracle.OracleSketch(kind, d, w, 1, wp, 5)
+    if preset == "random":
+        o.slim[...] = rng.integers(0, 3000, size=o.slim.shape).astype(np.uint32)
+    elif preset == "skewed":
+        o.slim[...] = (rng.pareto(1.2, size=o.slim.shape) * 50).astype(np.uint32)
+    if o.fat is not None and preset != "zero":
+        o.fat[...] = rng.integers(0, 2000, size=o.fat.shape).astype(np.uint32)
+    sk = make_sketch(kind, d, w, 1, wp, 5)
+    counters_of(sk).copy_(torch.from_numpy(o.slim.copy()))
+    if o.fat is not None:
+        sk.fat.counters.copy_(torch.from_numpy(o.fat.copy()))
+    bounds = np.linspace(0, n, 4).astype(int)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        st = o.apply_ops(ops[a:b], keys[a:b].astype(np.uint64))
+        assert st[0] == 0
+        sk.apply_ops(ops[a:b], keys[a:b])
+    assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
