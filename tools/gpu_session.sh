@@ -10,7 +10,7 @@ for w in $what; do
   case $w in
   tests) timeout 1800 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "tests rc=$?" ;;
   smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke rc=$?" ;;
-  bench) timeout 900 python bench.py --steps 5 --warmup 3 > $out/bench.json 2> $out/bench.err; echo "bench rc=$?"; tail -c 3000 $out/bench.json ;;
+  bench) timeout 900 python bench.py --steps 10 --warmup 3 > $out/bench.json 2> $out/bench.err; echo "bench rc=$?"; tail -c 3000 $out/bench.json ;;
   launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $out/launches_bench.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-cm \
       > $out/ncu_launch.log 2>&1; echo "launches rc=$?"; python tools/launches.py $out/launches_bench.csv > $out/launches_bench_summary.txt 2>&1 ;;
