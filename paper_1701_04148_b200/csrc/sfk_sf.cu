@@ -49,12 +49,6 @@ constexpr uint32_t REPLAY_BUDGET = 1024;
 #ifndef SFK_SHORT_RUN_MAX
 #define SFK_SHORT_RUN_MAX 32
 #endif
-#ifndef SFK_DROP_ROW0
-#define SFK_DROP_ROW0 1
-#endif
-#ifndef SFK_SHORT_ALL
-#define SFK_SHORT_ALL 0
-#endif
 constexpr bool SHORT_RUNS = SFK_SHORT_RUN_MAX > 0;
 constexpr uint32_t SHORT_RUN_MAX = SFK_SHORT_RUN_MAX;
 // engine run claiming: run ids per warp atomic, and how far ahead of a claim
@@ -407,7 +401,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
 }
 
 
-// ---------------------------------------------------------------- SF1: ignorable (op, row) pairs
+// ---------------------------------------------------------------- SF1 / CU: ignorable (op, row) pairs
 // An SF1 slim cell never drops below the batch net count of any key that maps
 // to it: inserts only raise cells, and a key's own inserts keep the min of its
 // d cells at or above its count (b_min >= its count, and each insert raises a
@@ -415,8 +409,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
 // belongs to a key whose count then was >= this op's b_min, the cell is >=
 // b_min at this op's turn: it is neither a min below b_min nor raised, and the
 // op's outcome does not depend on it. Such (op, row) pairs leave the cell's
-// sequence: the engine neither waits for nor publishes them. Row 0 is never
-// dropped, so runs stay contiguous in row-0 order.
+// sequence: the engine neither waits for nor publishes them. Any row may be
+// dropped; runs are then laid out in key order (runs_head_k, key_prev_k).
+// CU reuses the pass with "b_min" = 1 + an upper bound of the op's minimum
+// (segscan WRITE_OBS 5): a row whose lower bound exceeds it is not a minimum.
 
 // per-op count of its key among the batch's ops up to and including it
 __global__ void iota_k(uint32_t* __restrict__ t, uint32_t n) {
@@ -486,7 +482,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
     const uint32_t e = base + q;
     if (e >= N) break;
     const uint32_t lb = hd[q] ? 0u : run.v;
-    ign[e] = ((SFK_DROP_ROW0 || cc[q] >= row_cells) && tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
+    ign[e] = (tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
     run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
   }
 }
@@ -1422,7 +1418,7 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
     }
     return k.rem == 0;
   }
-  if (SHORT_RUNS && (SFK_SHORT_ALL || (info >> 31)) && L <= SHORT_RUN_MAX && k.rem == L) {
+  if (SHORT_RUNS && (info >> 31) && L <= SHORT_RUN_MAX && k.rem == L) {
     // short run (its delete bits are all in bits0): op by op
     // with the same few instructions in every lane, so a warp's lanes that
     // became ready together replay in lockstep instead of serialising the
