@@ -51,6 +51,9 @@ constexpr uint32_t REPLAY_BUDGET = 1024;
 #endif
 constexpr bool SHORT_RUNS = SFK_SHORT_RUN_MAX > 0;
 constexpr uint32_t SHORT_RUN_MAX = SFK_SHORT_RUN_MAX;
+// runs with per-op caps (SF2, CML, oracle-assisted) of at most this many ops
+// replay from caps loaded into registers when the run is claimed
+constexpr int SHORT_CAPS = 8;
 // engine run claiming: run ids per warp atomic, and how far ahead of a claim
 // the run records are prefetched into L2
 constexpr uint32_t CLAIM_POOL = 64;
@@ -1346,6 +1349,52 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
           break;
         }
       }
+      if (a.b_opdata && (k.e & 31u) == 0 && k.rem >= 64u && budget >= 64u) {
+        // whole words of a long run with per-op caps: the next words' caps
+        // and delete bits are prefetched into L1 while this word replays
+        uint32_t w = k.e >> 5;
+        const uint32_t nwf = min(k.rem, budget) >> 5;
+        const uint4* src = reinterpret_cast<const uint4*>(a.opdata);
+        for (uint32_t wi = 0; wi < nwf; ++wi, ++w) {
+          if (wi + 2 < nwf) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(src + (size_t)(w + 2) * 8));
+            if (((w + 2) & 31u) == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.delbits + w + 2));
+          }
+          uint4 cb[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cb[q] = __ldg(src + (size_t)w * 8 + q);
+          const uint32_t cdb = __ldg(a.delbits + w);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const uint4 v4 = cb[jj >> 2];
+            const uint32_t ob = (jj & 3) == 0 ? v4.x : (jj & 3) == 1 ? v4.y : (jj & 3) == 2 ? v4.z : v4.w;
+            if (!((cdb >> jj) & 1u)) {
+              k.x += 1u;
+              if (k.m < ob) {
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+                  if (c[i] == k.m) c[i] += 1u, raised[i] += 1u;
+                k.m += 1u;
+              }
+            } else {
+              k.x -= 1u;
+              uint32_t m = U32MAX;
+#pragma unroll
+              for (int i = 0; i < D; ++i) {
+                const int64_t T = (int64_t)A[i] + (int64_t)(int32_t)k.x + (int64_t)O[i];
+                if ((int64_t)c[i] > T) c[i] -= 1u;
+                m = min(m, c[i]);
+              }
+              k.m = m;
+            }
+          }
+        }
+        k.e += nwf * 32u;
+        k.rem -= nwf * 32u;
+        budget -= nwf * 32u;
+        ws[2] += nwf;
+        continue;
+      }
       const uint32_t off = k.e & 31u, avail = min(min(32u - off, k.rem), budget);
       const uint32_t bits = a.delbits[k.e >> 5] >> off;
       if (a.b_opdata) {
@@ -1665,6 +1714,9 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
   bool has = false, exhausted = false;
   uint32_t cells[D], rank[D], A[D], O[D], c[D], raised[D];
   uint32_t e0 = 0, info = 0, bits0 = 0, pend = 0;  // pend: bit i = cell i not seen ready yet
+  uint32_t sb[SHORT_CAPS];  // per-op caps of a short run (MODE 3 with per-op data), loaded at claim
+#pragma unroll
+  for (int q = 0; q < SHORT_CAPS; ++q) sb[q] = 0;
   uint32_t rid = 0;
 #pragma unroll
   for (int i = 0; i < D; ++i) raised[i] = 0, cells[i] = 0, rank[i] = 0, A[i] = 0, O[i] = 0, c[i] = 0;
@@ -1716,6 +1768,12 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
           }
           pend = (1u << D) - 1u;
           if (MODE <= 1) pend &= ~bits0;  // SF1 / CU: rows this run drops
+          if (MODE == 3 && a.b_opdata && (info & 0x7fffffffu) <= (uint32_t)SHORT_CAPS) {
+            // issue the short run's cap loads now; they land while its cells are polled
+            const uint32_t Ls = info & 0x7fffffffu;
+#pragma unroll
+            for (int q = 0; q < SHORT_CAPS; ++q) sb[q] = (uint32_t)q < Ls ? __ldg(a.opdata + e0 + q) : 0u;
+          }
           // a run that drops every row neither reads nor writes the slim (its
           // ops cannot raise): nothing to replay
           has = MODE > 1 || pend != 0;
@@ -1760,7 +1818,43 @@ __global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
     }
     if (has && !pend) {
       const long long t0 = clock64();
-      const bool done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws, lut, rlut);
+      bool done;
+      if (MODE == 3 && a.b_opdata && k.rem == (info & 0x7fffffffu) && k.rem <= (uint32_t)SHORT_CAPS) {
+        // short run with per-op caps (SF2 b_min, CML / oracle caps) from
+        // registers: insert x += 1, raise the rows at m when m < cap; delete
+        // x -= 1, c_i = c_i - 1 where c_i > A_i + x + O_i
+        uint32_t m = k.m;
+        int32_t x = (int32_t)k.x;
+#pragma unroll
+        for (int q = 0; q < SHORT_CAPS; ++q) {
+          if ((uint32_t)q >= k.rem) break;
+          if (!((bits0 >> q) & 1u)) {
+            x += 1;
+            if (m < sb[q]) {
+#pragma unroll
+              for (int i = 0; i < D; ++i)
+                if (c[i] == m) c[i] += 1u, raised[i] += 1u;
+              m += 1u;
+            }
+          } else {
+            x -= 1;
+            m = U32MAX;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const int64_t T = (int64_t)A[i] + (int64_t)x + (int64_t)O[i];
+              if ((int64_t)c[i] > T) c[i] -= 1u;
+              m = min(m, c[i]);
+            }
+          }
+        }
+        k.m = m;
+        k.x = (uint32_t)x;
+        k.e += k.rem;
+        k.rem = 0;
+        done = true;
+      } else {
+        done = replay_step<D, MODE>(a, k, e0, info, bits0, A, O, c, raised, ws, lut, rlut);
+      }
       st_cyc += clock64() - t0;
       if (done) {
         const uint32_t L = info & 0x7fffffffu;

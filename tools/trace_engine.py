@@ -61,13 +61,14 @@ def dag(keys, seeds, w):
 
 def main():
     alpha = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
+    variant = sys.argv[2] if len(sys.argv) > 2 else "sff"
     c = W.cfg3(seed=2017, alpha=alpha)
     keys = c["keys"].astype(np.uint64)
     nr, pred, rlen = dag(keys, seed_array(2017, 0, 4), 65536)
     ops_d = torch.from_numpy(c["ops"]).cuda()
     keys_d = torch.from_numpy(c["keys"]).cuda()
     for _ in range(2):
-        sk = P.SfSketch(P.SketchParams(d=4, w=65536, z=4, master_seed=2017), "sff")
+        sk = P.SfSketch(P.SketchParams(d=4, w=65536, z=4, w_prime=262144, master_seed=2017), variant)
         sk.apply_ops(ops_d, keys_d)
     torch.cuda.synchronize()
     tr = np.zeros(3 * nr, dtype=np.uint64)
