@@ -208,6 +208,22 @@ int sfk_cml_query(const uint16_t* exps, const uint64_t* seeds, int d, int64_t w,
                   int key_kind, int rec_len, int64_t n, const int64_t* value_table, int64_t* out,
                   void* stream);
 
+/* Trace ingestion (workloads.read_trace / load_trace, workloads.py:132-172):
+ * "OP,key" text lines parsed on the device. Phase 1 fills per-line arrays
+ * (device, nbytes + 1 entries each): line_pos (byte offset), status (0 blank
+ * or comment, 1 op, 2 "expected 'OP,key'", 3 unknown op token, 4 bad key,
+ * 5 key out of 64-bit range, 6 non-ASCII line left to the host), op, key;
+ * info (host int64[3]) = {lines, first error line (0-based) or -1, non-ASCII
+ * lines}. Phase 2 compacts the status-1 lines into ops / keys (device) and
+ * returns their count in *n_out (host). Universal newlines, str.strip()
+ * whitespace, int(key, 10) syntax (sign, digit-group underscores). */
+size_t sfk_trace_workspace_size(int64_t nbytes);
+int sfk_trace_parse_lines(const uint8_t* text, int64_t nbytes, int64_t* line_pos, uint8_t* status,
+                          uint8_t* op, uint64_t* key, int64_t* info, void* workspace,
+                          size_t workspace_bytes, void* stream);
+int sfk_trace_compact(const uint8_t* status, const uint8_t* op, const uint64_t* key, int64_t nlines,
+                      uint8_t* ops, uint64_t* keys, int64_t* n_out, void* workspace,
+                      size_t workspace_bytes, int64_t nbytes, void* stream);
 
 #ifdef __cplusplus
 }

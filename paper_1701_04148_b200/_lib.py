@@ -42,6 +42,9 @@ EXPORTS = (
     "sfk_cml_workspace_size",
     "sfk_cml_apply",
     "sfk_cml_query",
+    "sfk_trace_workspace_size",
+    "sfk_trace_parse_lines",
+    "sfk_trace_compact",
     "sfk_launch_count",
     "sfk_gen_query_keys",
     "sfk_engine_stats",
@@ -100,6 +103,10 @@ def load_library() -> ctypes.CDLL:
     L.sfk_cml_workspace_size.restype = SZ
     L.sfk_cml_apply.argtypes = [P, P, I, I64, P, P, I, I, I64, P, ctypes.c_uint64, I64, P, P, SZ, I, P]
     L.sfk_cml_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P, P]
+    L.sfk_trace_workspace_size.argtypes = [I64]
+    L.sfk_trace_workspace_size.restype = SZ
+    L.sfk_trace_parse_lines.argtypes = [P, I64, P, P, P, P, P, P, SZ, P]
+    L.sfk_trace_compact.argtypes = [P, P, P, I64, P, P, P, P, SZ, I64, P]
     L.sfk_launch_count.restype = ctypes.c_ulonglong
     L.sfk_engine_stats.argtypes = [P, I]
     L.sfk_engine_timing.argtypes = [I]

@@ -72,6 +72,11 @@ int count_fast(int32_t* counters, const uint64_t* seeds, int d, int64_t w, const
                cudaStream_t st);
 int ext_query(int which, const void* table, const uint64_t* seeds, int d, int64_t w, KeySrc ks, int64_t n,
               const int64_t* vtab, int64_t* out, cudaStream_t st);
+size_t trace_workspace_size(int64_t nb);
+int trace_parse_lines(const uint8_t* txt, int64_t nb, int64_t* line_pos, uint8_t* status, uint8_t* lop, uint64_t* lkey,
+                      int64_t* out_info, void* ws, size_t ws_bytes, cudaStream_t st);
+int trace_compact(const uint8_t* status, const uint8_t* lop, const uint64_t* lkey, int64_t nlines, uint8_t* ops,
+                  uint64_t* keys, int64_t* out_n, void* ws, size_t ws_bytes, int64_t nb, cudaStream_t st);
 int gated_precheck(const int64_t* tc, int64_t n, const double* gate, const uint16_t* exps, const uint32_t* slim,
                    int64_t cells, void* ws, size_t ws_bytes, bool* ok, cudaStream_t st);
 int launch_seq_ext(int kind, void* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, KeySrc ks,
@@ -333,6 +338,23 @@ int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t 
     return parallel_apply(8, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr, ks, cnt, inc_counts, result,
                           workspace, workspace_bytes, st, &ext);
   });
+}
+
+// ---------------------------------------------------------------- trace ingestion
+size_t sfk_trace_workspace_size(int64_t nbytes) { return trace_workspace_size(nbytes); }
+
+int sfk_trace_parse_lines(const uint8_t* text, int64_t nbytes, int64_t* line_pos, uint8_t* status, uint8_t* op,
+                          uint64_t* key, int64_t* info, void* workspace, size_t workspace_bytes, void* stream) {
+  if (nbytes < 0) { set_error("negative trace size"); return 1; }
+  return trace_parse_lines(text, nbytes, line_pos, status, op, key, info, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
+}
+
+int sfk_trace_compact(const uint8_t* status, const uint8_t* op, const uint64_t* key, int64_t nlines, uint8_t* ops,
+                      uint64_t* keys, int64_t* n_out, void* workspace, size_t workspace_bytes, int64_t nbytes,
+                      void* stream) {
+  return trace_compact(status, op, key, nlines, ops, keys, n_out, workspace, workspace_bytes, nbytes,
+                       (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- Count / CML

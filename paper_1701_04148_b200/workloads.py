@@ -165,3 +165,143 @@ def query_keys(seed: int, present: np.ndarray, alpha_q: float, t0: int, t1: int)
         todo = todo[hit]
         j += 1
     return out
+
+
+# ---------------------------------------------------------------- traces
+# The reference's trace format (workloads.py:132-184): one "OP,key" line per
+# operation, OP in {I, D}, key a base-10 integer in [0, 2^64); blank lines and
+# '#' comments are skipped; line numbers are 1-based over all lines.
+class Operation:
+    """One trace operation: ``op`` is "insert" or "delete"."""
+
+    __slots__ = ("op", "key")
+
+    def __init__(self, op: str, key: int):
+        self.op = op
+        self.key = key
+
+    def __eq__(self, other):
+        return isinstance(other, Operation) and (self.op, self.key) == (other.op, other.key)
+
+    def __repr__(self):
+        return f"Operation(op={self.op!r}, key={self.key!r})"
+
+
+def _trace_line(line: str, lineno: int):
+    """The reference's per-line rules (workloads.py:137-155), for the lines
+    the device leaves to the host (non-ASCII) and for error messages.
+    Returns None for a skipped line, else (op code, key)."""
+    from .errors import TraceFormatError
+
+    stripped = line.strip()
+    if not stripped or stripped.startswith("#"):
+        return None
+    parts = stripped.split(",")
+    if len(parts) != 2:
+        raise TraceFormatError(lineno, f"expected 'OP,key', got {stripped!r}")
+    token, key_text = parts[0].strip(), parts[1].strip()
+    if token not in ("I", "D"):
+        raise TraceFormatError(lineno, f"unknown op token {token!r}")
+    try:
+        key = int(key_text, 10)
+    except ValueError:
+        raise TraceFormatError(lineno, f"bad key {key_text!r}") from None
+    if not 0 <= key <= MASK64:
+        raise TraceFormatError(lineno, f"key {key} out of 64-bit range")
+    return (0 if token == "I" else 1), key
+
+
+def load_trace(path, device=None):
+    """Read a whole trace into (ops uint8, keys uint64) CUDA tensors, parsed
+    on the GPU (``csrc/sfk_trace.cu``); same results and the same
+    ``TraceFormatError`` (line number and message) as the reference's
+    ``load_trace``. Lines with non-ASCII bytes (Unicode whitespace or digits,
+    which Python's ``str.strip`` / ``int`` accept) are finished on the host."""
+    import torch
+
+    from . import _lib
+    from ._ops import device as default_device
+
+    dev = device if device is not None else default_device()
+    with open(path, "rb") as fh:
+        data = fh.read()
+    nb = len(data)
+    L = _lib.lib()
+    host = np.frombuffer(data, dtype=np.uint8) if nb else np.zeros(1, np.uint8)
+    text = torch.from_numpy(host.copy()).to(dev)
+    cap = nb + 1
+    pos = torch.empty(cap, dtype=torch.int64, device=dev)
+    status = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    lop = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    lkey = torch.zeros(cap, dtype=torch.uint64, device=dev)
+    ws = torch.empty(int(L.sfk_trace_workspace_size(nb)), dtype=torch.uint8, device=dev)
+    info = np.zeros(3, dtype=np.int64)
+    _lib.check(L.sfk_trace_parse_lines(text.data_ptr(), nb, pos.data_ptr(), status.data_ptr(), lop.data_ptr(),
+                                       lkey.data_ptr(), info.ctypes.data, ws.data_ptr(), ws.numel(),
+                                       _lib.stream_ptr()), "sfk_trace_parse_lines")
+    nlines, first_err, n_complex = (int(v) for v in info)
+
+    def line_text(i):
+        a = int(pos[i].item())
+        b = int(pos[i + 1].item()) if i + 1 < nlines else nb
+        return data[a:b].decode("utf-8")
+
+    if n_complex:
+        # non-ASCII lines: the reference's rules on the host (Unicode
+        # whitespace / digits); an error there counts in line order below
+        idx = torch.nonzero(status[:nlines] == 6).flatten().tolist()
+        for i in idx:
+            if first_err >= 0 and i > first_err:
+                break
+            try:
+                r = _trace_line(line_text(i), i + 1)
+            except Exception:  # noqa: BLE001 - re-raised in line order below
+                first_err = i if first_err < 0 else min(first_err, i)
+                break
+            if r is None:
+                status[i] = 0
+            else:
+                status[i] = 1
+                lop[i] = r[0]
+                lkey[i:i + 1].view(torch.int64).fill_(int(np.array([r[1]], np.uint64).view(np.int64)[0]))
+    if first_err >= 0:
+        _trace_line(line_text(first_err), first_err + 1)  # raises the reference's error
+        raise AssertionError("device flagged a trace line the host parser accepts")
+    ops = torch.empty(max(nlines, 1), dtype=torch.uint8, device=dev)
+    keys = torch.empty(max(nlines, 1), dtype=torch.uint64, device=dev)
+    n_out = np.zeros(1, dtype=np.int64)
+    _lib.check(L.sfk_trace_compact(status.data_ptr(), lop.data_ptr(), lkey.data_ptr(), nlines, ops.data_ptr(),
+                                   keys.data_ptr(), n_out.ctypes.data, ws.data_ptr(), ws.numel(), nb,
+                                   _lib.stream_ptr()), "sfk_trace_compact")
+    n = int(n_out[0])
+    return ops[:n], keys[:n]
+
+
+def read_trace(path):
+    """Stream Operations out of a trace (the reference's generator
+    semantics: operations before a bad line are yielded, then it raises)."""
+    from .errors import TraceFormatError
+
+    try:
+        ops, keys = load_trace(path)
+        err = None
+    except TraceFormatError as e:  # parse the prefix before the bad line
+        err = e
+        with open(path, "r", encoding="utf-8") as fh:
+            prefix = [ln for _, ln in zip(range(e.line_number - 1), fh)]
+        pairs = [r for i, ln in enumerate(prefix, start=1) if (r := _trace_line(ln, i)) is not None]
+        ops = np.array([p[0] for p in pairs], dtype=np.uint8)
+        keys = np.array([p[1] for p in pairs], dtype=np.uint64)
+    ops_h = ops.cpu().numpy() if hasattr(ops, "cpu") else ops
+    keys_h = keys.cpu().numpy() if hasattr(keys, "cpu") else keys
+    for o, k in zip(ops_h, keys_h):
+        yield Operation("insert" if o == 0 else "delete", int(k))
+    if err is not None:
+        raise err
+
+
+def write_trace(path, operations) -> None:
+    """Write Operations in the trace format (LF line endings)."""
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        for operation in operations:
+            fh.write(f"{'I' if operation.op == 'insert' else 'D'},{operation.key}\n")
