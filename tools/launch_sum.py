@@ -1,3 +1,5 @@
+"""Sum an ncu --metrics gpu__time_duration.sum --csv launch list by kernel
+(ms per kernel, share, launches). Usage: python tools/launch_sum.py launches.csv"""
 import csv, sys, collections
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 hdr = rows[0]
@@ -6,7 +8,7 @@ agg = collections.OrderedDict()
 for r in rows[1:]:
     if r[mi] != "gpu__time_duration.sum": continue
     v = float(r[vi].replace(",", "")); u = r[ui]
-    ms = v / 1e6 if u == "nsecond" else v / 1e3 if u == "usecond" else v if u == "msecond" else v
+    ms = v / 1e6 if u in ("nsecond", "ns") else v / 1e3 if u in ("usecond", "us") else v if u in ("msecond", "ms") else v / 1e6
     k = r[ki][:90]
     a = agg.setdefault(k, [0.0, 0]); a[0] += ms; a[1] += 1
 tot = sum(a[0] for a in agg.values())
