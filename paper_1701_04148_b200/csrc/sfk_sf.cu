@@ -2626,13 +2626,15 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
     cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
     if (int r = run_scan_z<true, 4, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
-    { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     cudaMemcpyAsync(L.fat_snap, dsub, (size_t)D * w * 4, cudaMemcpyDeviceToDevice, st);
     ScanOut sd{L.fat_snap, dsub, nullptr, L.obs2, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
     if (int r = run_scan_z<true, 3, true>(1, L.k_out, L.v_out, N, 0, L.tiles, sd, st)) return r;
+    // both scans can find the failing op (the deletion sub-sketch its own
+    // phantom / saturation): undo both only once t* is final
+    { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     { note_launch(); fat_undo_k<D, 2><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hs, dsub, 1u); }
     if (int r = run_engine<D, 3>(L, slim, slim_seeds, w, ks, n, 0, inc, st, true)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
