@@ -72,3 +72,82 @@ def test_fuzz_against_oracle(oracle, kind, seed, sequential):
     assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat, o.dsub)
     q = np.unique(keys)[:2000]
     np.testing.assert_array_equal(host(sk.query_many(q)), o.query_many(q))
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fuzz_count_cml_oracle(oracle, seed):
+    """Count, CML and the oracle-assisted slim over random shapes, presets
+    (near the int32 / u16 / u32 bounds), bases, counts and batch splits."""
+    import paper_1701_04148_b200 as P
+
+    rng = np.random.default_rng(77_000 + seed)
+    d = int(rng.integers(1, 11))
+    w = int(rng.choice([8, 31, 64, 200, 1024]))
+    n = int(rng.integers(1, 30_000))
+    v = int(rng.integers(3, 2000))
+    keys = rng.integers(0, 1 << 40, size=v, dtype=np.uint64)[rng.integers(0, v, size=n)]
+    seeds = oracle.seed_array(seed, 0, d)
+    batches = int(rng.integers(1, 4))
+    bounds = np.linspace(0, n, batches + 1).astype(int)
+
+    def run(apply_o, apply_g):
+        want = (0, -1)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            st, oi, _ = apply_o(a, b)
+            if st:
+                want = (st, a + oi)
+                break
+        got = (0, -1)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            try:
+                apply_g(a, b)
+            except (P.SaturationError, P.UnsupportedOperationError, P.PhantomDeletionError) as e:
+                got = ({P.PhantomDeletionError: 1, P.SaturationError: 2, P.UnsupportedOperationError: 3}[type(e)],
+                       a + int(str(e).split(":")[0].split()[1]))
+                break
+        assert got == want
+
+    # Count
+    ops = (rng.random(n) < 0.3).astype(np.uint8)
+    c = np.zeros((d, w), np.int32)
+    if rng.random() < 0.4:
+        c[...] = rng.choice(np.array([2147483647 - 3, -2147483648 + 3, 0], np.int32), size=c.shape)
+    cs = P.CountSketch(P.SketchParams(d=d, w=w, master_seed=seed))
+    cs.counters.copy_(torch.from_numpy(c.copy()))
+    run(lambda a, b: oracle.count_apply(c, seeds, ops[a:b], keys[a:b]), lambda a, b: cs.apply_ops(ops[a:b], keys[a:b]))
+    np.testing.assert_array_equal(host(cs.counters), c)
+    np.testing.assert_array_equal(host(cs.query_many(keys[:500])), oracle.count_query(c, seeds, keys[:500]))
+    # CML
+    base = float(rng.choice([1.0001, 1.01, 1.08, 1.5, 3.0]))
+    ops_c = np.zeros(n, np.uint8)
+    if rng.random() < 0.2:
+        ops_c[int(rng.integers(0, n))] = 1
+    e = np.zeros((d, w), np.uint16)
+    if rng.random() < 0.4:
+        e[...] = rng.integers(0xFFF0, 0x10000, size=e.shape).astype(np.uint16)
+    ml = P.CmlSketch(P.SketchParams(d=d, w=w, master_seed=seed), base=base, rng_seed=seed * 3)
+    ml.exponents.copy_(torch.from_numpy(e.copy()))
+    seen = [0]
+
+    def cml_o(a, b):
+        r = oracle.cml_apply(e, seeds, ops_c[a:b], keys[a:b], base, seed * 3, seen[0])
+        seen[0] += r[2]
+        return r
+
+    run(cml_o, lambda a, b: ml.apply_ops(ops_c[a:b], keys[a:b]))
+    np.testing.assert_array_equal(host(ml.exponents), e)
+    assert ml.insertions_seen == seen[0]
+    # oracle-assisted
+    tc = rng.integers(-3, 40, size=n).astype(np.int64)
+    if rng.random() < 0.2:
+        tc[rng.integers(0, n, size=5)] = 1 << 40
+    slim = np.zeros((d, w), np.uint32)
+    if rng.random() < 0.3:
+        slim[...] = np.uint32(0xFFFFFFFF - int(rng.integers(0, 30)))
+    inc = np.zeros(d, np.int64)
+    sk = P.SfSketch(P.SketchParams(d=d, w=w, z=2, master_seed=seed), "sff")
+    sk.slim.counters.copy_(torch.from_numpy(slim.copy()))
+    run(lambda a, b: oracle.oracle_slim_apply(slim, seeds, keys[a:b], tc[a:b], inc),
+        lambda a, b: sk.oracle_assisted_apply(keys[a:b], tc[a:b]))
+    np.testing.assert_array_equal(host(sk.slim.counters), slim)
+    np.testing.assert_array_equal(host(sk.slim.increment_counts), inc)
