@@ -151,3 +151,61 @@ def test_fuzz_count_cml_oracle(oracle, seed):
         lambda a, b: sk.oracle_assisted_apply(keys[a:b], tc[a:b]))
     np.testing.assert_array_equal(host(sk.slim.counters), slim)
     np.testing.assert_array_equal(host(sk.slim.increment_counts), inc)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_query_paths(oracle, seed):
+    """min_query over random shapes, value distributions (small, around the
+    u16 code boundary 0xF800, up to 2^32 - 1), key kinds and every path the
+    shape allows (auto, L2, shared memory, cluster)."""
+    import ctypes
+
+    from paper_1701_04148_b200 import _lib
+
+    rng = np.random.default_rng(55_000 + seed)
+    d = int(rng.integers(1, 9))
+    w = int(rng.choice([1, 7, 1000, 12800, 40000, 65536, 100_003, 1 << 18]))
+    dist = rng.integers(0, 4)
+    if dist == 0:
+        c = rng.integers(0, 300, size=(d, w), dtype=np.uint64)
+    elif dist == 1:
+        c = rng.integers(0xF700, 0xF900, size=(d, w), dtype=np.uint64)
+    elif dist == 2:
+        c = rng.integers(0, 1 << 32, size=(d, w), dtype=np.uint64)
+    else:
+        c = np.where(rng.random((d, w)) < 0.01, rng.integers(60000, 1 << 32, size=(d, w), dtype=np.uint64),
+                     rng.integers(0, 2000, size=(d, w), dtype=np.uint64))
+    c = c.astype(np.uint32)
+    n = int(rng.choice([1, 33, 5000, 300_000, 2_500_000]))
+    kind = int(rng.integers(0, 3))
+    seeds = oracle.seed_array(seed, 0, d)
+    if kind == _lib.KEY_U32:
+        keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        ku = keys.astype(np.uint64)
+        kt, rec = torch.from_numpy(keys).cuda(), 0
+    elif kind == _lib.KEY_U64:
+        ku = rng.integers(0, np.iinfo(np.uint64).max, size=n, dtype=np.uint64)
+        kt, rec = torch.from_numpy(ku).cuda(), 0
+    else:
+        rec = int(rng.integers(1, 20))
+        recs = rng.integers(0, 256, size=(n, rec), dtype=np.uint8)
+        ku = oracle.keys_from_records(recs)
+        kt = torch.from_numpy(recs.reshape(-1)).cuda()
+    want = oracle.min_query(c, seeds, ku, threads=4)
+    ct = torch.from_numpy(c).cuda()
+    L = _lib.lib()
+    paths = [0, 1]
+    if w * d * 4 <= 200 * 1024:
+        paths.append(2)
+    if 2 <= d <= 8 and w * 2 <= 110 * 1024:
+        paths.append(3)
+    for path in paths:
+        prev = L.sfk_query_path(path)
+        try:
+            out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+            _lib.check(L.sfk_min_query(ct.data_ptr(), seeds.ctypes.data_as(ctypes.c_void_p), d, w, kt.data_ptr(), kind,
+                                       rec, n, out.data_ptr(), _lib.stream_ptr()), "sfk_min_query")
+            torch.cuda.synchronize()
+        finally:
+            L.sfk_query_path(prev)
+        np.testing.assert_array_equal(out.cpu().numpy(), want, err_msg=f"path {path}")
