@@ -1364,6 +1364,46 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
 #pragma unroll
           for (int q = 0; q < 8; ++q) cb[q] = __ldg(src + (size_t)w * 8 + q);
           const uint32_t cdb = __ldg(a.delbits + w);
+          {
+            // collapsed replay: while no delete binds, every row is
+            // max(its value at the word start, m), so only the scalar min
+            // moves (m += [m < cap] per insert); a delete must keep every
+            // row <= A_i + O_i + x. If one would bind, redo the word exactly.
+            int64_t capmin = INT64_MAX, cmc = INT64_MIN;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const int64_t cap = (int64_t)A[i] + (int64_t)O[i];
+              capmin = min(capmin, cap);
+              cmc = max(cmc, (int64_t)c[i] - cap);
+            }
+            uint32_t mm = k.m;
+            int32_t xx = (int32_t)k.x;
+            bool okc = true;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const uint4 v4 = cb[jj >> 2];
+              const uint32_t ob = (jj & 3) == 0 ? v4.x : (jj & 3) == 1 ? v4.y : (jj & 3) == 2 ? v4.z : v4.w;
+              if (!((cdb >> jj) & 1u)) {
+                xx += 1;
+                mm += mm < ob ? 1u : 0u;
+              } else {
+                xx -= 1;
+                okc = okc && (int64_t)mm - capmin <= (int64_t)xx && cmc <= (int64_t)xx;
+              }
+            }
+            if (okc) {
+#pragma unroll
+              for (int i = 0; i < D; ++i) {
+                const uint32_t nc = max(c[i], mm);
+                raised[i] += nc - c[i];
+                c[i] = nc;
+              }
+              k.m = mm;
+              k.x = (uint32_t)xx;
+              ++ws[3];
+              continue;
+            }
+          }
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
             const uint4 v4 = cb[jj >> 2];
@@ -1703,7 +1743,7 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
 // yet (a ready cell stays ready: nobody else writes it before this run); a
 // long run is replayed REPLAY_BUDGET ops per iteration.
 template <int D, int MODE>
-__global__ void __launch_bounds__(256) poll_engine_k(EngineArgs<D> a) {
+__global__ void __launch_bounds__(256, 1) poll_engine_k(EngineArgs<D> a) {
   __shared__ uint32_t lut[256];
   __shared__ uint8_t rlut[WMAX * 8 * 256];
   build_step_lut(lut);
