@@ -3,6 +3,8 @@ over random shapes (d 1..8, power-of-two and odd widths, z 1..8), random
 key skews, delete mixes that include never-inserted keys (phantoms), preset
 counter states near saturation, and several batches per stream."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -12,6 +14,8 @@ from gpu_util import apply_batches, assert_state_equal, host, make_sketch
 pytestmark = pytest.mark.gpu
 
 KINDS = ["sff", "sf4", "sf3", "sf2", "sf1", "cm", "cu"]
+# SFK_FUZZ_SEEDS scales every fuzz test (default 40 seeds each)
+SEEDS = int(os.environ.get("SFK_FUZZ_SEEDS", "40"))
 
 
 def random_case(rng, kind):
@@ -42,7 +46,7 @@ def random_case(rng, kind):
 
 
 @pytest.mark.parametrize("sequential", [False, True])
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(SEEDS))
 @pytest.mark.parametrize("kind", KINDS)
 def test_fuzz_against_oracle(oracle, kind, seed, sequential):
     if sequential and seed % 4:
@@ -74,7 +78,7 @@ def test_fuzz_against_oracle(oracle, kind, seed, sequential):
     np.testing.assert_array_equal(host(sk.query_many(q)), o.query_many(q))
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(SEEDS))
 def test_fuzz_count_cml_oracle(oracle, seed):
     """Count, CML and the oracle-assisted slim over random shapes, presets
     (near the int32 / u16 / u32 bounds), bases, counts and batch splits."""
@@ -153,7 +157,7 @@ def test_fuzz_count_cml_oracle(oracle, seed):
     np.testing.assert_array_equal(host(sk.slim.increment_counts), inc)
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(SEEDS))
 def test_fuzz_query_paths(oracle, seed):
     """min_query over random shapes, value distributions (small, around the
     u16 code boundary 0xF800, up to 2^32 - 1), key kinds and every path the
