@@ -208,6 +208,21 @@ int sfk_cml_query(const uint16_t* exps, const uint64_t* seeds, int d, int64_t w,
                   int key_kind, int rec_len, int64_t n, const int64_t* value_table, int64_t* out,
                   void* stream);
 
+/* Synthetic streams (workloads.generate, workloads.py:92-131) on the device.
+ * sfk_pcg64_draws: draws [offset, offset + n) of numpy's Generator(PCG64)
+ * stream given its seeded 128-bit state / increment (host: bit_generator
+ * .state), as random() doubles, or, with a device CDF of v entries, as
+ * Zipf ranks searchsorted(cdf, u, side="right"). sfk_interleave_deletions:
+ * _kernels.interleave_deletions (_kernels.py:427-467), one device thread
+ * (the walk is sequential). Keys are then sfk_mix_batch(ranks). */
+int sfk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t offset,
+                    int64_t n, const double* cdf, int64_t v, int64_t* ranks, double* uniforms,
+                    void* stream);
+size_t sfk_interleave_workspace_size(int64_t v);
+int sfk_interleave_deletions(const int64_t* candidates, const double* decide, const double* pick,
+                             double p, int64_t n, int64_t v, uint8_t* ops, int64_t* ranks,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 /* Trace ingestion (workloads.read_trace / load_trace, workloads.py:132-172):
  * "OP,key" text lines parsed on the device. Phase 1 fills per-line arrays
  * (device, nbytes + 1 entries each): line_pos (byte offset), status (0 blank

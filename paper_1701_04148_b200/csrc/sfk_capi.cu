@@ -72,6 +72,10 @@ int count_fast(int32_t* counters, const uint64_t* seeds, int d, int64_t w, const
                cudaStream_t st);
 int ext_query(int which, const void* table, const uint64_t* seeds, int d, int64_t w, KeySrc ks, int64_t n,
               const int64_t* vtab, int64_t* out, cudaStream_t st);
+int launch_pcg_uniform(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t offset, int64_t n,
+                       const double* cdf, int64_t v, int64_t* ranks, double* uout, cudaStream_t st);
+int launch_interleave(const int64_t* cand, const double* decide, const double* pick, double p, int64_t n, int64_t v,
+                      uint8_t* ops, int64_t* ranks, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t trace_workspace_size(int64_t nb);
 int trace_parse_lines(const uint8_t* txt, int64_t nb, int64_t* line_pos, uint8_t* status, uint8_t* lop, uint64_t* lkey,
                       int64_t* out_info, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -338,6 +342,27 @@ int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t 
     return parallel_apply(8, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr, ks, cnt, inc_counts, result,
                           workspace, workspace_bytes, st, &ext);
   });
+}
+
+// ---------------------------------------------------------------- synthetic streams
+int sfk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t offset, int64_t n,
+                    const double* cdf, int64_t v, int64_t* ranks, double* uniforms, void* stream) {
+  if (offset < 0 || n < 0 || (cdf && (v < 1 || !ranks)) || (!cdf && !uniforms)) {
+    set_error("sfk_pcg64_draws: bad arguments");
+    return 1;
+  }
+  return launch_pcg_uniform(state_hi, state_lo, inc_hi, inc_lo, offset, n, cdf, v, ranks, uniforms,
+                            (cudaStream_t)stream);
+}
+
+size_t sfk_interleave_workspace_size(int64_t v) { return (size_t)(v > 0 ? v : 1) * 3 * 8 + 3 * 256; }
+
+int sfk_interleave_deletions(const int64_t* candidates, const double* decide, const double* pick, double p,
+                             int64_t n, int64_t v, uint8_t* ops, int64_t* ranks, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  if (n < 0 || v < 1) { set_error("sfk_interleave_deletions: bad sizes"); return 1; }
+  return launch_interleave(candidates, decide, pick, p, n, v, ops, ranks, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- trace ingestion

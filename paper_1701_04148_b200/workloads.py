@@ -305,3 +305,139 @@ def write_trace(path, operations) -> None:
     with open(path, "w", encoding="utf-8", newline="\n") as fh:
         for operation in operations:
             fh.write(f"{'I' if operation.op == 'insert' else 'D'},{operation.key}\n")
+
+
+# ---------------------------------------------------------------- the reference's synthetic streams
+# workloads.WorkloadSpec / generate (workloads.py:46-131), drawn on the GPU:
+# the same seed gives the same ops / ranks / keys as the reference.
+KINDS = ("uniform", "zipf", "trace")
+DELETION_MODES = ("none", "reverse_order", "interleaved")
+
+
+class WorkloadSpec:
+    """What to generate (``workloads.py:46-73``), validated the same way."""
+
+    __slots__ = ("kind", "distinct_items", "total_ops", "zipf_skew", "seed", "deletion_mode", "delete_prob",
+                 "trace_path")
+
+    def __init__(self, kind, distinct_items=0, total_ops=0, zipf_skew=0.99, seed=0, deletion_mode="none",
+                 delete_prob=0.0, trace_path=None):
+        from .errors import ConfigurationError
+
+        for name, val in (("kind", kind), ("distinct_items", distinct_items), ("total_ops", total_ops),
+                          ("zipf_skew", zipf_skew), ("seed", seed), ("deletion_mode", deletion_mode),
+                          ("delete_prob", delete_prob), ("trace_path", trace_path)):
+            object.__setattr__(self, name, val)
+        if kind not in KINDS:
+            raise ConfigurationError(f"unknown workload kind {kind!r}")
+        if kind == "trace":
+            if not trace_path:
+                raise ConfigurationError("trace workloads need trace_path")
+            return
+        if distinct_items < 1:
+            raise ConfigurationError("distinct_items must be >= 1")
+        if total_ops < 0:
+            raise ConfigurationError("total_ops must be >= 0")
+        if kind == "zipf" and not zipf_skew > 0:
+            raise ConfigurationError("zipf_skew must be > 0")
+        if deletion_mode not in DELETION_MODES:
+            raise ConfigurationError(f"unknown deletion mode {deletion_mode!r}")
+        if deletion_mode == "interleaved" and not 0.0 <= delete_prob < 1.0:
+            raise ConfigurationError("interleaved delete_prob must lie in [0, 1)")
+
+    def __setattr__(self, name, value):
+        raise AttributeError("WorkloadSpec is immutable")
+
+
+class Workload:
+    """A materialised stream: ``ops`` (uint8), ``keys`` (uint64) and, for
+    synthetic streams, ``ranks`` (int64), as CUDA tensors."""
+
+    def __init__(self, spec, ops, keys, ranks=None):
+        self.spec = spec
+        self.ops = ops
+        self.keys = keys
+        self.ranks = ranks
+
+    def __len__(self):
+        return int(self.ops.shape[0])
+
+    def operations(self):
+        for op, key in zip(self.ops.cpu().numpy(), self.keys.cpu().numpy()):
+            yield Operation("insert" if op == 0 else "delete", int(key))
+
+
+def zipf_probabilities(v: int, skew: float) -> np.ndarray:
+    """P(rank r) proportional to 1/(r+1)**skew (``workloads.py:92-96``)."""
+    weights = 1.0 / np.power(np.arange(1, v + 1, dtype=np.float64), skew)
+    return weights / weights.sum()
+
+
+def generate(spec: WorkloadSpec) -> Workload:
+    """``workloads.generate`` (``workloads.py:106-131``) with the draws on the
+    GPU. Zipf ranks: the numpy PCG64 stream of ``spec.seed`` evaluated in
+    parallel on the device (``sfk_pcg64_draws``) and searched in the same
+    float64 CDF. Uniform ranks use numpy's bounded-integer sampler, whose
+    rejection loop makes stream positions data-dependent, so those draws come
+    from numpy on the host. The interleaved-deletion walk runs on the device
+    (one thread: every step depends on the live-item set)."""
+    import torch
+
+    from . import _lib
+    from ._ops import device
+
+    if spec.kind == "trace":
+        ops, keys = load_trace(spec.trace_path)
+        return Workload(spec, ops, keys)
+    dev = device()
+    L = _lib.lib()
+    n, v = int(spec.total_ops), int(spec.distinct_items)
+    rng = np.random.Generator(np.random.PCG64(spec.seed))
+    st = rng.bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    sh, sl, ih, il = st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64
+
+    def draws(offset, count, cdf=None):
+        if cdf is not None:
+            out = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+            _lib.check(L.sfk_pcg64_draws(sh, sl, ih, il, offset, count, cdf.data_ptr(), cdf.numel(), out.data_ptr(),
+                                         None, _lib.stream_ptr()), "sfk_pcg64_draws")
+        else:
+            out = torch.empty(max(count, 1), dtype=torch.float64, device=dev)
+            _lib.check(L.sfk_pcg64_draws(sh, sl, ih, il, offset, count, None, 0, None, out.data_ptr(),
+                                         _lib.stream_ptr()), "sfk_pcg64_draws")
+        return out[:count]
+
+    used = 0  # stream position after the candidate draws (zipf: one draw each)
+    if spec.kind == "uniform":
+        cand = torch.from_numpy(rng.integers(0, v, size=n, dtype=np.int64)).to(dev)
+    else:
+        cdf = np.cumsum(zipf_probabilities(v, spec.zipf_skew))
+        cdf[-1] = 1.0  # the reference's guard: every draw lands inside
+        cand = draws(0, n, torch.from_numpy(cdf).to(dev))
+        used = n
+    if spec.deletion_mode == "none":
+        ops = torch.zeros(n, dtype=torch.uint8, device=dev)
+        ranks = cand
+    elif spec.deletion_mode == "reverse_order":
+        ops = torch.cat([torch.zeros(n, dtype=torch.uint8, device=dev), torch.ones(n, dtype=torch.uint8, device=dev)])
+        ranks = torch.cat([cand, torch.flip(cand, [0])])
+    else:
+        if spec.kind == "uniform":
+            decide = torch.from_numpy(rng.random(n)).to(dev)
+            pick = torch.from_numpy(rng.random(n)).to(dev)
+        else:
+            decide = draws(used, n)
+            pick = draws(used + n, n)
+        ops = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        ranks = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        ws = torch.empty(int(L.sfk_interleave_workspace_size(v)), dtype=torch.uint8, device=dev)
+        _lib.check(L.sfk_interleave_deletions(cand.data_ptr(), decide.data_ptr(), pick.data_ptr(),
+                                              float(spec.delete_prob), n, v, ops.data_ptr(), ranks.data_ptr(),
+                                              ws.data_ptr(), ws.numel(), _lib.stream_ptr()), "sfk_interleave_deletions")
+        ops, ranks = ops[:n], ranks[:n]
+    keys = torch.empty(ranks.numel(), dtype=torch.uint64, device=dev)
+    if ranks.numel():
+        _lib.check(L.sfk_mix_batch(ranks.data_ptr(), ranks.numel(), keys.data_ptr(), _lib.stream_ptr()),
+                   "sfk_mix_batch")
+    return Workload(spec, ops, keys, ranks)
