@@ -3,7 +3,7 @@ a set of specs (build container only; imports /root/reference):
 
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden_workloads.py
 
-Writes tests/golden/workloads.npz: per case the spec fields and the
+Writes tests/golden/streams/workloads.npz: per case the spec fields and the
 reference's ops / ranks (its keys are finalize64 of the ranks).
 """
 
@@ -55,7 +55,8 @@ def main():
         assert np.array_equal(wl.keys, _finalize(wl.ranks))  # keys = finalize64(rank): not stored
         meta[name] = spec
     out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
-    np.savez_compressed(os.path.join(OUT, "workloads.npz"), **out)
+    os.makedirs(os.path.join(OUT, "streams"), exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, "streams", "workloads.npz"), **out)
     print({k: len(out[k + "_ops"]) for k in meta})
 
 

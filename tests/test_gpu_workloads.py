@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1701_04148_b200 import _lib, workloads as W  # noqa: E402
 
-FX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "workloads.npz")
+FX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "streams", "workloads.npz")
 
 
 def load():
