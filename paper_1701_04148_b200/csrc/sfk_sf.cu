@@ -56,8 +56,14 @@ constexpr uint32_t SHORT_RUN_MAX = SFK_SHORT_RUN_MAX;
 constexpr int SHORT_CAPS = 8;
 // engine run claiming: run ids per warp atomic, and how far ahead of a claim
 // the run records are prefetched into L2
-constexpr uint32_t CLAIM_POOL = 64;
-constexpr uint32_t CLAIM_PREFETCH = 16384;
+#ifndef SFK_CLAIM_POOL
+#define SFK_CLAIM_POOL 64
+#endif
+#ifndef SFK_CLAIM_PREFETCH
+#define SFK_CLAIM_PREFETCH 16384
+#endif
+constexpr uint32_t CLAIM_POOL = SFK_CLAIM_POOL;
+constexpr uint32_t CLAIM_PREFETCH = SFK_CLAIM_PREFETCH;
 
 static uint32_t engine_budget() {
   static int v = -1;
