@@ -218,6 +218,15 @@ int sfk_cml_query(const uint16_t* exps, const uint64_t* seeds, int d, int64_t w,
 int sfk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t offset,
                     int64_t n, const double* cdf, int64_t v, int64_t* ranks, double* uniforms,
                     void* stream);
+/* numpy's Generator.integers(0, v, dtype=int64) for 1 <= v <= 2^32 from the
+ * same stream: n samples starting at 64-bit draw offset64 (Lemire's method
+ * with rejection over the low-then-high 32-bit halves of each draw; accepted
+ * positions compacted in parallel). *next_offset64 (host) = the stream
+ * position after them (numpy drops a half-used 64-bit draw). */
+size_t sfk_pcg64_bounded_workspace_size(int64_t n, int64_t v);
+int sfk_pcg64_bounded(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t offset64,
+                      int64_t n, int64_t v, int64_t* out, int64_t* next_offset64, void* workspace,
+                      size_t workspace_bytes, void* stream);
 size_t sfk_interleave_workspace_size(int64_t v);
 int sfk_interleave_deletions(const int64_t* candidates, const double* decide, const double* pick,
                              double p, int64_t n, int64_t v, uint8_t* ops, int64_t* ranks,

@@ -43,6 +43,8 @@ EXPORTS = (
     "sfk_cml_apply",
     "sfk_cml_query",
     "sfk_pcg64_draws",
+    "sfk_pcg64_bounded_workspace_size",
+    "sfk_pcg64_bounded",
     "sfk_interleave_workspace_size",
     "sfk_interleave_deletions",
     "sfk_trace_workspace_size",
@@ -108,6 +110,9 @@ def load_library() -> ctypes.CDLL:
     L.sfk_cml_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P, P]
     U64 = ctypes.c_uint64
     L.sfk_pcg64_draws.argtypes = [U64, U64, U64, U64, I64, I64, P, I64, P, P, P]
+    L.sfk_pcg64_bounded_workspace_size.argtypes = [I64, I64]
+    L.sfk_pcg64_bounded_workspace_size.restype = SZ
+    L.sfk_pcg64_bounded.argtypes = [U64, U64, U64, U64, I64, I64, I64, P, P, P, SZ, P]
     L.sfk_interleave_workspace_size.argtypes = [I64]
     L.sfk_interleave_workspace_size.restype = SZ
     L.sfk_interleave_deletions.argtypes = [P, P, P, ctypes.c_double, I64, I64, P, P, P, SZ, P]

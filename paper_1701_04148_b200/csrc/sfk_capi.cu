@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cmath>
 
 #include "sfk_common.cuh"
 
@@ -74,6 +75,9 @@ int ext_query(int which, const void* table, const uint64_t* seeds, int d, int64_
               const int64_t* vtab, int64_t* out, cudaStream_t st);
 int launch_pcg_uniform(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t offset, int64_t n,
                        const double* cdf, int64_t v, int64_t* ranks, double* uout, cudaStream_t st);
+size_t pcg_bounded_workspace_size(int64_t n, int64_t v);
+int launch_pcg_bounded(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t offset64, int64_t n, int64_t v,
+                       int64_t* out, int64_t* next_offset64, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_interleave(const int64_t* cand, const double* decide, const double* pick, double p, int64_t n, int64_t v,
                       uint8_t* ops, int64_t* ranks, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t trace_workspace_size(int64_t nb);
@@ -353,6 +357,22 @@ int sfk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint6
   }
   return launch_pcg_uniform(state_hi, state_lo, inc_hi, inc_lo, offset, n, cdf, v, ranks, uniforms,
                             (cudaStream_t)stream);
+}
+
+size_t sfk_pcg64_bounded_workspace_size(int64_t n, int64_t v) {
+  if (n < 0 || v < 1 || v > ((int64_t)1 << 32)) return 256;
+  return pcg_bounded_workspace_size(n, v);
+}
+
+int sfk_pcg64_bounded(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t offset64,
+                      int64_t n, int64_t v, int64_t* out, int64_t* next_offset64, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (n < 0 || v < 1 || v > ((int64_t)1 << 32) || !next_offset64) {
+    set_error("sfk_pcg64_bounded: bad arguments (1 <= v <= 2^32)");
+    return 1;
+  }
+  return launch_pcg_bounded(state_hi, state_lo, inc_hi, inc_lo, offset64, n, v, out, next_offset64, workspace,
+                            workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t sfk_interleave_workspace_size(int64_t v) { return (size_t)(v > 0 ? v : 1) * 3 * 8 + 3 * 256; }

@@ -2,6 +2,8 @@
 // launch counter. The generator is the counter-based construction of
 // paper_1701_04148_b200.workloads.query_keys, evaluated on the GPU so a
 // 1B-key batch never crosses PCIe; both sides produce identical keys.
+#include <cub/cub.cuh>
+
 #include "sfk_common.cuh"
 
 namespace sfk {
@@ -120,6 +122,117 @@ int launch_pcg_uniform(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64
   const int64_t nchunks = (n + PCG_CHUNK - 1) / PCG_CHUNK;
   { note_launch(); pcg_uniform_k<<<grid_for(nchunks, 128, sm_count() * 16), 128, 0, st>>>(sh, sl, ih, il, offset, n, cdf, v, ranks, uout); }
   return check_launch("pcg_uniform");
+}
+
+// numpy's Generator.integers(0, v) for int64 (v <= 2^32): 32-bit draws taken
+// from each 64-bit output low half first, Lemire's method with rejection
+// (a draw u is accepted iff (u * v) mod 2^32 >= (2^32 - v) mod v; the value
+// is (u * v) >> 32). Acceptance depends on the draw alone, so sample i is the
+// i-th accepted 32-bit position: flag every position in parallel, compact.
+__global__ void pcg_bounded_flags_k(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t offset64, int64_t k32,
+                                    uint32_t v, uint32_t thr, uint8_t* __restrict__ flag, int64_t* __restrict__ val) {
+  const u128 s0 = ((u128)sh << 64) | sl, inc = ((u128)ih << 64) | il;
+  const int64_t n64 = (k32 + 1) / 2;
+  const int64_t nchunks = (n64 + PCG_CHUNK - 1) / PCG_CHUNK;
+  for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
+       ch += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = ch * PCG_CHUNK, b = min(n64, a + PCG_CHUNK);
+    u128 st = pcg_advance(s0, inc, (uint64_t)(offset64 + a));
+    const u128 M = pcg_mult();
+    for (int64_t d = a; d < b; ++d) {
+      st = st * M + inc;
+      const uint64_t o = pcg_out(st);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t pos = 2 * d + h;
+        if (pos >= k32) break;
+        const uint32_t u = (uint32_t)(h ? (o >> 32) : o);
+        if (v == 0) {  // v = 2^32: numpy returns the raw 32-bit draw
+          flag[pos] = 1;
+          val[pos] = (int64_t)u;
+        } else {
+          const uint64_t m = (uint64_t)u * (uint64_t)v;
+          flag[pos] = (uint32_t)m >= thr ? 1 : 0;
+          val[pos] = (int64_t)(m >> 32);
+        }
+      }
+    }
+  }
+}
+
+// 32-bit draws needed for n samples: the expected count n / (1 - thr / 2^32)
+// plus 10 standard deviations (a shortfall is reported, never truncated)
+int64_t pcg_bounded_window(int64_t n, int64_t v) {
+  const double p = (double)((0x100000000ull - (uint64_t)v) % (uint64_t)v) / 4294967296.0;
+  const double e = (double)n / (1.0 - p);
+  return (int64_t)(e + 10.0 * sqrt(e + 1.0)) + 64;
+}
+
+static size_t bounded_tmp_bytes(int64_t k32) {
+  size_t a = 0, b = 0;
+  cub::DeviceSelect::Flagged(nullptr, a, (const int64_t*)nullptr, (const uint8_t*)nullptr, (int64_t*)nullptr,
+                             (int64_t*)nullptr, k32);
+  cub::DeviceSelect::Flagged(nullptr, b, cub::CountingInputIterator<int64_t>(0), (const uint8_t*)nullptr,
+                             (int64_t*)nullptr, (int64_t*)nullptr, k32);
+  return std::max(a, b);
+}
+
+size_t pcg_bounded_workspace_size(int64_t n, int64_t v) {
+  const int64_t k32 = pcg_bounded_window(n, v);
+  Carver cv(nullptr, ~size_t(0));
+  cv.take<uint8_t>((size_t)k32);
+  cv.take<int64_t>((size_t)k32);
+  cv.take<int64_t>((size_t)k32);
+  cv.take<int64_t>((size_t)k32);
+  cv.take<int64_t>(2);
+  cv.take<char>(bounded_tmp_bytes(k32));
+  return cv.off + 256;
+}
+
+int launch_pcg_bounded(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t offset64, int64_t n, int64_t v,
+                       int64_t* out, int64_t* next_offset64, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0) { *next_offset64 = offset64; return 0; }
+  if (v == 1) {  // numpy's range 0: no draws, all zeros
+    cudaMemsetAsync(out, 0, (size_t)n * 8, st);
+    *next_offset64 = offset64;
+    return check_launch("pcg_bounded");
+  }
+  const uint32_t vv = (uint32_t)v;  // 0 encodes v = 2^32 (raw draws)
+  const uint32_t thr = (uint32_t)((0x100000000ull - (uint64_t)v) % (uint64_t)v);
+  const int64_t k32 = pcg_bounded_window(n, v);
+  Carver cv(ws, ws_bytes);
+  uint8_t* flag = cv.take<uint8_t>((size_t)k32);
+  int64_t* val = cv.take<int64_t>((size_t)k32);
+  int64_t* acc = cv.take<int64_t>((size_t)k32);
+  int64_t* pos = cv.take<int64_t>((size_t)k32);
+  int64_t* sel = cv.take<int64_t>(2);
+  const size_t tb = bounded_tmp_bytes(k32);
+  void* tmp = cv.take<char>(tb);
+  if (!cv.ok || ws == nullptr) {
+    set_error("bounded draws: workspace too small (need %zu bytes)", cv.off + 256);
+    return 1;
+  }
+  const int64_t n64 = (k32 + 1) / 2, nchunks = (n64 + PCG_CHUNK - 1) / PCG_CHUNK;
+  { note_launch(); pcg_bounded_flags_k<<<grid_for(nchunks, 128, sm_count() * 16), 128, 0, st>>>(sh, sl, ih, il, offset64, k32, vv, thr, flag, val); }
+  size_t b1 = tb;
+  if (cub::DeviceSelect::Flagged(tmp, b1, val, flag, acc, sel, k32, st) != cudaSuccess) return 1;
+  b1 = tb;
+  if (cub::DeviceSelect::Flagged(tmp, b1, cub::CountingInputIterator<int64_t>(0), flag, pos, sel + 1, k32, st) !=
+      cudaSuccess)
+    return 1;
+  int64_t h[2];
+  cudaMemcpyAsync(h, sel, 16, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("bounded draws: sync failed"); return 1; }
+  if (h[0] < n) {
+    set_error("bounded draws: %lld accepted of %lld needed in the window", (long long)h[0], (long long)n);
+    return 1;
+  }
+  cudaMemcpyAsync(out, acc, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
+  int64_t last = 0;
+  cudaMemcpyAsync(&last, pos + (n - 1), 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("bounded draws: sync failed"); return 1; }
+  *next_offset64 = offset64 + (last + 2) / 2;  // 32-bit draws used: last + 1; a half-used 64-bit draw is dropped
+  return check_launch("pcg_bounded");
 }
 
 // _kernels.interleave_deletions (_kernels.py:427-467): a sequential walk over

@@ -377,9 +377,10 @@ def generate(spec: WorkloadSpec) -> Workload:
     """``workloads.generate`` (``workloads.py:106-131``) with the draws on the
     GPU. Zipf ranks: the numpy PCG64 stream of ``spec.seed`` evaluated in
     parallel on the device (``sfk_pcg64_draws``) and searched in the same
-    float64 CDF. Uniform ranks use numpy's bounded-integer sampler, whose
-    rejection loop makes stream positions data-dependent, so those draws come
-    from numpy on the host. The interleaved-deletion walk runs on the device
+    float64 CDF. Uniform ranks follow numpy's bounded-integer sampler
+    (Lemire with rejection): acceptance depends only on each 32-bit draw, so
+    the accepted positions are flagged and compacted in parallel
+    (``sfk_pcg64_bounded``). The interleaved-deletion walk runs on the device
     (one thread: every step depends on the live-item set)."""
     import torch
 
@@ -408,9 +409,15 @@ def generate(spec: WorkloadSpec) -> Workload:
                                          _lib.stream_ptr()), "sfk_pcg64_draws")
         return out[:count]
 
-    used = 0  # stream position after the candidate draws (zipf: one draw each)
+    used = 0  # stream position (64-bit draws) after the candidate draws
     if spec.kind == "uniform":
-        cand = torch.from_numpy(rng.integers(0, v, size=n, dtype=np.int64)).to(dev)
+        cand = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        ws = torch.empty(int(L.sfk_pcg64_bounded_workspace_size(n, v)), dtype=torch.uint8, device=dev)
+        nxt = np.zeros(1, dtype=np.int64)
+        _lib.check(L.sfk_pcg64_bounded(sh, sl, ih, il, 0, n, v, cand.data_ptr(), nxt.ctypes.data, ws.data_ptr(),
+                                       ws.numel(), _lib.stream_ptr()), "sfk_pcg64_bounded")
+        cand = cand[:n]
+        used = int(nxt[0])
     else:
         cdf = np.cumsum(zipf_probabilities(v, spec.zipf_skew))
         cdf[-1] = 1.0  # the reference's guard: every draw lands inside
@@ -423,12 +430,8 @@ def generate(spec: WorkloadSpec) -> Workload:
         ops = torch.cat([torch.zeros(n, dtype=torch.uint8, device=dev), torch.ones(n, dtype=torch.uint8, device=dev)])
         ranks = torch.cat([cand, torch.flip(cand, [0])])
     else:
-        if spec.kind == "uniform":
-            decide = torch.from_numpy(rng.random(n)).to(dev)
-            pick = torch.from_numpy(rng.random(n)).to(dev)
-        else:
-            decide = draws(used, n)
-            pick = draws(used + n, n)
+        decide = draws(used, n)
+        pick = draws(used + n, n)
         ops = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
         ranks = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         ws = torch.empty(int(L.sfk_interleave_workspace_size(v)), dtype=torch.uint8, device=dev)

@@ -45,3 +45,25 @@ def test_pcg64_draws_equal_numpy(seed, offset, n):
                                           offset, n, None, 0, None, out.data_ptr(), _lib.stream_ptr()), "draws")
     g.bit_generator.advance(offset)
     np.testing.assert_array_equal(out.cpu().numpy(), g.random(n))
+
+
+@pytest.mark.parametrize("seed,v,n,skip", [(6, 777, 30_000, 0), (1, 1, 100, 0), (3, 2**31 + 1, 50_000, 0),
+                                           (4, 2**32, 1000, 0), (5, 1_000_003, 200_000, 12345), (8, 3, 1, 0)])
+def test_pcg64_bounded_equal_numpy(seed, v, n, skip):
+    """Generator.integers(0, v, dtype=int64) from the device, including the
+    stream position it leaves (checked through the next random() draws)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    st = g.bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    L = _lib.lib()
+    out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(L.sfk_pcg64_bounded_workspace_size(n, v)), dtype=torch.uint8, device="cuda")
+    nxt = np.zeros(1, dtype=np.int64)
+    _lib.check(L.sfk_pcg64_bounded(st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64, skip, n, v,
+                                   out.data_ptr(), nxt.ctypes.data, ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+               "bounded")
+    g.bit_generator.advance(skip)
+    np.testing.assert_array_equal(out[:n].cpu().numpy(), g.integers(0, v, size=n, dtype=np.int64))
+    h = np.random.Generator(np.random.PCG64(seed))
+    h.bit_generator.advance(int(nxt[0]))
+    np.testing.assert_array_equal(h.random(4), g.random(4))
