@@ -24,6 +24,14 @@
 
 #include "sfk_common.cuh"
 
+// cluster query kernel shape: threads per CTA and keys per tile (u16 rows)
+#ifndef SFK_QUERY_NT
+#define SFK_QUERY_NT 512
+#endif
+#ifndef SFK_QUERY_TILE
+#define SFK_QUERY_TILE 8192
+#endif
+
 namespace sfk {
 
 template <int D, int UNR>
@@ -517,7 +525,7 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
 template <int D, typename CT, int TILE, int KK, bool VEC, bool POW2>
 static int try_cluster_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
                          int64_t* out, cudaStream_t st, int optin) {
-  constexpr int NT = 512;
+  constexpr int NT = SFK_QUERY_NT;
   constexpr int Q = ((TILE + D - 1) / D + 3) & ~3;
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
   const size_t smem = row_bytes + (sizeof(CT) == 2 ? 2 * OVF_STRIDE * 4 : 0) + (size_t)QNB * D * Q * sizeof(CT) +
@@ -642,7 +650,7 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
     if ((size_t)w * 4 + 2 * 8192 * 4 + 64 + 1024 <= (size_t)optin)
       rc = try_cluster<D, uint32_t, 8192>(counters, sd, wm, w, ks, n, out, st, optin);
     else
-      rc = try_cluster<D, uint16_t, 8192>(counters, sd, wm, w, ks, n, out, st, optin);
+      rc = try_cluster<D, uint16_t, SFK_QUERY_TILE>(counters, sd, wm, w, ks, n, out, st, optin);
     if (rc >= 0) return rc;
   }
   int blocks = grid_for(n, 256 * 4, sms * 8);
