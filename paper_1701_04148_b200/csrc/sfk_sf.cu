@@ -56,6 +56,14 @@ constexpr uint32_t SHORT_RUN_MAX = SFK_SHORT_RUN_MAX;
 constexpr int SHORT_CAPS = 8;
 // engine run claiming: run ids per warp atomic, and how far ahead of a claim
 // the run records are prefetched into L2
+// poll-loop backoff: a warp that made no progress for SFK_IDLE_SPINS
+// iterations sleeps up to SFK_IDLE_MAX_NS (0: never sleeps)
+#ifndef SFK_IDLE_SPINS
+#define SFK_IDLE_SPINS 4
+#endif
+#ifndef SFK_IDLE_MAX_NS
+#define SFK_IDLE_MAX_NS 0
+#endif
 #ifndef SFK_CLAIM_POOL
 #define SFK_CLAIM_POOL 64
 #endif
@@ -1916,8 +1924,8 @@ __global__ void __launch_bounds__(256, 1) poll_engine_k(EngineArgs<D> a) {
     }
     if (__any_sync(0xffffffffu, progressed)) {
       idle = 0;
-    } else if (++idle > 4) {
-      __nanosleep(min(idle * 4u, 32u));
+    } else if (++idle > SFK_IDLE_SPINS) {
+      if (SFK_IDLE_MAX_NS) __nanosleep(min(idle * 4u, (uint32_t)SFK_IDLE_MAX_NS));
     }
   }
 #pragma unroll
