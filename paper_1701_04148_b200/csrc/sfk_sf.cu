@@ -58,6 +58,10 @@ constexpr int SHORT_CAPS = 8;
 // the run records are prefetched into L2
 // poll-loop backoff: a warp that made no progress for SFK_IDLE_SPINS
 // iterations sleeps up to SFK_IDLE_MAX_NS (0: never sleeps)
+// engine lanes per SM: threads of its one block per SM (warp multiple)
+#ifndef SFK_ENGINE_THREADS
+#define SFK_ENGINE_THREADS 256
+#endif
 #ifndef SFK_IDLE_SPINS
 #define SFK_IDLE_SPINS 4
 #endif
@@ -1757,7 +1761,7 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
 // yet (a ready cell stays ready: nobody else writes it before this run); a
 // long run is replayed REPLAY_BUDGET ops per iteration.
 template <int D, int MODE>
-__global__ void __launch_bounds__(256, 1) poll_engine_k(EngineArgs<D> a) {
+__global__ void __launch_bounds__(SFK_ENGINE_THREADS, 1) poll_engine_k(EngineArgs<D> a) {
   __shared__ uint32_t lut[256];
   __shared__ uint8_t rlut[WMAX * 8 * 256];
   build_step_lut(lut);
@@ -2503,7 +2507,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
     ea.trace = g_trace;
   }
   if (g_time_engine) cudaEventRecord(g_ev[0], st);
-  { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), 256, 0, st>>>(ea); }
+  { note_launch(); poll_engine_k<D, MODE><<<sms * engine_blocks_per_sm(), SFK_ENGINE_THREADS, 0, st>>>(ea); }
   if (g_time_engine) {
     cudaEventRecord(g_ev[1], st);
     g_ev_pending = true;
