@@ -1422,28 +1422,36 @@ __device__ __forceinline__ bool replay_step(const EngineArgs<D>& a, Cursor& k, u
               continue;
             }
           }
+          {
+            // exact replay, branch-light 32-bit form: a delete's cap
+            // A_i + O_i + x is a count (0 .. 2^32 - 1), so modular u32 math is exact
+            uint32_t T[D];
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const uint4 v4 = cb[jj >> 2];
-            const uint32_t ob = (jj & 3) == 0 ? v4.x : (jj & 3) == 1 ? v4.y : (jj & 3) == 2 ? v4.z : v4.w;
-            if (!((cdb >> jj) & 1u)) {
-              k.x += 1u;
-              if (k.m < ob) {
+            for (int i = 0; i < D; ++i) T[i] = A[i] + O[i];
 #pragma unroll
-                for (int i = 0; i < D; ++i)
-                  if (c[i] == k.m) c[i] += 1u, raised[i] += 1u;
-                k.m += 1u;
+            for (int jj = 0; jj < 32; ++jj) {
+              const uint4 v4 = cb[jj >> 2];
+              const uint32_t ob = (jj & 3) == 0 ? v4.x : (jj & 3) == 1 ? v4.y : (jj & 3) == 2 ? v4.z : v4.w;
+              if (!((cdb >> jj) & 1u)) {
+                k.x += 1u;
+                const uint32_t up = k.m < ob ? 1u : 0u;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                  const uint32_t r = (c[i] == k.m) ? up : 0u;
+                  c[i] += r;
+                  raised[i] += r;
+                }
+                k.m += up;
+              } else {
+                k.x -= 1u;
+                uint32_t m = U32MAX;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                  c[i] -= c[i] > T[i] + k.x ? 1u : 0u;
+                  m = min(m, c[i]);
+                }
+                k.m = m;
               }
-            } else {
-              k.x -= 1u;
-              uint32_t m = U32MAX;
-#pragma unroll
-              for (int i = 0; i < D; ++i) {
-                const int64_t T = (int64_t)A[i] + (int64_t)(int32_t)k.x + (int64_t)O[i];
-                if ((int64_t)c[i] > T) c[i] -= 1u;
-                m = min(m, c[i]);
-              }
-              k.m = m;
             }
           }
         }
