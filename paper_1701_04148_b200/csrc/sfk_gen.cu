@@ -243,35 +243,136 @@ __global__ void interleave_k(const int64_t* __restrict__ cand, const double* __r
                              int64_t* __restrict__ ranks) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   int64_t npos = 0, cur = 0;
-  for (int64_t t = 0; t < n; ++t) {
-    if (decide[t] < p && npos > 0) {
-      int64_t slot = (int64_t)(pick[t] * (double)npos);
-      if (slot >= npos) slot = npos - 1;
-      const int64_t r = poslist[slot];
-      ops[t] = 1;
-      ranks[t] = r;
-      if (--counts[r] == 0) {
-        const int64_t last = poslist[npos - 1];
-        poslist[slot] = last;
-        posindex[last] = slot;
-        posindex[r] = -1;
-        --npos;
-      }
-    } else {
-      const int64_t r = cand[cur++];
-      ops[t] = 0;
-      ranks[t] = r;
-      if (++counts[r] == 1) {
-        poslist[npos] = r;
-        posindex[r] = npos;
-        ++npos;
+  constexpr int B = 8;  // decide / pick / candidate draws loaded B at a time
+  for (int64_t t0 = 0; t0 < n; t0 += B) {
+    double dd[B], pp[B];
+    int64_t cc[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      dd[q] = t0 + q < n ? __ldg(decide + t0 + q) : 1.0;
+      pp[q] = t0 + q < n ? __ldg(pick + t0 + q) : 0.0;
+      cc[q] = cur + q < n ? __ldg(cand + cur + q) : 0;
+    }
+    int used = 0;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int64_t t = t0 + q;
+      if (t >= n) break;
+      if (dd[q] < p && npos > 0) {
+        int64_t slot = (int64_t)(pp[q] * (double)npos);
+        if (slot >= npos) slot = npos - 1;
+        const int64_t r = poslist[slot];
+        ops[t] = 1;
+        ranks[t] = r;
+        if (--counts[r] == 0) {
+          const int64_t last = poslist[npos - 1];
+          poslist[slot] = last;
+          posindex[last] = slot;
+          posindex[r] = -1;
+          --npos;
+        }
+      } else {
+        int64_t r = cc[0];
+#pragma unroll
+        for (int u = 1; u < B; ++u)
+          if (u == used) r = cc[u];
+        ++used;
+        ops[t] = 0;
+        ranks[t] = r;
+        if (++counts[r] == 1) {
+          poslist[npos] = r;
+          posindex[r] = npos;
+          ++npos;
+        }
       }
     }
+    cur += used;
+  }
+}
+
+// the same walk with the live-item tables in shared memory (v small enough):
+// each step's table accesses cost shared-memory latency instead of L2's
+__global__ void __launch_bounds__(256) interleave_smem_k(const int64_t* __restrict__ cand,
+                                                         const double* __restrict__ decide,
+                                                         const double* __restrict__ pick, double p, int64_t n,
+                                                         int32_t v, uint8_t* __restrict__ ops,
+                                                         int64_t* __restrict__ ranks) {
+  extern __shared__ int32_t tab[];
+  int32_t* counts = tab;
+  int32_t* poslist = tab + v;
+  int32_t* posindex = tab + 2 * v;
+  for (int32_t r = threadIdx.x; r < v; r += blockDim.x) counts[r] = 0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int32_t npos = 0;
+  int64_t cur = 0;
+  constexpr int B = 8;  // decide / pick / candidate draws loaded B at a time
+  for (int64_t t0 = 0; t0 < n; t0 += B) {
+    double dd[B], pp[B];
+    int64_t cc[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      dd[q] = t0 + q < n ? __ldg(decide + t0 + q) : 1.0;
+      pp[q] = t0 + q < n ? __ldg(pick + t0 + q) : 0.0;
+      cc[q] = cur + q < n ? __ldg(cand + cur + q) : 0;
+    }
+    int used = 0;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int64_t t = t0 + q;
+      if (t >= n) break;
+      if (dd[q] < p && npos > 0) {
+        int64_t slot = (int64_t)(pp[q] * (double)npos);
+        if (slot >= npos) slot = npos - 1;
+        const int32_t r = poslist[slot];
+        ops[t] = 1;
+        ranks[t] = r;
+        if (--counts[r] == 0) {
+          const int32_t last = poslist[npos - 1];
+          poslist[slot] = last;
+          posindex[last] = (int32_t)slot;
+          posindex[r] = -1;
+          --npos;
+        }
+      } else {
+        // the next candidate: one of the B prefetched (inserts consume them in order)
+        int64_t rr = cc[0];
+#pragma unroll
+        for (int u = 1; u < B; ++u)
+          if (u == used) rr = cc[u];
+        ++used;
+        const int32_t r = (int32_t)rr;
+        ops[t] = 0;
+        ranks[t] = r;
+        if (++counts[r] == 1) {
+          poslist[npos] = r;
+          posindex[r] = npos;
+          ++npos;
+        }
+      }
+    }
+    cur += used;
   }
 }
 
 int launch_interleave(const int64_t* cand, const double* decide, const double* pick, double p, int64_t n, int64_t v,
                       uint8_t* ops, int64_t* ranks, void* ws, size_t ws_bytes, cudaStream_t st) {
+  {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t smem = (size_t)v * 3 * 4;
+    if (v < (int64_t)1 << 30 && smem + 1024 <= (size_t)optin) {
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(interleave_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+              cudaSuccess) {
+        cudaGetLastError();
+      } else {
+        if (n > 0) { note_launch(); interleave_smem_k<<<1, 256, smem, st>>>(cand, decide, pick, p, n, (int32_t)v, ops, ranks); }
+        return check_launch("interleave_smem");
+      }
+    }
+  }
   Carver cv(ws, ws_bytes);
   int64_t* counts = cv.take<int64_t>((size_t)v);
   int64_t* poslist = cv.take<int64_t>((size_t)v);
