@@ -59,6 +59,9 @@ constexpr int SHORT_CAPS = 8;
 // poll-loop backoff: a warp that made no progress for SFK_IDLE_SPINS
 // iterations sleeps up to SFK_IDLE_MAX_NS (0: never sleeps)
 // engine lanes per SM: threads of its one block per SM (warp multiple)
+#ifndef SFK_RUNREC_ALIGN
+#define SFK_RUNREC_ALIGN alignas(32)
+#endif
 #ifndef SFK_ENGINE_THREADS
 #define SFK_ENGINE_THREADS 256
 #endif
@@ -710,7 +713,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
 // must wait for) and, for SFF, the key's own slot count before the run (A)
 // and the maximum of the other slots of the bucket (O) in every row.
 template <int D>
-struct RunRec {
+struct SFK_RUNREC_ALIGN RunRec {  // whole 32-B sectors (full-sector stores, vector loads)
   uint32_t e0, info;
   uint32_t bits0;  // SFF: delete flags of the run's first 32 ops
   uint32_t cells[D];
@@ -2174,6 +2177,19 @@ struct Layout {
 // trigger), 5 SF3 (fold groups as buckets), 6 SF2 (flat fat + deletion sub-sketch),
 // 7 CML (u16 exponents widened into fat_snap), 8 oracle-assisted slim
 // (7 and 8: insert-only gated min-raise with a per-op gate, op-by-op replay)
+static uint64_t runrec_bytes(int d) {
+  switch (d) {
+    case 1: return sizeof(RunRec<1>);
+    case 2: return sizeof(RunRec<2>);
+    case 3: return sizeof(RunRec<3>);
+    case 4: return sizeof(RunRec<4>);
+    case 5: return sizeof(RunRec<5>);
+    case 6: return sizeof(RunRec<6>);
+    case 7: return sizeof(RunRec<7>);
+    default: return sizeof(RunRec<8>);
+  }
+}
+
 static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
   Carver cv(base, cap);
   Layout L{};
@@ -2234,7 +2250,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
     L.ign = cv.take<uint8_t>(sf1 ? N : 1);
     L.ftiles = cv.take<char>(sf1 ? ((N + SCAN_TILE - 1) / SCAN_TILE + 1) * 16 : 1);
   }
-  L.recs = cv.take<char>(engine ? (uint64_t)n * (12 + 16 * (uint64_t)d) : 1);
+  L.recs = cv.take<char>(engine ? (uint64_t)n * runrec_bytes(d) : 1);
   L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
   L.zops = cv.take<uint8_t>(kind == 8 ? (uint64_t)n : 1);
   L.omax0 = cv.take<uint32_t>(gated ? n / 32 + 2 : 1);
