@@ -59,6 +59,11 @@ constexpr int SHORT_CAPS = 8;
 // poll-loop backoff: a warp that made no progress for SFK_IDLE_SPINS
 // iterations sleeps up to SFK_IDLE_MAX_NS (0: never sleeps)
 // engine lanes per SM: threads of its one block per SM (warp multiple)
+// link records are written once and read back in other passes: streaming
+// (evict-first) stores keep them from displacing the scans' working sets in L2
+#ifndef SFK_LINKS_STREAMING
+#define SFK_LINKS_STREAMING 1
+#endif
 #ifndef SFK_RUNREC_ALIGN
 #define SFK_RUNREC_ALIGN alignas(32)
 #endif
@@ -416,8 +421,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
       // a sector written at another time costs L2 a DRAM fill.
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
       uint4* rec = reinterpret_cast<uint4*>(o.links) + ((size_t)t * o.D + row) * 2;
+#if SFK_LINKS_STREAMING
+      __stcs(rec, make_uint4(e - run.head, prev, rec_own, rec_oth));
+      __stcs(rec + 1, make_uint4(c, e, 0u, 0u));
+#else
       rec[0] = make_uint4(e - run.head, prev, rec_own, rec_oth);
       rec[1] = make_uint4(c, e, 0u, 0u);
+#endif
     }
     prev_t = t;
   }
@@ -598,12 +608,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
     const SegCnt el = segcnt_elem(keys, vals, ign, e);
     const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
     uint4* rec = links + ((size_t)t * D + row) * 2;
-    if (ign[e]) {
-      rec[0] = make_uint4(0u, IGN_MARK, 0u, 0u);
-    } else {
-      rec[0] = make_uint4(before.cnt, before.last, 0u, 0u);
-    }
+    const uint4 r0 = ign[e] ? make_uint4(0u, IGN_MARK, 0u, 0u) : make_uint4(before.cnt, before.last, 0u, 0u);
+#if SFK_LINKS_STREAMING
+    __stcs(rec, r0);
+    __stcs(rec + 1, make_uint4(c, e, 0u, 0u));
+#else
+    rec[0] = r0;
     rec[1] = make_uint4(c, e, 0u, 0u);
+#endif
     run = op(run, el);
   }
 }
