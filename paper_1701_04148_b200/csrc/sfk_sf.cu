@@ -806,7 +806,16 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
         rec.O[i] = 0;
       }
     }
+#if SFK_LINKS_STREAMING
+    {  // whole sectors, streaming: read back by the engine (prefetched ahead)
+      const uint4* src = reinterpret_cast<const uint4*>(&rec);
+      uint4* dst = reinterpret_cast<uint4*>(a.recs + r);
+#pragma unroll
+      for (int q = 0; q < (int)(sizeof(RunRec<D>) / 16); ++q) __stcs(dst + q, src[q]);
+    }
+#else
     a.recs[r] = rec;
+#endif
   }
 }
 
