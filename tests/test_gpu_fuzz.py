@@ -16,6 +16,7 @@ pytestmark = pytest.mark.gpu
 KINDS = ["sff", "sf4", "sf3", "sf2", "sf1", "cm", "cu"]
 # SFK_FUZZ_SEEDS scales every fuzz test (default 40 seeds each)
 SEEDS = int(os.environ.get("SFK_FUZZ_SEEDS", "40"))
+SEED0 = int(os.environ.get("SFK_FUZZ_SEED0", "0"))  # first seed; soak runs set it to explore new seeds
 
 
 def random_case(rng, kind):
@@ -46,7 +47,7 @@ def random_case(rng, kind):
 
 
 @pytest.mark.parametrize("sequential", [False, True])
-@pytest.mark.parametrize("seed", range(SEEDS))
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + SEEDS))
 @pytest.mark.parametrize("kind", KINDS)
 def test_fuzz_against_oracle(oracle, kind, seed, sequential):
     if sequential and seed % 4:
@@ -78,7 +79,7 @@ def test_fuzz_against_oracle(oracle, kind, seed, sequential):
     np.testing.assert_array_equal(host(sk.query_many(q)), o.query_many(q))
 
 
-@pytest.mark.parametrize("seed", range(SEEDS))
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + SEEDS))
 def test_fuzz_count_cml_oracle(oracle, seed):
     """Count, CML and the oracle-assisted slim over random shapes, presets
     (near the int32 / u16 / u32 bounds), bases, counts and batch splits."""
@@ -157,7 +158,7 @@ def test_fuzz_count_cml_oracle(oracle, seed):
     np.testing.assert_array_equal(host(sk.slim.increment_counts), inc)
 
 
-@pytest.mark.parametrize("seed", range(SEEDS))
+@pytest.mark.parametrize("seed", range(SEED0, SEED0 + SEEDS))
 def test_fuzz_query_paths(oracle, seed):
     """min_query over random shapes, value distributions (small, around the
     u16 code boundary 0xF800, up to 2^32 - 1), key kinds and every path the
