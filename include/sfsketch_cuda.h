@@ -65,6 +65,11 @@ extern "C" {
  * parity tests use it to cross-check the two on the GPU. */
 #define SFK_FLAG_SEQUENTIAL 1
 
+/* Threading: the compute entry points keep no state between calls (all
+ * scratch is the caller's workspace) and may run concurrently on different
+ * streams and host threads; sfk_last_error() is per host thread. The
+ * diagnostics below (engine timing / trace / stats, sfk_query_path) are
+ * process-global switches for benchmarks and tests, not for concurrent use. */
 int sfk_abi_version(void);
 const char* sfk_last_error(void);
 
