@@ -191,3 +191,41 @@ def test_parallel_equals_sequential_engine():
     np.testing.assert_array_equal(host(a.slim.counters), host(b.slim.counters))
     np.testing.assert_array_equal(host(a.fat.counters), host(b.fat.counters))
     np.testing.assert_array_equal(host(a.slim.increment_counts), host(b.slim.increment_counts))
+
+
+@pytest.mark.parametrize("variant", ("sff", "sf1", "sf2", "cm", "cu"))
+def test_concurrent_sketches_on_two_streams_and_threads(variant):
+    """The C ABI keeps no state between calls (include/sfsketch_cuda.h): two
+    sketches updated at the same time from two host threads on two streams
+    end in the same state as when updated one after the other."""
+    import threading
+
+    def streams(seed):
+        c = W.cfg2(seed=seed, n=300_000, v=20_000)
+        return [(c["ops"][a:a + 100_000], c["keys"][a:a + 100_000]) for a in (0, 100_000, 200_000)]
+
+    def run(sk, batches, errs):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for ops, keys in batches:
+                    sk.apply_ops(ops, keys)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    data = [streams(11), streams(12)]
+    serial = [make_sketch(variant, 4, 4096, 4, 16384, 3 + i) for i in range(2)]
+    for sk, b in zip(serial, data):
+        run(sk, b, [])
+    conc = [make_sketch(variant, 4, 4096, 4, 16384, 3 + i) for i in range(2)]
+    errs = []
+    th = [threading.Thread(target=run, args=(sk, b, errs)) for sk, b in zip(conc, data)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for a, b in zip(serial, conc):
+        np.testing.assert_array_equal(host(a.counters if variant in ("cm", "cu") else a.slim.counters),
+                                      host(b.counters if variant in ("cm", "cu") else b.slim.counters))
