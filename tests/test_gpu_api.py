@@ -229,3 +229,37 @@ def test_concurrent_sketches_on_two_streams_and_threads(variant):
     for a, b in zip(serial, conc):
         np.testing.assert_array_equal(host(a.counters if variant in ("cm", "cu") else a.slim.counters),
                                       host(b.counters if variant in ("cm", "cu") else b.slim.counters))
+
+
+@pytest.mark.parametrize("variant", ("sff", "sf4"))
+def test_sf_apply_replays_from_a_cuda_graph(variant):
+    """A single-chunk SF apply does not synchronise the host or allocate
+    (INTEGRATION.md §2), so it can be captured once in a CUDA graph and
+    replayed: each replay applies the batch again, bit-exact with direct
+    applies."""
+    from paper_1701_04148_b200._ops import normalize_stream
+
+    c = W.cfg2(seed=21, n=200_000, v=30_000)
+    ops = np.concatenate([c["ops"], np.ones(40_000, dtype=np.uint8)])
+    keys = np.concatenate([c["keys"], c["keys"][:40_000]])
+    ops_d, keys_d = torch.as_tensor(ops).cuda(), torch.as_tensor(keys).cuda()
+    ref = make_sketch(variant, 4, 4096, 4, None, 9)
+    sk = make_sketch(variant, 4, 4096, 4, None, 9)
+    ops_t, kb = normalize_stream(ops_d, keys_d)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        sk._submit(ops_t, kb)  # first application, and the workspace is allocated outside the capture
+    torch.cuda.synchronize()
+    ref.apply_ops(ops_d, keys_d)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        res = sk._submit(ops_t, kb)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        ref.apply_ops(ops_d, keys_d)
+        assert res.cpu().tolist()[0] == 0
+        np.testing.assert_array_equal(host(sk.slim.counters), host(ref.slim.counters))
+        np.testing.assert_array_equal(host(sk.fat.counters), host(ref.fat.counters))
+        np.testing.assert_array_equal(host(sk.slim.increment_counts), host(ref.slim.increment_counts))
