@@ -16,6 +16,7 @@ place:
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +62,16 @@ class KeyBatch:
         return KeyBatch(self.tensor[a:b], self.kind, self.rec_len, b - a)
 
 
+def _host_view(arr: np.ndarray) -> torch.Tensor:
+    """Zero-copy tensor over a host array that is only read (copied to the
+    device); read-only arrays (np.frombuffer, memmaps) are accepted as-is."""
+    if arr.flags.writeable:
+        return torch.from_numpy(arr)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr)
+
+
 def _to_device(t: torch.Tensor, dev: torch.device) -> torch.Tensor:
     if t.device != dev:
         t = t.to(dev, non_blocking=t.is_pinned())
@@ -77,7 +88,7 @@ def normalize_keys(keys) -> KeyBatch:
             arr = np.ascontiguousarray(keys, dtype=np.uint64)
         if arr.dtype.kind == "b":
             arr = arr.astype(np.uint64)
-        keys = torch.from_numpy(np.ascontiguousarray(arr))
+        keys = _host_view(np.ascontiguousarray(arr))
     t = keys
     if t.dtype == torch.uint8 and t.dim() == 2:
         t = _to_device(t, dev)
@@ -102,7 +113,7 @@ def normalize_stream(ops, keys):
     if isinstance(ops, torch.Tensor):
         o = ops
     else:
-        o = torch.from_numpy(np.ascontiguousarray(ops, dtype=np.uint8))
+        o = _host_view(np.ascontiguousarray(ops, dtype=np.uint8))
     if o.dim() != 1 or int(o.shape[0]) != kb.n:
         raise ConfigurationError("ops and keys must be 1-d sequences of equal length")
     if o.dtype != torch.uint8:
