@@ -3,6 +3,7 @@
 // parallel engine or the exact sequential device engine, and splits very
 // large batches into chunks the 32-bit pair encoding can address.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
@@ -103,6 +104,10 @@ __global__ void set_result_k(int64_t* result, int64_t status, int64_t idx, int64
 }
 
 // parallel kinds (sfk_sf.cu): 0 SFF, 1 SF1, 2 CU, 3 CM exact
+#ifndef SFK_SMALL_BATCH_DEFAULT
+#define SFK_SMALL_BATCH_DEFAULT 32
+#endif
+
 static int64_t chunk_ops(int d, int z) {
   // t << (kb + 1) must fit 32 bits and d * n must fit a signed int
   int kb = 0;
@@ -111,6 +116,16 @@ static int64_t chunk_ops(int d, int z) {
   int64_t lim_n = ((int64_t)1 << 30) / std::max(d, 1);
   return std::min(lim_t, lim_n);
 }
+
+// Batches of at most this many ops run on the exact one-thread device engine:
+// one launch and no host round trip, against ~17-24 launches (plus CUB's)
+// and, for CM / CU, a precheck read-back on the parallel pipeline, whose
+// fixed cost (~80-140 us per batch) dominates tiny batches such as the
+// reference's insert(key) / delete(key). sfk_small_batch_ops() sets it (0: off).
+static int64_t g_small_batch = SFK_SMALL_BATCH_DEFAULT;
+static int64_t small_batch_ops() { return __atomic_load_n(&g_small_batch, __ATOMIC_RELAXED); }
+
+static bool small_batch(int64_t n) { return n > 0 && n <= small_batch_ops(); }
 
 static const char* key_ptr(const void* keys, int key_kind, int rec_len, int64_t t0) {
   const char* p = static_cast<const char*>(keys);
@@ -199,6 +214,10 @@ int sfk_gen_query_keys(uint64_t seed, const uint32_t* present, const uint32_t* s
 
 const char* sfk_last_error(void) { return g_err; }
 
+int64_t sfk_small_batch_ops(int64_t ops) {
+  return ops < 0 ? small_batch_ops() : __atomic_exchange_n(&g_small_batch, ops, __ATOMIC_RELAXED);
+}
+
 int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream) {
   return launch_mix_batch(keys, n, out, (cudaStream_t)stream);
 }
@@ -224,7 +243,7 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
                  size_t workspace_bytes, int flags, void* stream) {
   if (check_common(d, w, key_kind, rec_len)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
-  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD || small_batch(n))
     return launch_seq_apply(0, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops,
                             KeySrc{keys, key_kind, rec_len}, nullptr, n, inc_counts, result, st);
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
@@ -254,7 +273,7 @@ int sfk_cu_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
   if (check_common(d, w, key_kind, rec_len)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   KeySrc all{keys, key_kind, rec_len};
-  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD || small_batch(n))
     return launch_seq_apply(1, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops, all, nullptr, n,
                             inc_counts, result, st);
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
@@ -309,7 +328,7 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
   if (variant == SFK_VARIANT_SF2 && dsub == nullptr) { set_error("SF2 needs the deletion sub-sketch"); return 1; }
   const int kind = sf_parallel_kind(variant, d, z, w, w_prime);
   KeySrc all{keys, key_kind, rec_len};
-  if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0) {
+  if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0 || small_batch(n)) {
     if (flat)
       return launch_seq_apply(2, variant, slim, fat, dsub, slim_seeds, fat_seeds, d, w, w_prime, w_prime / w, ops, all,
                               nullptr, n, inc_counts, result, st);

@@ -48,3 +48,17 @@ def baseline_fixture_names(prefix=""):
 def load_baseline_fixture(name):
     with np.load(os.path.join(BASELINES, name + ".npz"), allow_pickle=False) as z:
         return {k: z[k] for k in z.files}
+
+
+@pytest.fixture
+def parallel_engine_only():
+    """Tiny batches normally take the one-thread engine (sfk_small_batch_ops);
+    parity tests turn that off so the parallel pipeline sees them too."""
+    from paper_1701_04148_b200 import _lib
+
+    L = _lib.lib()
+    prev = L.sfk_small_batch_ops(0)
+    try:
+        yield
+    finally:
+        L.sfk_small_batch_ops(prev)

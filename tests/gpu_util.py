@@ -57,3 +57,4 @@ def set_state(sk, fx):
     if "pre_fat" in fx:
         sk.fat.counters.copy_(torch.from_numpy(fx["pre_fat"]))
     counters_of(sk).copy_(torch.from_numpy(fx["pre_slim"]))
+

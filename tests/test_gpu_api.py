@@ -263,3 +263,39 @@ def test_sf_apply_replays_from_a_cuda_graph(variant):
         np.testing.assert_array_equal(host(sk.slim.counters), host(ref.slim.counters))
         np.testing.assert_array_equal(host(sk.fat.counters), host(ref.fat.counters))
         np.testing.assert_array_equal(host(sk.slim.increment_counts), host(ref.slim.increment_counts))
+
+
+@pytest.mark.parametrize("kind", ("sff", "sf4", "sf3", "sf2", "sf1", "cm", "cu"))
+def test_tiny_batches_both_engines_match_oracle(oracle, kind):
+    """Batches of 1..40 ops, with the small-batch threshold at its default
+    (<= 32 ops: the one-launch one-thread engine) and off (always the parallel
+    pipeline): both end every batch in the oracle's state, including a
+    phantom delete that aborts a batch part way."""
+    from paper_1701_04148_b200 import _lib
+
+    L = _lib.lib()
+    assert L.sfk_small_batch_ops(-1) == 32
+    c = W.cfg3(seed=77, n_ins=900, v=60, alpha=1.2)
+    ops, keys = c["ops"].copy(), c["keys"].copy()
+    if kind in ("sf1", "cu", "cm"):
+        ops[:] = 0
+    else:
+        ops[500], keys[500] = 1, 0xFFFFFFFF  # a phantom: never inserted
+    wp = {"sf3": 4 * 16, "sf1": 64, "sf2": 64}.get(kind)
+    sizes = [1, 2, 3, 5, 8, 13, 21, 31, 32, 33, 40] * 6
+    for small in (32, 0):
+        prev = L.sfk_small_batch_ops(small)
+        try:
+            o = oracle.OracleSketch(kind, 3, 16, 4, wp, 5)
+            sk = make_sketch(kind, 3, 16, 4, wp, 5)
+            a = 0
+            for n in sizes:
+                b = min(a + n, len(ops))
+                if a >= b:
+                    break
+                st = o.apply_ops(ops[a:b], keys[a:b].astype(np.uint64))
+                assert apply_batches(sk, ops[a:b], keys[a:b]) == st[:2], (small, a, b)
+                assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat if kind not in ("cm", "cu") else None)
+                a = b
+        finally:
+            L.sfk_small_batch_ops(prev)

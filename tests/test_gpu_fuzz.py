@@ -11,7 +11,7 @@ import torch
 
 from gpu_util import apply_batches, assert_state_equal, host, make_sketch
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("parallel_engine_only")]
 
 KINDS = ["sff", "sf4", "sf3", "sf2", "sf1", "cm", "cu"]
 # SFK_FUZZ_SEEDS scales every fuzz test (default 40 seeds each)

@@ -9,7 +9,7 @@ import torch
 from conftest import fixture_names, load_fixture, load_hashing
 from gpu_util import apply_batches, assert_state_equal, counters_of, host, make_sketch, set_state
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("parallel_engine_only")]
 
 import paper_1701_04148_b200 as P  # noqa: E402
 from paper_1701_04148_b200 import device as D  # noqa: E402
