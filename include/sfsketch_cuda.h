@@ -75,7 +75,8 @@ const char* sfk_last_error(void);
 
 /* Batches of 1..ops ops (default 32) go to the exact one-thread device engine
  * (one launch, no host read-back) instead of the parallel pipeline, whose
- * fixed cost dominates tiny batches; SF, CM and CU applies. 0 turns it off;
+ * fixed cost dominates tiny batches: SF, CM, CU, Count, CML and oracle-
+ * assisted applies. 0 turns it off;
  * a negative value only reads. Returns the previous value. Process-global. */
 int64_t sfk_small_batch_ops(int64_t ops);
 

@@ -354,7 +354,7 @@ int sfk_oracle_slim_apply(uint32_t* slim, const uint64_t* seeds, int d, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   KeySrc all{keys, key_kind, rec_len};
   bool ok = false;
-  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0)
+  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0 && !small_batch(n))
     if (int r = gated_precheck(true_counts, n, nullptr, nullptr, slim, (int64_t)d * w, workspace, workspace_bytes, &ok, st)) return r;
   if (!ok)
     return launch_seq_apply(4, 0, slim, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, nullptr, all, true_counts, n,
@@ -430,7 +430,7 @@ int sfk_count_apply(int32_t* counters, const uint64_t* seeds, int d, int64_t w, 
   if (check_common(d, w, key_kind, rec_len)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   KeySrc all{keys, key_kind, rec_len};
-  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD)
+  if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD || small_batch(n))
     return launch_seq_ext(5, counters, seeds, d, w, ops, all, n, nullptr, 0, 0, result, st);
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
     KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
@@ -468,7 +468,7 @@ int sfk_cml_apply(uint16_t* exps, const uint64_t* seeds, int d, int64_t w, const
   cudaStream_t st = (cudaStream_t)stream;
   KeySrc all{keys, key_kind, rec_len};
   bool ok = false;
-  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0)
+  if (!(flags & SFK_FLAG_SEQUENTIAL) && d <= MAXD && n > 0 && !small_batch(n))
     if (int r = gated_precheck(nullptr, n, gate, exps, nullptr, (int64_t)d * w, workspace, workspace_bytes, &ok, st)) return r;
   if (!ok) return launch_seq_ext(6, exps, seeds, d, w, ops, all, n, gate, rng_seed, start_pos, result, st);
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
