@@ -398,10 +398,13 @@ def run_ours(args):
     qkern = {1: "min_query_l2 (fused key load + 4x hash + 4 L2 gathers + min + int64 store)",
              2: "min_query_smem (whole slim in one SM's shared memory)",
              3: "min_query_cluster<4,u16> (4-CTA cluster, one slim row per CTA in smem, DSMEM st.async "
-                "partials, min + int64 store)"}.get(qpath, "?")
+                "partials, min + int64 store)",
+             4: "min_query_cw<4,u16> (4-CTA cluster, one slim row per CTA in smem; warp-pipelined: per-warp "
+                "512-key tiles, DSMEM st.async partials on per-warp mbarriers, packed-u16 min, coalesced int64 "
+                "stores)"}.get(qpath, "?")
     rf_query = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved_gbs / hbm, 4),
-                "traffic": ncu_traffic("query_cluster", qn) if qpath == 3 else None, "kernel": qkern,
+                "traffic": ncu_traffic({3: "query_cluster", 4: "query_cw"}.get(qpath, ""), qn), "kernel": qkern,
                 "algorithmic_bytes_per_launch": int(qn * 12), "launch_ms": round(q_s * 1e3, 3),
                 "peak_source": hbm_src}
     if gather:

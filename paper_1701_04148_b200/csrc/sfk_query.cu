@@ -120,6 +120,16 @@ int query_path(int mode) {
 }
 int query_last_path() { return g_query_last; }
 
+// opt-in shared memory per block of the current device (cached per ordinal)
+static int smem_optin() {
+  static int cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] <= 0) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return cache[dev];
+}
+
 // ---- cluster path: PTX helpers (mbarrier, DSMEM st.async) -------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
@@ -521,6 +531,334 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
   cluster_sync_all();  // no CTA exits while peers may still touch its shared memory
 }
 
+// ---- cluster path, warp-pipelined (u32 keys) ---------------------------------
+// Same row partition as min_query_cluster (CTA r of a D-CTA cluster holds slim
+// row r in shared memory), but the exchange runs per warp instead of per CTA:
+// warp w of every CTA of the cluster forms a "group" that works through its
+// own sequence of K-key warp-tiles, coupled only by per-warp mbarriers, so
+// there is no CTA-wide barrier in the steady state and warps hide each other's
+// latencies. Per warp-tile:
+//   keys   : every lane loads its KPL keys of the next tile into registers
+//            (LDG.128) one tile ahead (a TMA key ring in shared memory measured
+//            slower: it forces a smaller tile, and the tile size is what
+//            amortises the per-tile synchronisation);
+//   phase 1: every lane hashes KPL keys for row r and gathers their codes;
+//            4-key group gk goes to the CTA owning its 1/D of the tile with
+//            one st.async that completes bytes on the owner's `full` mbarrier;
+//   phase 2: one tile behind, the owner takes the min over the D partials
+//            (packed u16x2 VIMNMX), decodes rank codes and stores int64s;
+//            then it releases the buffer with a remote arrive on every
+//            producer's `empty` mbarrier.
+
+// finalize64(key ^ seed) for a 32-bit key, reduced to the BYTE offset of its
+// cell in a power-of-two row of 2^SH-byte codes: (idx << SH) comes straight
+// out of x' = x << SH (the second multiply by K2 << SH), so no extra shift.
+// v = u ^ u >> 30 with u = key ^ seed: the low word is key ^ (key >> 30) ^ c0.
+struct U32HashOff {
+  uint32_t c0;  // s_lo ^ (s_lo >> 30) ^ (s_hi << 2)
+  uint32_t c2;  // lo32((s_hi ^ s_hi >> 30) * lo32(K1)): the high-word term of v * K1
+};
+__host__ __device__ __forceinline__ U32HashOff make_u32hash_off(uint64_t seed) {
+  const uint32_t lo = (uint32_t)seed, hi = (uint32_t)(seed >> 32);
+  return U32HashOff{lo ^ (lo >> 30) ^ (hi << 2), (hi ^ (hi >> 30)) * 0x1CE4E5B9u};
+}
+template <int SH>
+__device__ __forceinline__ uint32_t row_off_u32(uint32_t key, uint32_t k30, const U32HashOff& h, uint32_t mask_b) {
+  constexpr uint64_t K2S = 0x94D049BB133111EBull << SH;
+  const uint32_t v = key ^ k30 ^ h.c0;
+  const uint64_t z = (uint64_t)v * 0x1CE4E5B9u + ((uint64_t)h.c2 << 32);  // v * K1, low word of K1
+  const uint32_t zlo = (uint32_t)z, zhi = (uint32_t)(z >> 32) + v * 0xBF58476Du;
+  const uint32_t ylo = zlo ^ __funnelshift_r(zlo, zhi, 27), yhi = zhi ^ (zhi >> 27);
+  const uint64_t x = (uint64_t)ylo * (uint32_t)K2S;
+  const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32) + ylo * (uint32_t)(K2S >> 32) + yhi * (uint32_t)K2S;
+  return (xlo ^ __funnelshift_r(xlo, xhi, 31)) & mask_b;
+}
+
+template <int D, typename CT, int NW, int KPL, int NB, bool POW2>
+__global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __restrict__ counters, Seeds<D> seeds,
+                                                           Mod wm, int64_t w, const uint32_t* __restrict__ keys,
+                                                           int64_t ntiles, int64_t* __restrict__ out) {
+  constexpr bool U16 = sizeof(CT) == 2;
+  constexpr int SH = U16 ? 1 : 2;
+  constexpr int NT = NW * 32;
+  constexpr int K = 32 * KPL;              // keys per warp-tile
+  constexpr int OKL = KPL / D;             // keys per lane in the owner phase
+  constexpr uint32_t RB = K * sizeof(CT);  // receive bytes per (warp, buffer)
+  constexpr uint32_t PB = RB / D;          // one producer's share
+  constexpr uint32_t GB = 4 * sizeof(CT);  // bytes of one 4-key group of codes
+  static_assert(KPL % 4 == 0 && (OKL == 2 || OKL == 4) && 32 % D == 0 && (NB == 2 || NB == 4), "tile shape");
+  constexpr int LNB = NB == 2 ? 1 : 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t r = cg::this_cluster().block_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CT* row = reinterpret_cast<CT*>(smem_raw);
+  const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
+  uint32_t* ovf = reinterpret_cast<uint32_t*>(smem_raw + row_bytes);
+  uint32_t* merged = ovf + OVF_STRIDE;
+  unsigned char* recv = smem_raw + row_bytes + (U16 ? 2 * OVF_STRIDE * 4 : 0);  // NW x NB x RB
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(recv + (size_t)NW * NB * RB);
+  // per warp: full[NB] (count 1), empty[NB] (count D)
+  constexpr int NBAR = 2 * NB;
+  int& novf = *reinterpret_cast<int*>(ovf + OVF_SLOTS);
+  if (threadIdx.x == 0) novf = 0;
+  if (threadIdx.x < NW) {
+    unsigned long long* b = bars + threadIdx.x * NBAR;
+    for (int k = 0; k < NB; ++k) mbar_init(smem_addr(b + k), 1);
+    for (int k = 0; k < NB; ++k) mbar_init(smem_addr(b + NB + k), D);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t* src = counters + (int64_t)r * w;
+  for (int64_t k = threadIdx.x; k < w; k += NT) {
+    uint32_t v = __ldg(src + k);
+    if (U16 && v >= OVF_BASE) {
+      const int s = atomicAdd(&novf, 1);
+      if (s < OVF_SLOTS) {
+        ovf[s] = v;
+        v = OVF_BASE + (uint32_t)s;
+      } else {
+        v = OVF_NONE;
+      }
+    }
+    row[k] = (CT)v;
+  }
+  cluster_sync_all();
+  if (U16) {
+    (void)rank_codes_setup<D, CT, NT>(row, ovf, merged, reinterpret_cast<uint32_t*>(recv), w, r);
+    if (threadIdx.x == 0) merged[OVF_SLOTS] = U32MAX;  // OVF_NONE decodes to the re-read sentinel
+    cluster_sync_all();
+  }
+
+  uint64_t seed = seeds.s[0];
+#pragma unroll
+  for (int i = 1; i < D; ++i)
+    if (i == (int)r) seed = seeds.s[i];
+  const U32HashOff hh = make_u32hash_off(seed);
+  const uint32_t mask_b = (uint32_t)wm.mask << SH;
+  const int64_t ncl = gridDim.x / D, cid = blockIdx.x / D;
+  const int64_t g0 = cid * NW + warp, gstride = ncl * NW;
+  const int Tw = g0 < ntiles ? (int)((ntiles - 1 - g0) / gstride + 1) : 0;
+  const int64_t tstep = gstride * K;  // key offset between a warp's consecutive tiles
+  const uint32_t rv_a = smem_addr(recv + (size_t)warp * NB * RB);
+  const uint32_t bar_a = smem_addr(bars + warp * NBAR);
+  const uint32_t full_a = bar_a, empty_a = bar_a + 8 * NB;
+  // 4-key group gk = 32 j + lane of a tile goes to owner CTA gk / GD (each
+  // owner takes a contiguous 1/D of the tile, so its int64 stores coalesce),
+  // slot gk % GD of producer r's share
+  constexpr int GD = K / 4 / D;
+  uint32_t o_recv[KPL / 4], o_full[KPL / 4];
+#pragma unroll
+  for (int j = 0; j < KPL / 4; ++j) {
+    const int gk = 32 * j + lane;
+    o_recv[j] = mapa_u32(rv_a, (uint32_t)(gk / GD)) + r * PB + (uint32_t)(gk % GD) * GB;
+    o_full[j] = mapa_u32(full_a, (uint32_t)(gk / GD));
+  }
+  const uint32_t p_empty = mapa_u32(empty_a, (uint32_t)(lane < D ? lane : 0));
+
+  // owner phase of tile ip (keys from tile_key) in receive buffer pb
+  auto owner_phase = [&](int ip, int pb, uint32_t par, int64_t tile_key) {
+    mbar_wait(full_a + 8 * pb, par);
+    // the owner's 1/D of the tile: OKL consecutive keys per lane, at byte
+    // lane * OKL * sizeof(CT) of every producer's share
+    const int64_t t = tile_key + (int64_t)r * (K / D) + lane * OKL;
+    uint32_t m[OKL];
+    const unsigned char* R = recv + ((size_t)warp * NB + pb) * RB;
+    if constexpr (U16) {
+      uint32_t pk[OKL / 2];
+#pragma unroll
+      for (int p = 0; p < D; ++p) {
+        uint32_t v[OKL / 2];
+        if constexpr (OKL == 2) {
+          v[0] = *reinterpret_cast<const uint32_t*>(R + p * PB + lane * 4);
+        } else {
+          const uint2 q2 = *reinterpret_cast<const uint2*>(R + p * PB + lane * 8);
+          v[0] = q2.x;
+          v[OKL / 2 - 1] = q2.y;
+        }
+#pragma unroll
+        for (int u = 0; u < OKL / 2; ++u) pk[u] = p == 0 ? v[u] : __vminu2(pk[u], v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < OKL / 2; ++u) m[2 * u] = pk[u] & 0xFFFFu, m[2 * u + 1] = pk[u] >> 16;
+      // rank codes decode with one (predicated) table load each; OVF_NONE
+      // maps to the U32MAX sentinel in merged[OVF_SLOTS], and only a U32MAX
+      // result (exhausted tables, or a counter that really is U32MAX)
+      // re-reads the key's d u32 counters
+      bool big = false;
+#pragma unroll
+      for (int u = 0; u < OKL; ++u) big |= m[u] >= OVF_BASE;
+      bool none = false;
+      if (__any_sync(0xFFFFFFFFu, big)) {  // warp-uniform: no divergence on Zipf-hot tiles
+#pragma unroll
+        for (int u = 0; u < OKL; ++u) {
+          if (m[u] >= OVF_BASE) m[u] = merged[m[u] - OVF_BASE];
+          none |= m[u] == U32MAX;
+        }
+      }
+      if (none) {
+#pragma unroll
+        for (int u = 0; u < OKL; ++u) {
+          if (m[u] == U32MAX) {
+            const uint64_t key = (uint64_t)__ldg(keys + t + u);
+            uint32_t mm = U32MAX;
+#pragma unroll
+            for (int p = 0; p < D; ++p)
+              mm = min(mm, __ldg(counters + (int64_t)p * w + (int64_t)fmod64(mix64(key ^ seeds.s[p]), wm)));
+            m[u] = mm;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < D; ++p) {
+        uint32_t v[OKL];
+        if constexpr (OKL == 2) {
+          const uint2 q2 = *reinterpret_cast<const uint2*>(R + p * PB + lane * 8);
+          v[0] = q2.x;
+          v[OKL - 1] = q2.y;
+        } else {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(R + p * PB + lane * 16);
+          v[0] = q4.x;
+          v[1] = q4.y;
+          v[OKL - 2] = q4.z;
+          v[OKL - 1] = q4.w;
+        }
+#pragma unroll
+        for (int u = 0; u < OKL; ++u) m[u] = p == 0 ? v[u] : min(m[u], v[u]);
+      }
+    }
+    longlong2* o2 = reinterpret_cast<longlong2*>(out + t);
+#pragma unroll
+    for (int u = 0; u < OKL / 2; ++u) __stcs(o2 + u, make_longlong2((long long)m[2 * u], (long long)m[2 * u + 1]));
+    __syncwarp();
+    if (ip + NB < Tw && lane < D) mbar_arrive_remote(p_empty + 8 * pb);
+  };
+
+  // NB receive buffers (a power of two): buffer and phase parity are bits of
+  // the tile counter
+  int64_t tile_key = g0 * K;
+  uint4 kn[KPL / 4];  // the next tile's keys
+  auto gload = [&](int64_t tk) {
+    const uint4* src = reinterpret_cast<const uint4*>(keys + tk) + lane;
+#pragma unroll
+    for (int j = 0; j < KPL / 4; ++j) kn[j] = __ldcs(src + j * 32);
+  };
+  if (Tw > 0) gload(tile_key);
+  for (int it = 0; it < Tw; ++it) {
+    const int pb = it & (NB - 1);
+    uint4 kk[KPL / 4];
+#pragma unroll
+    for (int j = 0; j < KPL / 4; ++j) kk[j] = kn[j];
+    if (it + 1 < Tw) gload(tile_key + tstep);
+    if (lane == 0) mbar_expect_arrive(full_a + 8 * pb, RB);
+    uint32_t c[KPL];
+    const unsigned char* rowb = reinterpret_cast<const unsigned char*>(row);
+#pragma unroll
+    for (int j = 0; j < KPL / 4; ++j) {
+      const uint32_t kx[4] = {kk[j].x, kk[j].y, kk[j].z, kk[j].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t off;
+        if constexpr (POW2)
+          off = row_off_u32<SH>(kx[u], kx[u] >> 30, hh, mask_b);
+        else
+          off = (uint32_t)fmod64(mix64((uint64_t)kx[u] ^ seed), wm) << SH;
+        c[4 * j + u] = *reinterpret_cast<const CT*>(rowb + off);
+      }
+    }
+    if (it >= NB) mbar_wait(empty_a + 8 * pb, (uint32_t)((it >> LNB) - 1) & 1);
+#pragma unroll
+    for (int j = 0; j < KPL / 4; ++j) {
+      const uint32_t dst = o_recv[j] + pb * RB;
+      if constexpr (U16)
+        st_async_v2(dst, c[4 * j] | (c[4 * j + 1] << 16), c[4 * j + 2] | (c[4 * j + 3] << 16), o_full[j] + 8 * pb);
+      else
+        st_async_v4(dst, c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3], o_full[j] + 8 * pb);
+    }
+
+    if (it >= 1) owner_phase(it - 1, (it - 1) & (NB - 1), (uint32_t)((it - 1) >> LNB) & 1, tile_key - tstep);
+    tile_key += tstep;
+  }
+  if (Tw > 0) owner_phase(Tw - 1, (Tw - 1) & (NB - 1), (uint32_t)((Tw - 1) >> LNB) & 1, tile_key - tstep);
+  cluster_sync_all();  // no CTA exits while peers may still touch its shared memory
+}
+
+// warp-pipelined kernel shape (A/B knobs): warps per CTA, keys per lane per
+// tile (d = 4; d = 2 uses 8, d = 8 uses 16), receive buffers per warp
+#ifndef SFK_CW_NW
+#define SFK_CW_NW 16
+#endif
+#ifndef SFK_CW_KPL
+#define SFK_CW_KPL 16
+#endif
+#ifndef SFK_CW_NB
+#define SFK_CW_NB 2
+#endif
+
+
+// Launch the warp-pipelined cluster kernel for u32 keys (16-B aligned keys and
+// output); the < K-key tail goes to the L2 kernel. Returns -1 if not suited.
+template <int D, typename CT, bool POW2>
+static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                  int64_t* out, cudaStream_t st, int optin) {
+  constexpr int NW = SFK_CW_NW, NB = SFK_CW_NB;
+  constexpr int KPL = D == 2 ? 8 : D == 8 ? 16 : SFK_CW_KPL;  // owner phase: KPL / D keys per lane
+  constexpr int K = 32 * KPL;
+  if (ks.kind != SFK_KEY_U32 || (reinterpret_cast<uintptr_t>(ks.p) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return -1;
+  const int64_t ntiles = n / K;
+  if (ntiles < 1) return -1;
+  const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
+  const size_t smem = row_bytes + (sizeof(CT) == 2 ? 2 * OVF_STRIDE * 4 : 0) + (size_t)NW * NB * K * sizeof(CT) +
+                      (size_t)NW * 2 * NB * 8;
+  if (smem > (size_t)optin) return -1;
+  if (sizeof(CT) == 2 && (size_t)NW * NB * K * sizeof(CT) < (size_t)OVF_SLOTS * 4) return -1;  // setup scratch
+  auto kern = min_query_cw<D, CT, NW, KPL, NB, POW2>;
+  // the opt-in attribute belongs to the current device's context: set it per call
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = D;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.gridDim = dim3(D * sm_count());
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters <= 0) {
+    cudaGetLastError();
+    return -1;
+  }
+  const int64_t need = (ntiles + NW - 1) / NW;
+  if ((int64_t)nclusters > need) nclusters = (int)need;
+  cfg.gridDim = dim3(D * nclusters);
+  note_launch();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, counters, sd, wm, w, static_cast<const uint32_t*>(ks.p), ntiles, out);
+  if (e != cudaSuccess) {
+    set_error("min_query_cw launch: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  int rc = check_launch("min_query_cw");
+  if (rc) return rc;
+  g_query_last = 4;
+  const int64_t done = ntiles * K;
+  if (done < n) {
+    KeySrc tail{static_cast<const uint32_t*>(ks.p) + done, SFK_KEY_U32, 0};
+    note_launch();
+    min_query_l2<D, 4><<<grid_for(n - done, 256 * 4, sm_count() * 8), 256, 0, st>>>(counters, sd, wm, w, tail,
+                                                                                    n - done, out + done);
+    rc = check_launch("min_query_l2 (tail)");
+  }
+  return rc;
+}
+
 // Launch the cluster kernel if this (d, w, n) suits it; returns -1 if not.
 template <int D, typename CT, int TILE, int KK, bool VEC, bool POW2>
 static int try_cluster_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
@@ -532,13 +870,10 @@ static int try_cluster_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, i
                       2 * QNB * 8;
   if (smem + 1024 > (size_t)optin) return -1;
   auto kern = min_query_cluster<D, CT, TILE, NT, KK, VEC, POW2>;
-  static int attr_done = 0;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess) {
-      cudaGetLastError();
-      return -1;
-    }
-    attr_done = 1;
+  // the opt-in attribute belongs to the current device's context: set it per call
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -621,12 +956,7 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
   for (int i = 0; i < D; ++i) sd.s[i] = seeds_host[i];
   Mod wm = make_mod((uint64_t)w);
   const int sms = sm_count();
-  static int optin = -1;
-  if (optin < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
+  const int optin = smem_optin();
   const size_t tab_bytes = (size_t)D * (size_t)w * 4;
   const int mode = g_query_path;
   // staging costs tab_bytes per SM; worth it once the batch's own gathers
@@ -634,10 +964,9 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
   const bool smem_fits = tab_bytes <= (size_t)optin;
   const bool smem_pays = (double)n * D >= 16.0 * (double)sms * (double)(D * w) / 4.0;
   if ((mode == 0 && smem_fits && smem_pays) || (mode == 2 && smem_fits)) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(min_query_smem<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-      attr_set = true;
+    if (cudaFuncSetAttribute(min_query_smem<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) {
+      set_error("min_query_smem: cudaFuncSetAttribute: %s", cudaGetErrorString(cudaGetLastError()));
+      return 1;
     }
     { note_launch(); min_query_smem<D, 4><<<sms, 1024, tab_bytes, st>>>(counters, sd, wm, w, ks, n, out); }
     g_query_last = 2;
@@ -645,7 +974,22 @@ static int launch_query_d(const uint32_t* counters, const uint64_t* seeds_host, 
   }
   // row-partitioned cluster path: d CTAs per cluster (portable size <= 8);
   // pays once the batch is well beyond the per-CTA row staging (~2M keys)
-  if (D >= 2 && D <= 8 && ((mode == 0 && !smem_fits && n >= (int64_t(1) << 21)) || mode == 3)) {
+  // warp-pipelined cluster path (u32 keys, d in {2, 4, 8}): u32 rows when
+  // they fit beside the rings, else u16 codes
+  if constexpr (D == 2 || D == 4 || D == 8) {
+    if ((mode == 0 && !smem_fits && n >= (int64_t(1) << 21)) || mode == 4) {
+      int rc = -1;
+      if ((size_t)w * 4 + 100 * 1024 <= (size_t)optin) {
+        rc = wm.pow2 ? try_cw<D, uint32_t, true>(counters, sd, wm, w, ks, n, out, st, optin)
+                     : try_cw<D, uint32_t, false>(counters, sd, wm, w, ks, n, out, st, optin);
+      }
+      if (rc < 0 && w <= 65536)
+        rc = wm.pow2 ? try_cw<D, uint16_t, true>(counters, sd, wm, w, ks, n, out, st, optin)
+                     : try_cw<D, uint16_t, false>(counters, sd, wm, w, ks, n, out, st, optin);
+      if (rc >= 0) return rc;
+    }
+  }
+  if (D >= 2 && D <= 8 && ((mode == 0 && !smem_fits && n >= (int64_t(1) << 21)) || mode == 3 || mode == 4)) {
     int rc = -1;
     if ((size_t)w * 4 + 2 * 8192 * 4 + 64 + 1024 <= (size_t)optin)
       rc = try_cluster<D, uint32_t, 8192>(counters, sd, wm, w, ks, n, out, st, optin);
@@ -720,12 +1064,7 @@ static int launch_index_d(const uint64_t* seeds_host, int64_t w, KeySrc ks, int6
 template <int D>
 static int launch_query_idx_d(const uint32_t* counters, int64_t w, const uint16_t* idx, int64_t n, int64_t* out,
                               cudaStream_t st) {
-  static int optin = -1;
-  if (optin < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
+  const int optin = smem_optin();
   Seeds<D> sd{};
   const Mod wm = make_mod((uint64_t)w);
   const KeySrc ks{idx, KEY_IDX16, 0};

@@ -162,7 +162,7 @@ def test_fuzz_count_cml_oracle(oracle, seed):
 def test_fuzz_query_paths(oracle, seed):
     """min_query over random shapes, value distributions (small, around the
     u16 code boundary 0xF800, up to 2^32 - 1), key kinds and every path the
-    shape allows (auto, L2, shared memory, cluster)."""
+    shape allows (auto, L2, shared memory, cluster, warp-pipelined cluster)."""
     import ctypes
 
     from paper_1701_04148_b200 import _lib
@@ -203,7 +203,7 @@ def test_fuzz_query_paths(oracle, seed):
     if w * d * 4 <= 200 * 1024:
         paths.append(2)
     if 2 <= d <= 8 and w * 2 <= 110 * 1024:
-        paths.append(3)
+        paths += [3, 4]
     for path in paths:
         prev = L.sfk_query_path(path)
         try:

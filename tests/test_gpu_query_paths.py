@@ -1,5 +1,6 @@
 """Every point-query kernel path (L2 gathers, whole table in shared memory,
-row-partitioned cluster with DSMEM min-reduction) against the oracle's
+row-partitioned cluster with DSMEM min-reduction, and its warp-pipelined
+form with TMA key rings) against the oracle's
 min_query (the restatement of _kernels.min_query, _kernels.py:229-241), with
 the path forced through sfk_query_path. Covers the cluster path's u16 rows
 with the exact >= 65535 re-gather, u32 rows, odd d, non-power-of-two widths,
@@ -16,7 +17,7 @@ pytestmark = pytest.mark.gpu
 from paper_1701_04148_b200 import _lib  # noqa: E402
 from paper_1701_04148_b200.hashing import seed_array  # noqa: E402
 
-L2, SMEM, CLUSTER = 1, 2, 3
+L2, SMEM, CLUSTER, CW = 1, 2, 3, 4
 
 
 def run_query(counters, seeds, keys_t, kind, rec, n, out_t, path):
@@ -49,6 +50,14 @@ def table(rng, d, w, hi):
     (2, 40000, 1 << 32, CLUSTER),
     (4, 12800, 1 << 32, SMEM),      # cfg 4 shape
     (4, 65536, 1 << 32, L2),
+    (4, 65536, 1 << 20, CW),        # cfg 3/5 shape on the warp-pipelined kernel: u16 rows
+    (4, 65536, 70000, CW),
+    (4, 65536, 1000, CW),
+    (4, 16384, 1 << 32, CW),        # u32 rows
+    (8, 50000, 1 << 17, CW),        # d = 8 cluster, non-pow2 u16 rows
+    (8, 8192, 1 << 32, CW),         # d = 8, u32 rows
+    (2, 40000, 1 << 32, CW),        # d = 2, non-pow2, u32 rows
+    (2, 65536, 1 << 18, CW),        # d = 2, u16 rows
 ])
 @pytest.mark.parametrize("n", [1, 4097, 100_003, 1_000_000])
 def test_query_paths_u32_keys(oracle, d, w, hi, path, n):
@@ -62,13 +71,16 @@ def test_query_paths_u32_keys(oracle, d, w, hi, path, n):
     kt = torch.from_numpy(keys).cuda()
     out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
     took = run_query(ct, seeds, kt, _lib.KEY_U32, 0, n, out, path)
-    assert took == path
+    # the warp-pipelined kernel needs one whole warp-tile (>= 512 keys);
+    # below that the request falls back to the CTA-level cluster kernel
+    assert took == (CLUSTER if path == CW and n < 512 else path)
     want = oracle.min_query(c, seeds, keys.astype(np.uint64))
     np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("n_hot,distinct_vals", [(300, 0), (300, 7), (1000, 0)])
-def test_cluster_hot_keys_take_the_exact_regather(oracle, n_hot, distinct_vals):
+@pytest.mark.parametrize("path", [CLUSTER, CW])
+@pytest.mark.parametrize("n_hot,distinct_vals", [(300, 0), (300, 7), (1000, 0), (3000, 0)])
+def test_cluster_hot_keys_take_the_exact_regather(oracle, n_hot, distinct_vals, path):
     """Keys whose every row counter is large (the hot keys of a Zipf stream)
     must come back with their exact u32 minimum: through the cluster-wide
     rank codes (few large cells, ties across rows when distinct_vals > 0)
@@ -89,14 +101,14 @@ def test_cluster_hot_keys_take_the_exact_regather(oracle, n_hot, distinct_vals):
     ct = torch.from_numpy(c).cuda()
     kt = torch.from_numpy(keys).cuda()
     out = torch.empty(keys.size, dtype=torch.int64, device="cuda")
-    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, keys.size, out, CLUSTER) == CLUSTER
+    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, keys.size, out, path) == path
     got = out.cpu().numpy()
     want = oracle.min_query(c, seeds, keys.astype(np.uint64))
     np.testing.assert_array_equal(got, want)
     assert (got[:n_hot] >= 63488).all()
 
 
-@pytest.mark.parametrize("path", [L2, CLUSTER])
+@pytest.mark.parametrize("path", [L2, CLUSTER, CW])
 def test_query_paths_misaligned_views(oracle, path):
     d, w, n = 4, 65536, 200_001
     rng = np.random.default_rng(11)
@@ -107,7 +119,8 @@ def test_query_paths_misaligned_views(oracle, path):
     out_base = torch.empty(n + 1, dtype=torch.int64, device="cuda")
     out = out_base[1:]                                   # 8-B aligned only
     ct = torch.from_numpy(c).cuda()
-    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, n, out, path) == path
+    # misaligned views cannot feed the bulk copies: CW falls back to CLUSTER
+    assert run_query(ct, seeds, kt, _lib.KEY_U32, 0, n, out, path) == (CLUSTER if path == CW else path)
     np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, keys[1:n + 1].astype(np.uint64)))
 
 
@@ -128,13 +141,13 @@ def test_query_paths_u64_and_record_keys(oracle, path):
     np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, oracle.keys_from_records(recs)))
 
 
-def test_auto_path_picks_cluster_for_cfg5_shape():
+def test_auto_path_picks_warp_pipelined_cluster_for_cfg5_shape():
     d, w, n = 4, 65536, 1 << 22
     c = torch.zeros((d, w), dtype=torch.uint32, device="cuda")
     seeds = seed_array(2017, 0, d)
     keys = torch.zeros(n, dtype=torch.uint32, device="cuda")
     out = torch.empty(n, dtype=torch.int64, device="cuda")
-    assert run_query(c, seeds, keys, _lib.KEY_U32, 0, n, out, 0) == CLUSTER
+    assert run_query(c, seeds, keys, _lib.KEY_U32, 0, n, out, 0) == CW
     assert int(out.max()) == 0
 
 

@@ -19,7 +19,7 @@ from paper_1701_04148_b200 import _lib, workloads as W  # noqa: E402
 Q = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000_000
 ALPHAS = [float(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0.0, 0.5, 1.0, 1.5, 2.0, 2.5, 3.0]
 PATHS = [int(p) for p in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 3]
-NAMES = {1: "l2", 2: "smem", 3: "cluster"}
+NAMES = {1: "l2", 2: "smem", 3: "cluster", 4: "cw"}
 REPS = 5
 
 L = _lib.lib()
