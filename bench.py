@@ -9,15 +9,24 @@ One step = the SF sketch hot path over one synthetic batch:
   3. query: the cfg-5 batch of Q point queries (default 1B uint32 keys, half
      present with Zipf(1.0) rank skew, half absent) sharded contiguously over
      the N GPUs, each answering its slice with the fused hash+gather+min kernel.
+This is north_star's multi-GPU layout (strong scaling: the job is fixed, the
+build stays on one GPU, the queries spread). ``--replicas`` instead runs N
+independent sketches (weak scaling). Beside the headline the line reports
+``insert`` and ``query`` separately (Mitems/s, fraction of the random-gather
+roofline, CPU ratio), and ``cm_merge``: the cfg-2 count-min build sharded by
+stream over the N GPUs and merged with one NCCL all-reduce.
 value = (ops applied + queries answered) / step time (max over ranks),
 Mitems/s. Inputs are device-resident for ``value``; ``e2e`` repeats the step
 through the same public API from pinned HOST buffers (H2D of ops/keys and
 query keys, D2H of the estimates inside the timed region).
 
-``--impl reference`` times the CPU oracle (a C port of the reference's numba
-kernels, tests pin it bit-exact to the reference) on the host cores for the
-same workload: the build single-threaded (single-writer contract), the
-queries on all host threads, extrapolated from a bounded sample.
+``--impl reference`` times the reference's own CPU implementation (the
+``sfsketch`` package installed unmodified in ``baseline/_ref``, numba
+kernels) on the host cores for the same workload: the build single-threaded
+(single-writer contract), the queries split over all host threads
+(``bench.py:153-162`` of the reference), extrapolated from a bounded sample.
+Without ``baseline/_ref`` it falls back to the C port of those kernels
+(``oracle/``, pinned bit-exact to the reference).
 """
 
 from __future__ import annotations
@@ -53,14 +62,17 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cm", action="store_true", help="skip the cfg-2 CM merge leg")
-    ap.add_argument("--shared-slim", action="store_true",
-                    help="N>1: build once on rank 0, broadcast the slim, shard the queries (strong scaling) "
-                         "instead of one independent replica per GPU (weak scaling, the default)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent sketch per GPU (weak scaling) instead of the default build on rank 0 "
+                         "+ slim broadcast + sharded queries")
+    ap.add_argument("--shared-slim", action="store_true", help="(default; kept for old command lines)")
+    ap.add_argument("--cpu-kind", default="auto", choices=["auto", "reference", "port"],
+                    help="CPU baseline: the reference package in baseline/_ref (numba) or the C port")
     return ap.parse_args()
 
 
 def replicas(args, world):
-    return world > 1 and not args.shared_slim
+    return world > 1 and args.replicas
 
 
 def workload_config(args, world):
@@ -69,7 +81,8 @@ def workload_config(args, world):
                "shard); rank r builds its own cfg-3 stream (seed %d + r) and answers its own %d queries; no "
                "data-path collective" % (world, SEED, args.queries))
     elif world > 1:
-        par = "build on rank 0 (order-dependent), slim broadcast, queries sharded over %d GPU(s)" % world
+        par = ("north_star layout: build on rank 0 (SF updates are order-dependent), NCCL broadcast of the slim, "
+               "queries sharded contiguously over %d GPUs" % world)
     else:
         par = "1 GPU"
     return {
@@ -173,30 +186,85 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_measure(args, stream, present_sample_keys, threads):
-    """Oracle (C port of the reference kernels): build single-threaded over the
-    full 12M-op stream, queries with `threads` threads over a sample."""
-    from oracle import oracle as orc
+def ref_package():
+    """The unmodified reference package installed in baseline/_ref (None if absent)."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(p, "sfsketch", "__init__.py")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/sfk_numba_cache")
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    try:
+        import sfsketch
+    except Exception:  # noqa: BLE001 - e.g. numba missing: the port stands in
+        return None
+    return sfsketch
 
-    orc.lib()
-    o = orc.OracleSketch("sff", D, W, Z, None, SEED)
+
+def cpu_kind(args):
+    if args.cpu_kind == "port":
+        return "port", None
+    ref = ref_package()
+    if ref is None and args.cpu_kind == "reference":
+        raise SystemExit("baseline/_ref holds no importable sfsketch")
+    return ("reference", ref) if ref is not None else ("port", None)
+
+
+def cpu_measure(args, stream, qs, threads, kind="port", ref=None):
+    """The CPU path on the host: the full 12M-op cfg-3 build single-threaded
+    (the reference's single-writer contract), then `qs` queries split over
+    `threads` threads; kind "reference" drives the reference package's own
+    SfSketch (numba; JIT warmed first as the reference's bench.py:155,181
+    does), kind "port" the C restatement. Returns (value Mitems/s, build s,
+    query s, sample text, sketch)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    ops = stream["ops"]
     keys64 = stream["keys"].astype(np.uint64)
-    t0 = time.perf_counter()
-    st = o.apply_ops(stream["ops"], keys64)
-    t_build = time.perf_counter() - t0
-    assert st[0] == 0
-    qs = present_sample_keys
-    out = np.ones(qs.shape[0], dtype=np.int64)  # pre-faulted output, as a server would reuse
-    o.query_many(qs[: min(qs.shape[0], 1 << 20)], threads=threads, out=out[: min(qs.shape[0], 1 << 20)])  # warm
-    t0 = time.perf_counter()
-    o.query_many(qs, threads=threads, out=out)
-    t_q = time.perf_counter() - t0
-    n_ops = stream["ops"].shape[0]
+    n_ops = ops.shape[0]
+    if kind == "reference":
+        sk = ref.SfSketch(ref.SketchParams(d=D, w=W, z=Z, master_seed=SEED), "sff")
+        sk.apply_ops(ops[:1], keys64[:1])  # compile
+        t0 = time.perf_counter()
+        sk.apply_ops(ops[1:], keys64[1:])
+        t_build = (time.perf_counter() - t0) * n_ops / (n_ops - 1)
+        q64 = qs.astype(np.uint64)
+        chunks = np.array_split(q64, threads)
+        sk.query_many(q64[:16])  # compile
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            t0 = time.perf_counter()
+            outs = [f.result() for f in [pool.submit(sk.query_many, c) for c in chunks]]
+            t_q = time.perf_counter() - t0
+        est = np.concatenate(outs)
+        what = "reference sfsketch (baseline/_ref, numba)"
+    else:
+        from oracle import oracle as orc
+
+        orc.lib()
+        sk = orc.OracleSketch("sff", D, W, Z, None, SEED)
+        t0 = time.perf_counter()
+        st = sk.apply_ops(ops, keys64)
+        t_build = time.perf_counter() - t0
+        assert st[0] == 0
+        est = np.ones(qs.shape[0], dtype=np.int64)  # pre-faulted output, as a server would reuse
+        m = min(qs.shape[0], 1 << 20)
+        sk.query_many(qs[:m], threads=threads, out=est[:m])  # warm
+        t0 = time.perf_counter()
+        sk.query_many(qs, threads=threads, out=est)
+        t_q = time.perf_counter() - t0
+        what = "C port of the reference kernels (oracle/)"
     t_total = t_build + t_q * (args.queries / qs.shape[0])
     value = (n_ops + args.queries) / t_total / 1e6
-    sample = (f"full 12M-op cfg-3 build on 1 thread ({t_build:.2f} s) + {qs.shape[0]:,} cfg-5 queries on "
-              f"{threads} threads ({t_q:.2f} s), query time extrapolated to {args.queries:,}")
-    return value, t_build, t_q, sample, o
+    sample = (f"{what}: full {n_ops:,}-op cfg-3 build on 1 thread ({t_build:.2f} s) + {qs.shape[0]:,} cfg-5 queries "
+              f"on {threads} threads ({t_q:.2f} s), query time extrapolated to {args.queries:,}")
+    return value, t_build, t_q, sample, sk, est
+
+
+def cpu_state(kind, sk):
+    """(slim, fat) of a CPU sketch of either kind, as numpy arrays."""
+    if kind == "reference":
+        return sk.slim.counters, sk.fat.counters
+    return sk.slim, sk.fat
 
 
 def run_reference(args):
@@ -205,30 +273,45 @@ def run_reference(args):
         return
     from paper_1701_04148_b200 import workloads as Wl
 
+    kind, ref = cpu_kind(args)
     stream = Wl.cfg3(seed=SEED, alpha=args.alpha)
-    sample_n = 100_000_000
+    sample_n = 50_000_000 if kind == "reference" else 100_000_000
     qs = Wl.query_keys(SEED + 5, stream["distinct"], args.alpha_q, 0, sample_n)
-    from oracle import oracle as orc
-
-    threads = orc.max_threads()
+    threads = len(os.sched_getaffinity(0))
     times = []
     for k in range(args.warmup + args.steps):
-        value, tb, tq, sample, _ = cpu_measure(args, stream, qs, threads)
+        value, tb, tq, sample, _, _ = cpu_measure(args, stream, qs, threads, kind, ref)
         if k >= args.warmup:
             times.append((value, tb, tq))
     value = statistics.median([t[0] for t in times])
+    tb = statistics.median([t[1] for t in times])
+    tq = statistics.median([t[2] for t in times])
     n_items = 12_000_000 + args.queries
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mitems/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(n_items / (value * 1e6) * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": round(n_items / (value * 1e6) * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak" if (args.gpus > 1 and args.replicas) else "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": workload_config(args, args.gpus),
-        "cpu_baseline": {"value": round(value, 3), "unit": "Mitems/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mitems/s", "cores": threads, "kind": kind,
+                         "sample": sample, "cpu": cpu_model()},
+        "insert": {"Mitems_s": round(12_000_000 / tb / 1e6, 3), "threads": 1},
+        "query": {"Mitems_s": round(qs.shape[0] / tq / 1e6, 3), "threads": threads},
         "e2e": {"value": round(value, 3), "unit": "Mitems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------ CM merge leg
@@ -241,7 +324,7 @@ def run_cm_leg(args, world, rank, dev):
     import torch.distributed as dist
 
     import paper_1701_04148_b200 as P
-    from paper_1701_04148_b200 import distributed as Dd, workloads as Wl
+    from paper_1701_04148_b200 import workloads as Wl
 
     c = Wl.cfg2(seed=SEED)
     ops_d = torch.from_numpy(c["ops"]).to(dev)
@@ -258,7 +341,7 @@ def run_cm_leg(args, world, rank, dev):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if world > 1:
-            Dd.sharded_cm_apply(cm, ops_d, keys_d)
+            cm.sharded_apply_(ops_d, keys_d)
         else:
             cm.apply_ops(ops_d, keys_d)
         e1.record()
@@ -271,17 +354,42 @@ def run_cm_leg(args, world, rank, dev):
     ms = float(t.item())
     n = int(c["ops"].shape[0])
     out = {"workload": "cfg2 CM d=4 w=65536, 10M inserts Zipf(1.0) over 1M distinct uint32 keys, stream sharded "
-                       "over %d GPU(s) + NCCL sum all-reduce of the counters" % world,
-           "ms": round(ms, 3), "Mitems_s": round(n / (ms * 1e-3) / 1e6, 2), "ops": n}
+                       "over %d GPU(s) (global precheck, raw signed deltas, one NCCL sum all-reduce; "
+                       "distributed.sharded_cm_apply)" % world if world > 1 else
+                       "cfg2 CM d=4 w=65536, 10M inserts Zipf(1.0) over 1M distinct uint32 keys, 1 GPU "
+                       "(CmSketch.apply_ops: device precheck + warp-aggregated atomics)",
+           "ms": round(ms, 3), "Mitems_s": round(n / (ms * 1e-3) / 1e6, 2), "ops": n, "n_gpus": world}
+    _, _, gather = measured_peaks()
+    if gather and gather.get("red_1MiB_Gps"):
+        # d atomic counter updates per op against the measured RED peak on a
+        # 1 MiB L2-resident table, per GPU
+        upd = n * D / (ms * 1e-3) / 1e9 / world
+        out["gather"] = {"red_Gps_per_gpu": round(upd, 1), "peak_Gps": gather["red_1MiB_Gps"],
+                         "frac": round(upd / gather["red_1MiB_Gps"], 4),
+                         "peak_source": "profiles/gather_peaks.json (RED.ADD on a 1 MiB table)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as orc
+        kind, ref = cpu_kind(args)
+        keys64 = c["keys"].astype(np.uint64)
+        if kind == "reference":
+            r = ref.CmSketch(ref.SketchParams(d=D, w=W, master_seed=SEED))
+            r.apply_ops(c["ops"][:1], keys64[:1])  # compile
+            t0 = time.perf_counter()
+            r.apply_ops(c["ops"][1:], keys64[1:])
+            cpu_rate = (n - 1) / (time.perf_counter() - t0) / 1e6
+            want = r.counters
+        else:
+            from oracle import oracle as orc
 
-        o = orc.OracleSketch("cm", D, W, master_seed=SEED)
-        t0 = time.perf_counter()
-        o.apply_ops(c["ops"], c["keys"].astype(np.uint64))
-        out["cpu_port_Mitems_s"] = round(n / (time.perf_counter() - t0) / 1e6, 2)
-        assert np.array_equal(cm.counters.cpu().numpy(), o.slim), "CM counters differ from the oracle"
-        out["parity"] = "counters bit-exact vs oracle"
+            o = orc.OracleSketch("cm", D, W, master_seed=SEED)
+            t0 = time.perf_counter()
+            o.apply_ops(c["ops"], keys64)
+            cpu_rate = n / (time.perf_counter() - t0) / 1e6
+            want = o.slim
+        out["cpu_Mitems_s"] = round(cpu_rate, 2)
+        out["cpu_kind"] = kind
+        out["cpu_ratio"] = round(out["Mitems_s"] / cpu_rate, 1)
+        assert np.array_equal(cm.counters.cpu().numpy(), want), "CM counters differ from the CPU reference"
+        out["parity"] = f"counters bit-exact vs the CPU {kind}"
     return out
 
 
@@ -487,21 +595,58 @@ def run_ours(args):
     cm_leg = None if args.no_cm else run_cm_leg(args, world, rank, dev)
 
     # ------------------------------------------------ parity gate + CPU baseline (rank 0, N=1)
-    cpu = None
-    if rank == 0:
-        from oracle import oracle as orc
-
-        sample_n = 100_000_000
+    cpu = cpu_port = None
+    cpu_build_s = cpu_q_rate = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        kind, ref = cpu_kind(args)
+        threads = len(os.sched_getaffinity(0))
+        sample_n = 50_000_000
         qs = qkeys[:sample_n].cpu().numpy()
-        threads = orc.max_threads()
-        if not args.no_cpu_baseline and world == 1:
-            v, tb, tq, sample, o = cpu_measure(args, stream, qs, threads)
-            cpu = {"value": round(v, 3), "unit": "Mitems/s", "cores": threads, "kind": "port", "sample": sample,
-                   "build_s": round(tb, 3)}
-            ok = (np.array_equal(sk.slim.counters.cpu().numpy(), o.slim)
-                  and np.array_equal(sk.fat.counters.cpu().numpy(), o.fat)
-                  and np.array_equal(qout[:sample_n].cpu().numpy(), o.query_many(qs, threads=threads)))
-            assert ok, "GPU state differs from the oracle"
+        gpu_slim, gpu_fat = sk.slim.counters.cpu().numpy(), sk.fat.counters.cpu().numpy()
+        gpu_est = qout[:sample_n].cpu().numpy()
+        for k in ([kind, "port"] if kind == "reference" else ["port"]):
+            v, tb, tq, sample, csk, est_c = cpu_measure(args, stream, qs, threads, k, ref)
+            c_slim, c_fat = cpu_state(k, csk)
+            ok = (np.array_equal(gpu_slim, c_slim) and np.array_equal(gpu_fat, c_fat)
+                  and np.array_equal(gpu_est, est_c))
+            assert ok, f"GPU state differs from the CPU {k}"
+            entry = {"value": round(v, 3), "unit": "Mitems/s", "cores": threads, "kind": k, "sample": sample,
+                     "build_s": round(tb, 3), "query_Mitems_s": round(qs.shape[0] / tq / 1e6, 2),
+                     "parity": "slim, fat and the sample's estimates bit-exact vs the GPU run", "cpu": cpu_model()}
+            if cpu is None:
+                cpu, cpu_build_s, cpu_q_rate = entry, tb, qs.shape[0] / tq / 1e6
+            else:
+                cpu_port = entry
+
+    # ------------------------------------------------ insert and query as first-class figures
+    g4 = float(gather.get("gather_4MiB_Gps", 0.0)) if gather else 0.0
+    ins_rate = n_ops * (world if rep else 1) / (build_ms * 1e-3) / 1e6 if build_ms else None
+    insert = {"Mitems_s": round(ins_rate, 2) if ins_rate else None, "ms": round(build_ms, 3), "ops": n_ops,
+              "engine_ms": round(eng_ms, 3) if eng_ms > 0 else None, "touches_per_item": 8,
+              "touches_note": "SURVEY §8(d): 4 fat RMW + 4 slim reads per insert (+ the slim raises), "
+                              "SFF deletes 4 fat RMW + 4 bucket reads + 4 slim RMW"}
+    if ins_rate and g4:
+        insert["gather"] = {"achieved_Gps": round(ins_rate * 8 / 1e3, 2), "peak_Gps": g4,
+                            "frac": round(ins_rate * 8 / 1e3 / g4, 4),
+                            "peak_source": "profiles/gather_peaks.json (random 4-B loads, 4 MiB L2-resident table)"}
+    if "engine" in rf and "latency_roofline" in rf["engine"]:
+        insert["latency_roofline"] = rf["engine"]["latency_roofline"]
+    if cpu_build_s:
+        insert["cpu_Mitems_s"] = round(n_ops / cpu_build_s / 1e6, 2)
+        insert["cpu_threads"] = 1
+        insert["cpu_ratio"] = round(ins_rate / insert["cpu_Mitems_s"], 1)
+    q_rate = args.queries * (world if rep else 1) / (query_ms * 1e-3) / 1e6 if query_ms else None
+    query = {"Mitems_s": round(q_rate, 1) if q_rate else None, "ms": round(query_ms, 3), "queries": args.queries,
+             "n_gpus": world, "per_gpu_Mitems_s": round(qn / q_s / 1e6, 1),
+             "kernel": qkern, "touches_per_item": 4, "hbm_frac": rf_query["frac"]}
+    if "gather" in rf_query:
+        query["gather"] = rf_query["gather"]
+    if cpu_q_rate:
+        query["cpu_Mitems_s"] = round(cpu_q_rate, 1)
+        query["cpu_threads"] = len(os.sched_getaffinity(0))
+        query["cpu_ratio"] = round(q_rate / cpu_q_rate, 1)
+    if world > 1 and not rep:
+        query["bcast_ms"] = round(bcast_ms, 3)
 
     if rank == 0:
         line = {
@@ -509,8 +654,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True,
             "scaling": "weak" if (rep or world == 1) else "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded, SURVEY.md §8(d))",
-            "config": workload_config(args, world), "breakdown": breakdown, "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e, "cm_merge": cm_leg, "gpu_launches": int(launches),
+            "config": workload_config(args, world), "insert": insert, "query": query, "breakdown": breakdown,
+            "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_port": cpu_port, "e2e": e2e,
+            "cm_merge": cm_leg, "gpu_launches": int(launches),
             "gpu_launches_note": "own kernels only (sfk_launch_count); CUB radix-sort/scan launches not counted",
             "clocks": clk,
         }

@@ -152,6 +152,18 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
                  const void* keys, int key_kind, int rec_len, int64_t n, int64_t* inc_counts,
                  int64_t* result, void* workspace, size_t workspace_bytes, int flags, void* stream);
 
+/* Raw signed count-min update (no reference counterpart; the building block
+ * of stream-sharded CM builds, distributed.sharded_cm_apply, which replaces
+ * one _kernels.cm_apply call, _kernels.py:62-88, by per-rank shards):
+ * counters[i, h_i(key_t)] += 1 for an insert and -= 1 for a delete, modulo
+ * 2^32, with no saturation or phantom checks and no tallies. The caller
+ * proves that no op of the whole batch can fail (sfk_cm_apply's precheck:
+ * max counter + inserts <= 2^32 - 1, and no deletes or min counter >=
+ * deletes), so summing the shards' deltas equals the sequential apply.
+ * d <= 8. Warp-aggregated atomics; asynchronous on `stream`. */
+int sfk_cm_delta(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops,
+                 const void* keys, int key_kind, int rec_len, int64_t n, void* stream);
+
 /* Replaces _kernels.cu_apply (_kernels.py:91-115), called from
  * CuSketch.apply_ops (baselines.py:156-162). */
 size_t sfk_cu_workspace_size(int d, int64_t w, int64_t n);

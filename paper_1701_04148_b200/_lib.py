@@ -30,6 +30,7 @@ EXPORTS = (
     "sfk_min_query",
     "sfk_cm_workspace_size",
     "sfk_cm_apply",
+    "sfk_cm_delta",
     "sfk_cu_workspace_size",
     "sfk_cu_apply",
     "sfk_sf_workspace_size",
@@ -95,6 +96,7 @@ def load_library() -> ctypes.CDLL:
     apply_args = [P, P, I, I64, P, P, I, I, I64, P, P, P, SZ, I, P]
     L.sfk_cm_apply.argtypes = apply_args
     L.sfk_cu_apply.argtypes = apply_args
+    L.sfk_cm_delta.argtypes = [P, P, I, I64, P, P, I, I, I64, P]
     L.sfk_sf_workspace_size.argtypes = [I, I, I64, I64, I, I64]
     L.sfk_sf_workspace_size.restype = SZ
     L.sfk_sf_apply.argtypes = [I, P, P, P, P, P, I, I64, I64, I, P, P, I, I, I64, P, P, P, SZ, I, P]

@@ -93,10 +93,30 @@ class CmSketch(_CounterSketch):
     def allreduce_(self, group=None) -> None:
         """Merge stream-sharded replicas in place: counters and tallies are
         sums over shards (count-min updates commute). uint32 counters travel
-        as int32; two's-complement sums wrap exactly like uint32 sums."""
+        as int32; two's-complement sums wrap exactly like uint32 sums, and a
+        merged counter above 2^32 - 1 raises ``SaturationError`` on every
+        rank."""
         from .distributed import allreduce_counters_
 
         self.insertions_seen = allreduce_counters_(self.counters, self.increment_counts, self.insertions_seen, group)
+
+    def sharded_apply_(self, ops, keys, group=None) -> None:
+        """``apply_ops`` over a batch every rank holds, computed by all ranks
+        together (``distributed.sharded_cm_apply``)."""
+        from .distributed import sharded_cm_apply
+
+        sharded_cm_apply(self, ops, keys, group)
+
+    # hooks of distributed.sharded_cm_apply
+    _normalize = staticmethod(normalize_stream)
+    _raise_for_status = staticmethod(raise_for_status)
+
+    def _cm_delta_(self, delta: torch.Tensor, ops_t: torch.Tensor, kb) -> None:
+        """Raw signed +-1 per row into `delta` (mod 2^32, no checks)."""
+        L = _lib.lib()
+        p = self.params
+        _lib.check(L.sfk_cm_delta(delta.data_ptr(), self._seeds.ctypes.data, p.d, p.w, ops_t.data_ptr(), kb.ptr(),
+                                  kb.kind, kb.rec_len, kb.n, _lib.stream_ptr()), "sfk_cm_delta")
 
 
 class CuSketch(_CounterSketch):

@@ -262,6 +262,17 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
   });
 }
 
+int sfk_cm_delta(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const uint8_t* ops, const void* keys,
+                 int key_kind, int rec_len, int64_t n, void* stream) {
+  if (check_common(d, w, key_kind, rec_len)) return 1;
+  if (d > MAXD) {
+    set_error("sfk_cm_delta: d=%d exceeds %d", d, MAXD);
+    return 1;
+  }
+  if (n <= 0) return 0;
+  return cm_fast(counters, seeds, d, w, ops, KeySrc{keys, key_kind, rec_len}, n, (cudaStream_t)stream);
+}
+
 size_t sfk_cu_workspace_size(int d, int64_t w, int64_t n) {
   if (d > MAXD) return 256;
   return parallel_workspace_size(2, d, w, 0, 1, std::min<int64_t>(n, chunk_ops(d, 1)));
