@@ -323,11 +323,15 @@ struct ScanOut {
   uint32_t D;
   uint32_t row_cells;
   Ctl* ctl;
+  uint32_t* tkey;            // WRITE_OBS 6: [e] the op t of sorted element e
+  uint32_t* tval;            //   and its post-op own fat count (b_min candidates, min-reduced per op later)
 };
 
 // WRITE_OBS: 0 none, 1 obs (b_min / bucket max), 2 obs2 (own count, max of the others),
 //            3 obs2 (own count, sum of the others clamped to 2^32 - 1: the SF2/SF3/SF4 trigger)
 //            5 obs (CU drop pass: 1 + an upper bound of each op's minimum; fat_init = the slim)
+//            6 tkey / tval (SF1 / SF2 b_min: (t, post-op own count) per element in cell order,
+//              coalesced; bmin_from_pairs reduces them per op)
 template <int Z, bool HAS_FAT, int WRITE_OBS, bool WRITE_LINKS>
 __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ vals, uint32_t N, int kb,
@@ -385,6 +389,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
           o.obs2[(size_t)t * o.D + row] = make_uint2((uint32_t)post_own, others);
         }
       }
+      if (WRITE_OBS == 6) {
+        o.tkey[e] = t;
+        o.tval[e] = (uint32_t)min(post_own, (int64_t)U32MAX);
+      }
       if (WRITE_OBS == 4) {
         // b_min of op t = min over its d rows of the post-op own fat count:
         // one 4-B atomicMin per (op, row) into a per-op word (a scattered
@@ -434,6 +442,29 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
   if (HAS_FAT && local_fail != NONE32) atomicMin(&o.ctl->fail_t, local_fail);
 }
 
+
+// ---------------------------------------------------------------- SF1 / SF2: b_min per op
+// b_min of op t = min over its d rows of its post-op own fat count. The fat
+// scan runs in cell order, so the d candidates of an op sit at random
+// places; rather than a 4-B atomicMin per (op, row) into a per-op array far
+// larger than L2 (every atomic a DRAM sector fill and write-back: cfg 4's
+// scan moved 34.7 GB), the scan writes (t, candidate) pairs in place, a
+// partial radix sort on t's bits above BMIN_BITS groups them into ranges of
+// 2^BMIN_BITS consecutive ops (every op has exactly d pairs, so range b
+// starts at pair d b 2^BMIN_BITS), and one CTA per range takes the minima in
+// shared memory.
+constexpr int BMIN_BITS = 13;
+__global__ void __launch_bounds__(512) bmin_bucket_k(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ tval,
+                                                     uint32_t n, uint32_t d, uint32_t* __restrict__ obs) {
+  __shared__ uint32_t bm[1 << BMIN_BITS];
+  const uint32_t t0 = blockIdx.x << BMIN_BITS, cnt = min(n - t0, 1u << BMIN_BITS);
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) bm[i] = U32MAX;
+  __syncthreads();
+  const size_t p1 = ((size_t)t0 + cnt) * d;
+  for (size_t p = (size_t)t0 * d + threadIdx.x; p < p1; p += blockDim.x) atomicMin(bm + (tkey[p] - t0), tval[p]);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) obs[t0 + i] = bm[i];
+}
 
 // ---------------------------------------------------------------- SF1 / CU: ignorable (op, row) pairs
 // An SF1 slim cell never drops below the batch net count of any key that maps
@@ -2621,6 +2652,28 @@ __global__ void fold_scatter_k(const uint32_t* __restrict__ grp, uint32_t* __res
 
 int launch_load_keys(KeySrc ks, int64_t n, uint64_t* out, cudaStream_t st);  // sfk_query.cu
 
+// per-op b_min from the fat scan's (t, candidate) pairs in k_in / v_in (see
+// bmin_bucket_k); uses k_out / v_out (the fat-sorted pairs are dead by then)
+static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_t st) {
+  const int tbits = bits_for((uint64_t)n);
+  const uint32_t* tk = L.k_in;
+  const uint32_t* tv = L.v_in;
+  if (tbits > BMIN_BITS) {
+    size_t bytes = L.cub_tmp_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N,
+                                                    BMIN_BITS, tbits, st);
+    if (e != cudaSuccess) {
+      set_error("b_min sort: %s", cudaGetErrorString(e));
+      return (int)e;
+    }
+    tk = L.k_out;
+    tv = L.v_out;
+  }
+  const uint32_t nb = (n + (1u << BMIN_BITS) - 1) >> BMIN_BITS;
+  { note_launch(); bmin_bucket_k<<<nb, 512, 0, st>>>(tk, tv, n, (uint32_t)d, L.obs); }
+  return check_launch("bmin_bucket");
+}
+
 // SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
 static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st) {
   const int sms = sm_count();
@@ -2671,9 +2724,9 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
     if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
-    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
-    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
-    if (int r = run_scan_z<true, 4, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl, L.k_in, L.v_in};
+    if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    if (int r = bmin_from_pairs(L, n, N, D, st)) return r;
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
@@ -2726,9 +2779,9 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
     if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
-    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl};
-    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
-    if (int r = run_scan_z<true, 4, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl, L.k_in, L.v_in};
+    if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+    if (int r = bmin_from_pairs(L, n, N, D, st)) return r;
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;

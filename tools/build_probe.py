@@ -22,6 +22,10 @@ if variant == "cu":
     c = W.cfg2(seed=2017)
     ops, keys = torch.from_numpy(c["ops"]).to(dev), torch.from_numpy(c["keys"]).to(dev)
     params = P.SketchParams(d=4, w=65536, master_seed=2017)
+elif cfg == "1":
+    c = W.cfg1(seed=2017)
+    ops, keys = torch.from_numpy(c["ops"]).to(dev), torch.from_numpy(c["keys"]).to(dev)
+    params = P.SketchParams(d=4, w=16384, w_prime=65536, master_seed=2017)
 elif cfg == "4":
     c = W.cfg4(seed=2017)
     ops, keys = torch.from_numpy(c["ops"]).to(dev), torch.from_numpy(c["records"]).to(dev)
