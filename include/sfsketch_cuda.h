@@ -52,6 +52,12 @@ extern "C" {
 #define SFK_PHANTOM 1
 #define SFK_SATURATED 2
 #define SFK_UNSUPPORTED 3
+/* an op code other than 0 (insert) / 1 (delete): nothing of the batch is
+ * applied and op_index is the first such op (the reference rejects the batch
+ * in normalize_stream before any kernel runs, _ops.py:27-34, with
+ * ConfigurationError). Checked on the device by sfk_sf_apply, sfk_cm_apply
+ * and sfk_cu_apply. */
+#define SFK_BAD_OPCODE 4
 
 /* SF variant codes: sf.py:57 (_FLAT_VARIANT_CODE) and sf.py:171-172 (mode) */
 #define SFK_VARIANT_SF1 1

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("SFK_LIB_PATH") or os.path.join(_HERE, "_lib", "libsfs
 CSRC = os.path.join(_HERE, "csrc")
 
 KEY_U64, KEY_U32, KEY_RECORD = 0, 1, 2
-OK, PHANTOM, SATURATED, UNSUPPORTED = 0, 1, 2, 3
+OK, PHANTOM, SATURATED, UNSUPPORTED, BAD_OPCODE = 0, 1, 2, 3, 4
 VARIANT_CODE = {"sf1": 1, "sf2": 2, "sf3": 3, "sf4": 4, "sff": 6}
 FLAG_SEQUENTIAL = 1
 

@@ -107,7 +107,14 @@ def normalize_keys(keys) -> KeyBatch:
     raise ConfigurationError(f"keys must be integers, got {t.dtype}")
 
 
-def normalize_stream(ops, keys):
+BAD_OPCODE_MSG = "op codes must be 0 (insert) or 1 (delete)"
+
+
+def normalize_stream(ops, keys, check_ops: bool = True):
+    """``_ops.py:27-34``. ``check_ops=False``: the op codes are validated on
+    the device by the apply itself (SF, CM, CU: status BAD_OPCODE, nothing
+    applied, raised as the same ConfigurationError by raise_for_status), which
+    saves a reduction and a host sync per batch."""
     dev = device()
     kb = normalize_keys(keys)
     if isinstance(ops, torch.Tensor):
@@ -119,8 +126,8 @@ def normalize_stream(ops, keys):
     if o.dtype != torch.uint8:
         o = o.to(torch.uint8) if o.device == dev else o.to(torch.uint8)
     o = _to_device(o, dev)
-    if kb.n and bool((o > OP_DELETE).any()):
-        raise ConfigurationError("op codes must be 0 (insert) or 1 (delete)")
+    if check_ops and kb.n and bool((o > OP_DELETE).any()):
+        raise ConfigurationError(BAD_OPCODE_MSG)
     return o, kb
 
 
@@ -135,6 +142,8 @@ def raise_for_status(status: int, op_index: int, keys: KeyBatch) -> None:
     """``_ops.py:44-59``: the same exception types and messages."""
     if status == _lib.OK:
         return
+    if status == _lib.BAD_OPCODE:
+        raise ConfigurationError(BAD_OPCODE_MSG)
     key = keys.key_at(op_index)
     if status == _lib.PHANTOM:
         raise PhantomDeletionError(f"op {op_index}: deleting key {key} would drive a counter below zero")

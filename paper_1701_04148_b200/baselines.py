@@ -37,6 +37,7 @@ from .sf import query_min
 class _CounterSketch:
     kind = ""
     supports_deletion = True
+    _device_checks_ops = False
     _entry = ""
     _ws_entry = ""
 
@@ -56,7 +57,8 @@ class _CounterSketch:
         self.apply_ops(*single_op(OP_DELETE, key))
 
     def apply_ops(self, ops, keys, *, sequential: bool = False) -> None:
-        ops_t, kb = normalize_stream(ops, keys)
+        # CM / CU validate op codes on the device (status BAD_OPCODE)
+        ops_t, kb = normalize_stream(ops, keys, check_ops=not self._device_checks_ops)
         result = self._submit(ops_t, kb, sequential)
         status, bad, n_ins = Scratch.read(result)
         self.insertions_seen += n_ins
@@ -89,6 +91,7 @@ class CmSketch(_CounterSketch):
     supports_deletion = True
     _entry = "sfk_cm_apply"
     _ws_entry = "sfk_cm_workspace_size"
+    _device_checks_ops = True
 
     def allreduce_(self, group=None) -> None:
         """Merge stream-sharded replicas in place: counters and tallies are
@@ -127,6 +130,7 @@ class CuSketch(_CounterSketch):
     supports_deletion = False
     _entry = "sfk_cu_apply"
     _ws_entry = "sfk_cu_workspace_size"
+    _device_checks_ops = True
 
     def delete(self, key: int) -> None:
         raise UnsupportedOperationError("conservative update cannot be reversed; deletion is unsupported")

@@ -144,6 +144,23 @@ static int check_common(int d, int64_t w, int key_kind, int rec_len) {
   return 0;
 }
 
+// A batch split into several chunks is checked for bad op codes (anything
+// but 0 / 1) before the first chunk runs, so a rejected batch applies
+// nothing; single-chunk batches are checked on the device inside the apply.
+static int bad_ops_first(const uint8_t* ops, int64_t n, int64_t chunk, void* ws, size_t ws_bytes, int64_t* result,
+                         cudaStream_t st, bool* rejected) {
+  *rejected = false;
+  if (n <= chunk) return 0;
+  Stats s;
+  if (int r = collect_stats(ops, n, nullptr, 0, ws, ws_bytes, &s, st)) return r;
+  if (s.first_bad < (unsigned long long)n) {
+    *rejected = true;
+    { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_BAD_OPCODE, (int64_t)s.first_bad, 0, nullptr, 0, 0); }
+    return check_launch("set_result");
+  }
+  return 0;
+}
+
 // Run `body(t0, cnt, result)` over chunks; accumulate {status, op_index, n_ins}.
 template <typename F>
 static int chunked(int64_t n, int64_t chunk, int64_t* result, cudaStream_t st, F body) {
@@ -246,10 +263,17 @@ int sfk_cm_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
   if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD || small_batch(n))
     return launch_seq_apply(0, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops,
                             KeySrc{keys, key_kind, rec_len}, nullptr, n, inc_counts, result, st);
+  bool rejected = false;
+  if (int r = bad_ops_first(ops, n, chunk_ops(d, 1), workspace, workspace_bytes, result, st, &rejected)) return r;
+  if (rejected) return 0;
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
     KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
     Stats s;
     if (int r = collect_stats(ops + t0, cnt, counters, (int64_t)d * w, workspace, workspace_bytes, &s, st)) return r;
+    if (s.first_bad < (unsigned long long)cnt) {  // reject the batch: nothing applied
+      { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_BAD_OPCODE, (int64_t)s.first_bad, 0, nullptr, 0, 0); }
+      return check_launch("set_result");
+    }
     // no insert can meet a saturated counter and no delete a zero one
     const bool safe = ((uint64_t)s.cmax + s.n_ins <= 0xFFFFFFFFull) && (s.n_del == 0 || (uint64_t)s.cmin >= s.n_del);
     if (safe) {
@@ -287,10 +311,17 @@ int sfk_cu_apply(uint32_t* counters, const uint64_t* seeds, int d, int64_t w, co
   if ((flags & SFK_FLAG_SEQUENTIAL) || d > MAXD || small_batch(n))
     return launch_seq_apply(1, 0, counters, nullptr, nullptr, seeds, nullptr, d, w, 0, 1, ops, all, nullptr, n,
                             inc_counts, result, st);
+  bool rejected = false;
+  if (int r = bad_ops_first(ops, n, chunk_ops(d, 1), workspace, workspace_bytes, result, st, &rejected)) return r;
+  if (rejected) return 0;
   return chunked(n, chunk_ops(d, 1), result, st, [&](int64_t t0, int64_t cnt) -> int {
     KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
     Stats s;
     if (int r = collect_stats(ops + t0, cnt, counters, (int64_t)d * w, workspace, workspace_bytes, &s, st)) return r;
+    if (s.first_bad < (unsigned long long)cnt) {  // reject the batch: nothing applied
+      { note_launch(); set_result_k<<<1, 1, 0, st>>>(result, SFK_BAD_OPCODE, (int64_t)s.first_bad, 0, nullptr, 0, 0); }
+      return check_launch("set_result");
+    }
     // the CU min can reach 0xFFFFFFFF only if some counter climbs that far:
     // counters grow by at most one per insert
     if ((uint64_t)s.cmax + s.ins_before_first_del < 0xFFFFFFFFull)
@@ -346,6 +377,10 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
     return launch_seq_apply(3, variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, nullptr, slim_seeds, fat_seeds, d, w, 0,
                             z, ops, all, nullptr, n, inc_counts, result, st);
   }
+  bool rejected = false;
+  if (int r = bad_ops_first(ops, n, chunk_ops(d, kind_z(kind, z)), workspace, workspace_bytes, result, st, &rejected))
+    return r;
+  if (rejected) return 0;
   return chunked(n, chunk_ops(d, kind_z(kind, z)), result, st, [&](int64_t t0, int64_t cnt) -> int {
     KeySrc ks{key_ptr(keys, key_kind, rec_len, t0), key_kind, rec_len};
     return parallel_apply(kind, slim, fat, dsub, slim_seeds, fat_seeds, d, w, w_prime, z, ops + t0, ks, cnt,

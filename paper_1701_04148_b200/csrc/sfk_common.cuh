@@ -116,6 +116,7 @@ struct Stats {
   unsigned long long first_del;  // min index of a delete (or n)
   unsigned long long ins_before_first_del;
   uint32_t cmax, cmin;
+  unsigned long long first_bad;  // min index of an op code other than 0 / 1 (or n)
 };
 
 // per-op gate inputs of the gated engine kinds (sfk_sf.cu kinds 7 and 8)

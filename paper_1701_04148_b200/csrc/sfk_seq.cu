@@ -40,6 +40,15 @@ __global__ void seq_apply_k(SeqArgs a, int kind, int variant) {
   int64_t n_ins = 0;
   int64_t status = SFK_OK, bad = -1;
   const int64_t w = a.w, wp = a.wp, z = a.z;
+  if (a.ops) {  // a bad op code rejects the whole batch before anything is applied
+    for (int64_t t = 0; t < a.n; ++t)
+      if (a.ops[t] > 1) {
+        a.result[0] = SFK_BAD_OPCODE;
+        a.result[1] = t;
+        a.result[2] = 0;
+        return;
+      }
+  }
   for (int64_t t = 0; t < a.n; ++t) {
     const uint64_t key = load_key(a.keys, t);
     const int op = a.ops ? a.ops[t] : 0;

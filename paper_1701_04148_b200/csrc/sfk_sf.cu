@@ -118,7 +118,7 @@ struct Ctl {
   unsigned long long n_ins;  // inserts applied (t < t*)
   uint32_t qhead, qtail;     // engine ready queue
   uint32_t executed;         // engine runs finished
-  uint32_t pad;
+  uint32_t bad_op;           // first op whose code is not 0 / 1 (NONE32: none); the batch is then a no-op
 };
 
 // ---------------------------------------------------------------- 1. hash_emit
@@ -145,10 +145,12 @@ struct HashArgs {
 
 template <int D, int KIND>
 __global__ void __launch_bounds__(256) hash_emit_k(HashArgs<D> a) {
-  uint32_t local_fail = NONE32;
+  uint32_t local_fail = NONE32, local_bad = NONE32;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = load_key(a.keys, t);
-    const uint32_t op = a.ops[t];
+    const uint32_t code = a.ops[t];
+    const uint32_t op = code != 0;  // anything but 0 / 1 makes the batch a no-op (t* = 0, below)
+    if (code > 1 && local_bad == NONE32) local_bad = (uint32_t)t;
     if (a.unsupported_deletes && op != 0 && local_fail == NONE32) local_fail = (uint32_t)t;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -167,6 +169,12 @@ __global__ void __launch_bounds__(256) hash_emit_k(HashArgs<D> a) {
   }
   // grid-stride order means a thread's first delete is its smallest
   if (local_fail != NONE32) atomicMin(&a.ctl->fail_t, local_fail);
+  // a bad op code: report the first one and apply nothing (every op counts as
+  // at or after the failing op, so the fat is undone and no run is replayed)
+  if (local_bad != NONE32) {
+    atomicMin(&a.ctl->bad_op, local_bad);
+    atomicMin(&a.ctl->fail_t, 0u);
+  }
 }
 
 // ---------------------------------------------------------------- 3. segscan
@@ -2027,6 +2035,7 @@ __global__ void ctl_init_k(Ctl* ctl) {
   ctl->qhead = 0;
   ctl->qtail = 0;
   ctl->executed = 0;
+  ctl->bad_op = NONE32;
 }
 
 // undo the fat deltas of ops t >= t* (the fat was written for the whole
@@ -2051,6 +2060,12 @@ __global__ void fat_undo_k(HashArgs<D> a, uint32_t* __restrict__ fat, uint32_t z
 // result = {status, op_index, n_ins}; CM tallies (+n_ins per row)
 __global__ void finalize_k(const Ctl* ctl, const uint8_t* __restrict__ ops, int variant_kind, int64_t* result,
                            unsigned long long* inc, int d, int cm_tallies) {
+  if (ctl->bad_op != NONE32) {
+    result[0] = SFK_BAD_OPCODE;
+    result[1] = (int64_t)ctl->bad_op;
+    result[2] = 0;
+    return;
+  }
   const uint32_t ts = ctl->fail_t;
   int64_t status = SFK_OK;
   if (ts != NONE32) {
@@ -2109,20 +2124,24 @@ __global__ void __launch_bounds__(256) cm_atomic_k(uint32_t* __restrict__ counte
 
 
 __global__ void stats_ops_k(const uint8_t* __restrict__ ops, int64_t n, Stats* st) {
-  unsigned long long ins = 0, del = 0, fd = 0xFFFFFFFFFFFFFFFFull;
+  unsigned long long ins = 0, del = 0, fd = 0xFFFFFFFFFFFFFFFFull, fb = 0xFFFFFFFFFFFFFFFFull;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    if (ops[t]) { ++del; if ((unsigned long long)t < fd) fd = t; }
+    const uint8_t o = ops[t];
+    if (o) { ++del; if ((unsigned long long)t < fd) fd = t; }
     else ++ins;
+    if (o > 1 && (unsigned long long)t < fb) fb = t;
   }
   for (int off = 16; off > 0; off >>= 1) {
     ins += __shfl_down_sync(0xffffffffu, ins, off);
     del += __shfl_down_sync(0xffffffffu, del, off);
     fd = min(fd, __shfl_down_sync(0xffffffffu, fd, off));
+    fb = min(fb, __shfl_down_sync(0xffffffffu, fb, off));
   }
   if ((threadIdx.x & 31) == 0) {
     if (ins) atomicAdd(&st->n_ins, ins);
     if (del) atomicAdd(&st->n_del, del);
     if (fd != 0xFFFFFFFFFFFFFFFFull) atomicMin(&st->first_del, fd);
+    if (fb != 0xFFFFFFFFFFFFFFFFull) atomicMin(&st->first_bad, fb);
   }
 }
 __global__ void stats_ins_before_k(const uint8_t* __restrict__ ops, Stats* st) {
@@ -2889,6 +2908,7 @@ int collect_stats(const uint8_t* ops, int64_t n, const uint32_t* counters, int64
   Stats* s = cv.take<Stats>(1);
   Stats init{};
   init.first_del = (unsigned long long)n;
+  init.first_bad = (unsigned long long)n;
   init.cmax = 0;
   init.cmin = U32MAX;
   cudaMemcpyAsync(s, &init, sizeof(Stats), cudaMemcpyHostToDevice, st);

@@ -192,11 +192,11 @@ class SfSketch:
             raise UnsupportedOperationError(
                 "sketch already ran in oracle-assisted mode; regular updates would break it"
             )
-        ops_t, kb = normalize_stream(ops, keys)
-        if kb.n:
-            self._used_normal = True
+        ops_t, kb = normalize_stream(ops, keys, check_ops=False)  # op codes checked on the device
         result = self._submit(ops_t, kb, sequential)
         status, bad, n_ins = Scratch.read(result)
+        if kb.n and status != _lib.BAD_OPCODE:  # a rejected batch leaves the sketch untouched
+            self._used_normal = True
         self.slim.insertions_seen += n_ins
         raise_for_status(status, bad, kb)
 

@@ -299,3 +299,49 @@ def test_tiny_batches_both_engines_match_oracle(oracle, kind):
                 a = b
         finally:
             L.sfk_small_batch_ops(prev)
+
+
+def _state(sk):
+    if isinstance(sk, P.SfSketch):
+        parts = [sk.slim.counters, sk.slim.increment_counts, sk.fat.counters]
+        if sk.deletion_sub is not None:
+            parts.append(sk.deletion_sub.counters)
+        return [host(p).copy() for p in parts] + [sk.slim.insertions_seen]
+    return [host(sk.counters).copy(), host(sk.increment_counts).copy(), sk.insertions_seen]
+
+
+@pytest.mark.parametrize("kind", ALL + ("cm", "cu"))
+@pytest.mark.parametrize("n,bad_at", [(5, 3), (40, 0), (5000, 4321), (5000, 1)])
+@pytest.mark.parametrize("sequential", [False, True])
+@pytest.mark.parametrize("code", [2, 255])
+def test_bad_op_codes_reject_the_whole_batch_on_the_device(kind, n, bad_at, sequential, code):
+    """An op code other than 0 / 1 anywhere in the batch: ConfigurationError
+    with the reference's message (_ops.py:27-34) and nothing applied, ops
+    before it included. The SF / CM / CU applies check the codes on the device
+    (status SFK_BAD_OPCODE) on the one-thread engine (<= 32 ops or
+    sequential=True) and on the parallel pipeline alike."""
+    from paper_1701_04148_b200.errors import ConfigurationError
+
+    sk = make_sketch(kind, 4, 256, 4, 1024, 11)
+    rng = np.random.default_rng(n + bad_at)
+    warm = rng.integers(0, 1000, size=3000, dtype=np.uint64)
+    sk.apply_ops(np.zeros(warm.size, np.uint8), warm)
+    before = _state(sk)
+    keys = torch.from_numpy(rng.choice(warm, size=n)).cuda()
+    ops = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    ops[bad_at] = code
+    with pytest.raises(ConfigurationError, match="op codes must be 0"):
+        sk.apply_ops(ops, keys, sequential=sequential)
+    for a, b in zip(before, _state(sk)):
+        np.testing.assert_array_equal(a, b)
+    # the sketch is still usable, and a fresh sketch that only saw a rejected
+    # batch may still switch to the oracle-assisted mode
+    ops[bad_at] = 0
+    sk.apply_ops(ops, keys, sequential=sequential)
+    if isinstance(sk, P.SfSketch):
+        fresh = make_sketch(kind, 4, 256, 4, 1024, 11)
+        bad = torch.full((3,), 7, dtype=torch.uint8, device="cuda")
+        with pytest.raises(ConfigurationError):
+            fresh.apply_ops(bad, torch.arange(3, dtype=torch.int64, device="cuda"))
+        fresh.oracle_assisted_insert(5, 1)
+        assert fresh.query(5) == 1

@@ -105,7 +105,7 @@ def _gpu_sharded_cm_phantom(rank, world):
     ops = np.zeros(keys.size, np.uint8)
     ops[70_000] = 1
     keys[70_000] = 12345  # never inserted: the first failing op
-    cm = P.CmSketch(P.SketchParams(d=4, w=2048, master_seed=1))
+    cm = P.CmSketch(P.SketchParams(d=4, w=1 << 20, master_seed=1))
     try:
         cm.sharded_apply_(ops, keys)
     except Exception as e:  # noqa: BLE001
@@ -120,7 +120,7 @@ def test_sharded_cm_apply_gpu_fallback_raises_on_every_rank(oracle):
     ops = np.zeros(keys.size, np.uint8)
     ops[70_000] = 1
     keys[70_000] = 12345
-    o = oracle.OracleSketch("cm", 4, 2048, master_seed=1)
+    o = oracle.OracleSketch("cm", 4, 1 << 20, master_seed=1)
     st = o.apply_ops(ops, keys)
     assert st[0] == 1 and st[1] == 70_000
     assert out[0][0] == out[1][0] == "PhantomDeletionError", out
