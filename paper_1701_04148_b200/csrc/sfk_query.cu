@@ -531,6 +531,18 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
   cluster_sync_all();  // no CTA exits while peers may still touch its shared memory
 }
 
+// warp-pipelined kernel shape (A/B knobs): warps per CTA, keys per lane per
+// tile (d = 4; d = 2 uses 8, d = 8 uses 16), receive buffers per warp
+#ifndef SFK_CW_NW
+#define SFK_CW_NW 16
+#endif
+#ifndef SFK_CW_KPL
+#define SFK_CW_KPL 16
+#endif
+#ifndef SFK_CW_NB
+#define SFK_CW_NB 2
+#endif
+
 // ---- cluster path, warp-pipelined (u32 keys) ---------------------------------
 // Same row partition as min_query_cluster (CTA r of a D-CTA cluster holds slim
 // row r in shared memory), but the exchange runs per warp instead of per CTA:
@@ -562,16 +574,38 @@ __host__ __device__ __forceinline__ U32HashOff make_u32hash_off(uint64_t seed) {
   const uint32_t lo = (uint32_t)seed, hi = (uint32_t)(seed >> 32);
   return U32HashOff{lo ^ (lo >> 30) ^ (hi << 2), (hi ^ (hi >> 30)) * 0x1CE4E5B9u};
 }
+// Written in PTX so that ptxas keeps the short form (15 per key and row with
+// the shift of k30 and the gather): one 3-input LOP3 for v, the first product
+// as three FMA-pipe IMADs (lo, hi + the seed's high-word term, hi word of
+// K1), two funnel/xor pairs, IMAD.WIDE + 2 IMAD, and the final
+// (x ^ x >> 31) & mask as one SHF + one LOP3. (From C++ the compiler
+// re-associates v through key ^ seed and adds a carry chain: ~17.5.)
+// k30 = key >> 30.
 template <int SH>
-__device__ __forceinline__ uint32_t row_off_u32(uint32_t key, uint32_t k30, const U32HashOff& h, uint32_t mask_b) {
+__device__ __forceinline__ uint32_t row_off_u32(uint32_t key, uint32_t k30, uint32_t c0, uint32_t c2, uint32_t mask_b) {
   constexpr uint64_t K2S = 0x94D049BB133111EBull << SH;
-  const uint32_t v = key ^ k30 ^ h.c0;
-  const uint64_t z = (uint64_t)v * 0x1CE4E5B9u + ((uint64_t)h.c2 << 32);  // v * K1, low word of K1
-  const uint32_t zlo = (uint32_t)z, zhi = (uint32_t)(z >> 32) + v * 0xBF58476Du;
-  const uint32_t ylo = zlo ^ __funnelshift_r(zlo, zhi, 27), yhi = zhi ^ (zhi >> 27);
-  const uint64_t x = (uint64_t)ylo * (uint32_t)K2S;
-  const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32) + ylo * (uint32_t)(K2S >> 32) + yhi * (uint32_t)K2S;
-  return (xlo ^ __funnelshift_r(xlo, xhi, 31)) & mask_b;
+  uint32_t r;
+  asm("{\n\t"
+      ".reg .b32 v, zl, zh, t, yl, yh, xl, xh;\n\t"
+      ".reg .b64 x;\n\t"
+      "lop3.b32 v, %1, %2, %3, 0x96;\n\t"
+      "mul.lo.u32 zl, v, 0x1CE4E5B9;\n\t"
+      "mad.hi.u32 zh, v, 0x1CE4E5B9, %4;\n\t"
+      "mad.lo.u32 zh, v, 0xBF58476D, zh;\n\t"
+      "shf.r.wrap.b32 t, zl, zh, 27;\n\t"
+      "xor.b32 yl, zl, t;\n\t"
+      "shr.u32 t, zh, 27;\n\t"
+      "xor.b32 yh, zh, t;\n\t"
+      "mul.wide.u32 x, yl, %6;\n\t"
+      "mov.b64 {xl, xh}, x;\n\t"
+      "mad.lo.u32 xh, yl, %7, xh;\n\t"
+      "mad.lo.u32 xh, yh, %6, xh;\n\t"
+      "shf.r.wrap.b32 t, xl, xh, 31;\n\t"
+      "lop3.b32 %0, xl, t, %5, 0x28;\n\t"
+      "}"
+      : "=r"(r)
+      : "r"(key), "r"(k30), "r"(c0), "r"(c2), "r"(mask_b), "n"((uint32_t)K2S), "n"((uint32_t)(K2S >> 32)));
+  return r;
 }
 
 template <int D, typename CT, int NW, int KPL, int NB, bool POW2>
@@ -760,7 +794,7 @@ __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __res
       for (int u = 0; u < 4; ++u) {
         uint32_t off;
         if constexpr (POW2)
-          off = row_off_u32<SH>(kx[u], kx[u] >> 30, hh, mask_b);
+          off = row_off_u32<SH>(kx[u], kx[u] >> 30, hh.c0, hh.c2, mask_b);
         else
           off = (uint32_t)fmod64(mix64((uint64_t)kx[u] ^ seed), wm) << SH;
         c[4 * j + u] = *reinterpret_cast<const CT*>(rowb + off);
@@ -783,17 +817,7 @@ __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __res
   cluster_sync_all();  // no CTA exits while peers may still touch its shared memory
 }
 
-// warp-pipelined kernel shape (A/B knobs): warps per CTA, keys per lane per
-// tile (d = 4; d = 2 uses 8, d = 8 uses 16), receive buffers per warp
-#ifndef SFK_CW_NW
-#define SFK_CW_NW 16
-#endif
-#ifndef SFK_CW_KPL
-#define SFK_CW_KPL 16
-#endif
-#ifndef SFK_CW_NB
-#define SFK_CW_NB 2
-#endif
+
 
 
 // Launch the warp-pipelined cluster kernel for u32 keys (16-B aligned keys and
