@@ -139,6 +139,13 @@ int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_
  * negative mode only reads. Returns the previous mode. sfk_query_last_path()
  * returns the path (1-4) the last sfk_min_query launch took. */
 int sfk_query_path(int mode);
+
+/* Small-batch engine selection (no reference counterpart). SFF / SF4 batches
+ * of at most `ops` ops (default 192; 0 = off) run on the warp-cooperative
+ * exact engine: ops in stream order, each op's d x z counter reads in one
+ * round of parallel loads, one launch and no host round trip. A negative
+ * value only reads. Returns the previous value. */
+int64_t sfk_warp_batch_ops(int64_t ops);
 int sfk_query_last_path(void);
 
 /* Two-phase form of sfk_min_query (no reference counterpart; same

@@ -155,22 +155,32 @@ def raise_for_status(status: int, op_index: int, keys: KeyBatch) -> None:
 
 
 class Scratch:
-    """Per-sketch device scratch: the result triple and a growable workspace."""
+    """Per-sketch scratch: the result triple and a growable device workspace.
+
+    The result triple lives in pinned host memory, which the kernels write
+    through its (unified-address) device mapping, so reading it back costs a
+    stream synchronisation and no copy launch."""
 
     def __init__(self):
         self.result = None
         self.ws = None
+        self._dev = None
 
     def get(self, nbytes: int):
         dev = device()
-        if self.result is None or self.result.device != dev:
-            self.result = torch.zeros(3, dtype=torch.int64, device=dev)
+        if self.result is None or self._dev != dev:
+            self.result = torch.zeros(3, dtype=torch.int64).pin_memory()
             self.ws = None
+            self._dev = dev
         if self.ws is None or self.ws.numel() < nbytes:
             self.ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
         return self.result, self.ws
 
     @staticmethod
     def read(result: torch.Tensor):
-        s, i, n = (int(v) for v in result.tolist())
+        if result.is_cuda:
+            s, i, n = (int(v) for v in result.tolist())
+        else:  # pinned, written by the device: wait for the stream, then read in place
+            torch.cuda.current_stream().synchronize()
+            s, i, n = (int(v) for v in result.tolist())
         return s, i, n

@@ -59,6 +59,9 @@ int launch_gen_query_keys(uint64_t, const uint32_t*, const uint32_t*, uint32_t, 
 int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* s_seeds,
                      const uint64_t* f_seeds, int d, int64_t w, int64_t wp, int64_t z, const uint8_t* ops, KeySrc ks,
                      const int64_t* true_counts, int64_t n, int64_t* inc, int64_t* result, cudaStream_t st);
+int launch_seqw_bucket(int variant, uint32_t* slim, uint32_t* fat, const uint64_t* s_seeds, const uint64_t* f_seeds,
+                       int d, int64_t w, int64_t z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
+                       int64_t* result, cudaStream_t st);
 size_t parallel_workspace_size(int kind, int d, int64_t w, int64_t wp, int z, int64_t n);
 int engine_stats(unsigned long long* out, int reset);
 int engine_timing(int on);
@@ -126,6 +129,16 @@ static int64_t g_small_batch = SFK_SMALL_BATCH_DEFAULT;
 static int64_t small_batch_ops() { return __atomic_load_n(&g_small_batch, __ATOMIC_RELAXED); }
 
 static bool small_batch(int64_t n) { return n > 0 && n <= small_batch_ops(); }
+
+// SFF / SF4 batches up to this many ops run on the warp-cooperative exact
+// engine (seqw_bucket_k): one launch, no host round trip, ~0.1-0.3 us per op
+// instead of the parallel pipeline's ~140 us fixed cost. sfk_warp_batch_ops()
+// sets it (0: off).
+#ifndef SFK_WARP_BATCH_DEFAULT
+#define SFK_WARP_BATCH_DEFAULT 192
+#endif
+static int64_t g_warp_batch = SFK_WARP_BATCH_DEFAULT;
+static int64_t warp_batch_ops() { return __atomic_load_n(&g_warp_batch, __ATOMIC_RELAXED); }
 
 static const char* key_ptr(const void* keys, int key_kind, int rec_len, int64_t t0) {
   const char* p = static_cast<const char*>(keys);
@@ -233,6 +246,10 @@ const char* sfk_last_error(void) { return g_err; }
 
 int64_t sfk_small_batch_ops(int64_t ops) {
   return ops < 0 ? small_batch_ops() : __atomic_exchange_n(&g_small_batch, ops, __ATOMIC_RELAXED);
+}
+
+int64_t sfk_warp_batch_ops(int64_t ops) {
+  return ops < 0 ? warp_batch_ops() : __atomic_exchange_n(&g_warp_batch, ops, __ATOMIC_RELAXED);
 }
 
 int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream) {
@@ -349,6 +366,15 @@ static int kind_z(int kind, int z) { return (kind == 0 || kind == 4 || kind == 5
 size_t sfk_sf_workspace_size(int variant, int d, int64_t w, int64_t w_prime, int z, int64_t n) {
   const int kind = sf_parallel_kind(variant, d, z, w, w_prime);
   if (kind < 0) return 256;
+  // the warp engine takes SFF / SF4 batches up to warp_batch_ops() ops
+  // without a workspace (the same test sfk_sf_apply makes; it falls back to
+  // the parallel pipeline only for shapes the warp does not fit)
+  if ((variant == SFK_VARIANT_SFF || variant == SFK_VARIANT_SF4) && n > 0 && n <= warp_batch_ops() && d <= MAXD &&
+      w < (int64_t(1) << 24)) {
+    int Z = 1;
+    while (Z < z) Z <<= 1;
+    if ((int64_t)d * Z <= 32) return 256;
+  }
   return parallel_workspace_size(kind, d, w, w_prime, z, std::min<int64_t>(n, chunk_ops(d, kind_z(kind, z))));
 }
 
@@ -370,6 +396,11 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
   if (variant == SFK_VARIANT_SF2 && dsub == nullptr) { set_error("SF2 needs the deletion sub-sketch"); return 1; }
   const int kind = sf_parallel_kind(variant, d, z, w, w_prime);
   KeySrc all{keys, key_kind, rec_len};
+  if (bucketed && !(flags & SFK_FLAG_SEQUENTIAL) && n > 0 && n <= warp_batch_ops()) {
+    const int rc = launch_seqw_bucket(variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, slim_seeds, fat_seeds, d, w, z,
+                                      ops, all, n, inc_counts, result, st);
+    if (rc >= 0) return rc;
+  }
   if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0 || small_batch(n)) {
     if (flat)
       return launch_seq_apply(2, variant, slim, fat, dsub, slim_seeds, fat_seeds, d, w, w_prime, w_prime / w, ops, all,

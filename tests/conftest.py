@@ -58,7 +58,9 @@ def parallel_engine_only():
 
     L = _lib.lib()
     prev = L.sfk_small_batch_ops(0)
+    prev_w = L.sfk_warp_batch_ops(0)
     try:
         yield
     finally:
         L.sfk_small_batch_ops(prev)
+        L.sfk_warp_batch_ops(prev_w)

@@ -283,8 +283,11 @@ def test_tiny_batches_both_engines_match_oracle(oracle, kind):
         ops[500], keys[500] = 1, 0xFFFFFFFF  # a phantom: never inserted
     wp = {"sf3": 4 * 16, "sf1": 64, "sf2": 64}.get(kind)
     sizes = [1, 2, 3, 5, 8, 13, 21, 31, 32, 33, 40] * 6
-    for small in (32, 0):
+    # (one-thread threshold, warp-engine threshold): the one-thread engine,
+    # the warp engine (SFF / SF4 only), the parallel pipeline
+    for small, warp in ((32, 0), (0, 2048), (0, 0)):
         prev = L.sfk_small_batch_ops(small)
+        prev_w = L.sfk_warp_batch_ops(warp)
         try:
             o = oracle.OracleSketch(kind, 3, 16, 4, wp, 5)
             sk = make_sketch(kind, 3, 16, 4, wp, 5)
@@ -294,11 +297,12 @@ def test_tiny_batches_both_engines_match_oracle(oracle, kind):
                 if a >= b:
                     break
                 st = o.apply_ops(ops[a:b], keys[a:b].astype(np.uint64))
-                assert apply_batches(sk, ops[a:b], keys[a:b]) == st[:2], (small, a, b)
+                assert apply_batches(sk, ops[a:b], keys[a:b]) == st[:2], (small, warp, a, b)
                 assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat if kind not in ("cm", "cu") else None)
                 a = b
         finally:
             L.sfk_small_batch_ops(prev)
+            L.sfk_warp_batch_ops(prev_w)
 
 
 def _state(sk):
@@ -345,3 +349,55 @@ def test_bad_op_codes_reject_the_whole_batch_on_the_device(kind, n, bad_at, sequ
             fresh.apply_ops(bad, torch.arange(3, dtype=torch.int64, device="cuda"))
         fresh.oracle_assisted_insert(5, 1)
         assert fresh.query(5) == 1
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_warp_engine_matches_oracle(oracle, seed):
+    """The warp-cooperative small-batch engine (SFF / SF4, d x z <= 32 after
+    rounding z up to a power of two) against the oracle: random shapes,
+    Zipf-skewed keys (repeated buckets back to back), deletes including
+    phantoms, fat presets near 2^32 (saturation), u32 / u64 / record keys,
+    several batches; states equal after every batch."""
+    from paper_1701_04148_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(9100 + seed)
+    kind = ("sff", "sf4")[seed % 2]
+    d = int(rng.integers(1, 9))
+    z = int(rng.integers(1, 9))
+    while d * (1 << (z - 1).bit_length()) > 32:
+        z = max(1, z // 2)
+    w = int(rng.choice([7, 64, 1000, 65536]))
+    n = int(rng.integers(1, 3000))
+    vocab = rng.integers(0, 1 << 62, size=int(rng.integers(1, 200)), dtype=np.uint64)
+    ranks = np.minimum(rng.zipf(1.3, size=n) - 1, vocab.size - 1)
+    keys = vocab[ranks]
+    ops = np.zeros(n, np.uint8)
+    dm = rng.random(n) < rng.choice([0.0, 0.2, 0.45])
+    ops[dm] = 1
+    o = oracle.OracleSketch(kind, d, w, z, None, seed)
+    sk = make_sketch(kind, d, w, z, None, seed)
+    if seed % 3 == 0:  # near saturation
+        o.fat[...] = np.uint32(0xFFFFFFFF - 50)
+        sk.fat.counters.fill_(0xFFFFFFFF - 50)
+    kk = rng.integers(0, 3)
+    if kk == 1:
+        keys_in = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        keys_o = keys_in.astype(np.uint64)
+    elif kk == 2:
+        recs = rng.integers(0, 256, size=(vocab.size, 13), dtype=np.uint8)[ranks]
+        keys_in, keys_o = recs, oracle.keys_from_records(recs)
+    else:
+        keys_in, keys_o = keys, keys
+    prev = L.sfk_warp_batch_ops(1 << 20)
+    try:
+        bounds = np.unique(np.concatenate([[0, n], rng.integers(0, n, size=3)]))
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            st = o.apply_ops(ops[a:b], keys_o[a:b])
+            got = apply_batches(sk, ops[a:b], keys_in[a:b])
+            assert got == st[:2], (a, b)
+            assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+            if st[0] != 0:
+                break
+    finally:
+        L.sfk_warp_batch_ops(prev)

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_api.py -x -q -k "warp or tiny or bad_op" > gpurun_out/w2_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/w2_pytest.log
+timeout 300 python tools/api_overhead.py > gpurun_out/w2_overhead.jsonl 2>&1
+timeout 600 python tools/small_batch_curve.py > gpurun_out/w2_curve.jsonl 2> gpurun_out/w2_curve.err
