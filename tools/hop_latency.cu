@@ -7,7 +7,9 @@
 // hop = half a round trip. Also measured: the same ping-pong while every other SM
 // runs 8 warps that poll random cells of a 2 MiB table (the engine's
 // background load). The engine's critical path x the idle hop latency is its
-// latency roofline.
+// latency roofline. Round 2 adds hot-spot backgrounds: the pollers hit only
+// `hot` distinct cells (1 = the ping-pong cell itself, 64 = a few hot cells
+// elsewhere), as lanes waiting on the same hot slim cells do.
 //
 // Output: one JSON object on stdout.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o hop_latency hop_latency.cu
@@ -34,7 +36,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // blocks 0 and 1: the ping-pong pair (thread 0 each); other blocks: pollers
 __global__ void pingpong(unsigned long long* cell, int rounds, unsigned long long* ns_out,
-                         unsigned long long* table, uint32_t mask, volatile int* stop) {
+                         unsigned long long* table, uint32_t mask, volatile int* stop, int hot) {
   if (blockIdx.x >= 2) {  // background load: random relaxed polls
     uint32_t s = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
     unsigned long long acc = 0;
@@ -42,7 +44,8 @@ __global__ void pingpong(unsigned long long* cell, int rounds, unsigned long lon
 #pragma unroll 4
       for (int i = 0; i < 64; ++i) {
         s ^= s << 13; s ^= s >> 17; s ^= s << 5;
-        acc += ld_rel(table + (s & mask));
+        const unsigned long long* p = hot == 1 ? cell : hot > 1 ? table + (s % hot) * 4096 : table + (s & mask);
+        acc += ld_rel(p);
       }
     }
     if (acc == 42) table[0] = acc;
@@ -75,14 +78,15 @@ int main() {
   CK(cudaMemset(table, 0, tab_words * 8));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  double res[2];
-  for (int loaded = 0; loaded < 2; ++loaded) {
+  double res[4];
+  const int hots[4] = {0, 0, 1, 64};
+  for (int loaded = 0; loaded < 4; ++loaded) {
     double best = 1e30;
     for (int rep = 0; rep < 3; ++rep) {
       CK(cudaMemset(cell, 0, 256));
       CK(cudaMemset(stop, 0, 4));
       const int blocks = loaded ? sms : 2;
-      pingpong<<<blocks, loaded ? 256 : 32>>>(cell, rounds, ns, table, (uint32_t)(tab_words - 1), stop);
+      pingpong<<<blocks, loaded ? 256 : 32>>>(cell, rounds, ns, table, (uint32_t)(tab_words - 1), stop, hots[loaded]);
       CK(cudaGetLastError());
       CK(cudaDeviceSynchronize());
       unsigned long long h = 0;
@@ -92,7 +96,9 @@ int main() {
     }
     res[loaded] = best;
   }
-  printf("{\"hop_ns_idle\": %.1f, \"hop_ns_loaded\": %.1f, \"rounds\": %d, \"background\": "
-         "\"%d CTAs x 256 threads polling a 2 MiB table\"}\n", res[0], res[1], rounds, sms - 2);
+  printf("{\"hop_ns_idle\": %.1f, \"hop_ns_loaded\": %.1f, \"hop_ns_hot_same_cell\": %.1f, "
+         "\"hop_ns_hot_64_cells\": %.1f, \"rounds\": %d, \"background\": "
+         "\"%d CTAs x 256 threads polling a 2 MiB table / the ping-pong cell / 64 hot cells\"}\n",
+         res[0], res[1], res[2], res[3], rounds, sms - 2);
   return 0;
 }
