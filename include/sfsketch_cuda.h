@@ -133,8 +133,8 @@ int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_
  * numba loop). mode: 0 = automatic (default), 1 = L2 gathers, 2 = whole table
  * in one SM's shared memory (only if it fits), 3 = row-partitioned cluster
  * (d CTAs, one row each, DSMEM min-reduction; only for 2 <= d <= 8 and a row
- * that fits), 4 = its warp-pipelined form (u32 keys, d in {2, 4, 8}, 16-B
- * aligned keys and output, >= one 512-key warp-tile; otherwise as 3); a
+ * that fits), 4 = its warp-pipelined form (u32 or u64 keys, d in {2, 4, 8},
+ * 16-B aligned keys and output, >= one warp-tile of keys; otherwise as 3); a
  * mode that does not apply falls back to the L2 path. A
  * negative mode only reads. Returns the previous mode. sfk_query_last_path()
  * returns the path (1-4) the last sfk_min_query launch took. */

@@ -608,13 +608,52 @@ __device__ __forceinline__ uint32_t row_off_u32(uint32_t key, uint32_t k30, uint
   return r;
 }
 
-template <int D, typename CT, int NW, int KPL, int NB, bool POW2>
+// The same reduction for a 64-bit key (the reference's own key dtype): the
+// high word of key ^ seed is no longer a per-CTA constant, so v and the first
+// product take the full 64-bit form (17 instructions per key and row).
+template <int SH>
+__device__ __forceinline__ uint32_t row_off_u64(uint32_t klo, uint32_t khi, uint32_t slo, uint32_t shi,
+                                                uint32_t mask_b) {
+  constexpr uint64_t K2S = 0x94D049BB133111EBull << SH;
+  uint32_t r;
+  asm("{\n\t"
+      ".reg .b32 ul, uh, vl, vh, zl, zh, t, yl, yh, xl, xh;\n\t"
+      ".reg .b64 x;\n\t"
+      "xor.b32 ul, %1, %3;\n\t"
+      "xor.b32 uh, %2, %4;\n\t"
+      "shf.r.wrap.b32 t, ul, uh, 30;\n\t"
+      "xor.b32 vl, ul, t;\n\t"
+      "shr.u32 t, uh, 30;\n\t"
+      "xor.b32 vh, uh, t;\n\t"
+      "mul.lo.u32 zl, vl, 0x1CE4E5B9;\n\t"
+      "mul.hi.u32 zh, vl, 0x1CE4E5B9;\n\t"
+      "mad.lo.u32 zh, vl, 0xBF58476D, zh;\n\t"
+      "mad.lo.u32 zh, vh, 0x1CE4E5B9, zh;\n\t"
+      "shf.r.wrap.b32 t, zl, zh, 27;\n\t"
+      "xor.b32 yl, zl, t;\n\t"
+      "shr.u32 t, zh, 27;\n\t"
+      "xor.b32 yh, zh, t;\n\t"
+      "mul.wide.u32 x, yl, %6;\n\t"
+      "mov.b64 {xl, xh}, x;\n\t"
+      "mad.lo.u32 xh, yl, %7, xh;\n\t"
+      "mad.lo.u32 xh, yh, %6, xh;\n\t"
+      "shf.r.wrap.b32 t, xl, xh, 31;\n\t"
+      "lop3.b32 %0, xl, t, %5, 0x28;\n\t"
+      "}"
+      : "=r"(r)
+      : "r"(klo), "r"(khi), "r"(slo), "r"(shi), "r"(mask_b), "n"((uint32_t)K2S), "n"((uint32_t)(K2S >> 32)));
+  return r;
+}
+
+// KU64: 64-bit keys (else u32)
+template <int D, typename CT, int NW, int KPL, int NB, bool POW2, bool KU64>
 __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __restrict__ counters, Seeds<D> seeds,
-                                                           Mod wm, int64_t w, const uint32_t* __restrict__ keys,
+                                                           Mod wm, int64_t w, const void* __restrict__ keys_v,
                                                            int64_t ntiles, int64_t* __restrict__ out) {
   constexpr bool U16 = sizeof(CT) == 2;
   constexpr int SH = U16 ? 1 : 2;
   constexpr int NT = NW * 32;
+  constexpr int KW = KU64 ? 2 : 1;  // 32-bit words per key
   constexpr int K = 32 * KPL;              // keys per warp-tile
   constexpr int OKL = KPL / D;             // keys per lane in the owner phase
   constexpr uint32_t RB = K * sizeof(CT);  // receive bytes per (warp, buffer)
@@ -733,7 +772,8 @@ __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __res
 #pragma unroll
         for (int u = 0; u < OKL; ++u) {
           if (m[u] == U32MAX) {
-            const uint64_t key = (uint64_t)__ldg(keys + t + u);
+            const uint64_t key = KU64 ? __ldg(static_cast<const unsigned long long*>(keys_v) + t + u)
+                                      : (uint64_t)__ldg(static_cast<const uint32_t*>(keys_v) + t + u);
             uint32_t mm = U32MAX;
 #pragma unroll
             for (int p = 0; p < D; ++p)
@@ -771,32 +811,43 @@ __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __res
   // NB receive buffers (a power of two): buffer and phase parity are bits of
   // the tile counter
   int64_t tile_key = g0 * K;
-  uint4 kn[KPL / 4];  // the next tile's keys
+  uint4 kn[KW * KPL / 4];  // the next tile's keys (4-key group j*32 + lane: KW uint4s)
   auto gload = [&](int64_t tk) {
-    const uint4* src = reinterpret_cast<const uint4*>(keys + tk) + lane;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(keys_v) + tk * KW) + lane * KW;
 #pragma unroll
-    for (int j = 0; j < KPL / 4; ++j) kn[j] = __ldcs(src + j * 32);
+    for (int j = 0; j < KPL / 4; ++j)
+#pragma unroll
+      for (int h = 0; h < KW; ++h) kn[KW * j + h] = __ldcs(src + j * 32 * KW + h);
   };
   if (Tw > 0) gload(tile_key);
   for (int it = 0; it < Tw; ++it) {
     const int pb = it & (NB - 1);
-    uint4 kk[KPL / 4];
+    uint4 kk[KW * KPL / 4];
 #pragma unroll
-    for (int j = 0; j < KPL / 4; ++j) kk[j] = kn[j];
+    for (int j = 0; j < KW * KPL / 4; ++j) kk[j] = kn[j];
     if (it + 1 < Tw) gload(tile_key + tstep);
     if (lane == 0) mbar_expect_arrive(full_a + 8 * pb, RB);
     uint32_t c[KPL];
     const unsigned char* rowb = reinterpret_cast<const unsigned char*>(row);
 #pragma unroll
     for (int j = 0; j < KPL / 4; ++j) {
-      const uint32_t kx[4] = {kk[j].x, kk[j].y, kk[j].z, kk[j].w};
+      uint32_t klo[4], khi[4];
+      if constexpr (KU64) {
+        klo[0] = kk[2 * j].x, khi[0] = kk[2 * j].y, klo[1] = kk[2 * j].z, khi[1] = kk[2 * j].w;
+        klo[2] = kk[2 * j + 1].x, khi[2] = kk[2 * j + 1].y, klo[3] = kk[2 * j + 1].z, khi[3] = kk[2 * j + 1].w;
+      } else {
+        klo[0] = kk[j].x, klo[1] = kk[j].y, klo[2] = kk[j].z, klo[3] = kk[j].w;
+        khi[0] = khi[1] = khi[2] = khi[3] = 0u;
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         uint32_t off;
-        if constexpr (POW2)
-          off = row_off_u32<SH>(kx[u], kx[u] >> 30, hh.c0, hh.c2, mask_b);
+        if constexpr (POW2 && KU64)
+          off = row_off_u64<SH>(klo[u], khi[u], (uint32_t)seed, (uint32_t)(seed >> 32), mask_b);
+        else if constexpr (POW2)
+          off = row_off_u32<SH>(klo[u], klo[u] >> 30, hh.c0, hh.c2, mask_b);
         else
-          off = (uint32_t)fmod64(mix64((uint64_t)kx[u] ^ seed), wm) << SH;
+          off = (uint32_t)fmod64(mix64(((uint64_t)khi[u] << 32 | klo[u]) ^ seed), wm) << SH;
         c[4 * j + u] = *reinterpret_cast<const CT*>(rowb + off);
       }
     }
@@ -820,16 +871,18 @@ __global__ void __launch_bounds__(NW * 32, 1) min_query_cw(const uint32_t* __res
 
 
 
-// Launch the warp-pipelined cluster kernel for u32 keys (16-B aligned keys and
-// output); the < K-key tail goes to the L2 kernel. Returns -1 if not suited.
-template <int D, typename CT, bool POW2>
-static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
-                  int64_t* out, cudaStream_t st, int optin) {
+// Launch the warp-pipelined cluster kernel for u32 / u64 keys (16-B aligned
+// keys and output); the < K-key tail goes to the L2 kernel. Returns -1 if not
+// suited.
+template <int D, typename CT, bool POW2, bool KU64>
+static int try_cw_k(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                    int64_t* out, cudaStream_t st, int optin) {
   constexpr int NW = SFK_CW_NW, NB = SFK_CW_NB;
-  constexpr int KPL = D == 2 ? 8 : D == 8 ? 16 : SFK_CW_KPL;  // owner phase: KPL / D keys per lane
+  // owner phase: KPL / D keys per lane; u64 keys take half the tile of u32
+  // ones at d = 4 (the prefetched keys' registers)
+  constexpr int KPL = D == 2 ? 8 : D == 8 ? 16 : (KU64 ? 8 : SFK_CW_KPL);
   constexpr int K = 32 * KPL;
-  if (ks.kind != SFK_KEY_U32 || (reinterpret_cast<uintptr_t>(ks.p) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
-    return -1;
+  if ((reinterpret_cast<uintptr_t>(ks.p) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return -1;
   const int64_t ntiles = n / K;
   if (ntiles < 1) return -1;
   const size_t row_bytes = ((size_t)w * sizeof(CT) + 15) & ~size_t(15);
@@ -837,7 +890,7 @@ static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t 
                       (size_t)NW * 2 * NB * 8;
   if (smem > (size_t)optin) return -1;
   if (sizeof(CT) == 2 && (size_t)NW * NB * K * sizeof(CT) < (size_t)OVF_SLOTS * 4) return -1;  // setup scratch
-  auto kern = min_query_cw<D, CT, NW, KPL, NB, POW2>;
+  auto kern = min_query_cw<D, CT, NW, KPL, NB, POW2, KU64>;
   // the opt-in attribute belongs to the current device's context: set it per call
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
@@ -864,7 +917,7 @@ static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t 
   if ((int64_t)nclusters > need) nclusters = (int)need;
   cfg.gridDim = dim3(D * nclusters);
   note_launch();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, counters, sd, wm, w, static_cast<const uint32_t*>(ks.p), ntiles, out);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, counters, sd, wm, w, ks.p, ntiles, out);
   if (e != cudaSuccess) {
     set_error("min_query_cw launch: %s", cudaGetErrorString(e));
     return (int)e;
@@ -874,13 +927,21 @@ static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t 
   g_query_last = 4;
   const int64_t done = ntiles * K;
   if (done < n) {
-    KeySrc tail{static_cast<const uint32_t*>(ks.p) + done, SFK_KEY_U32, 0};
+    KeySrc tail{static_cast<const char*>(ks.p) + done * (KU64 ? 8 : 4), ks.kind, 0};
     note_launch();
     min_query_l2<D, 4><<<grid_for(n - done, 256 * 4, sm_count() * 8), 256, 0, st>>>(counters, sd, wm, w, tail,
                                                                                     n - done, out + done);
     rc = check_launch("min_query_l2 (tail)");
   }
   return rc;
+}
+
+template <int D, typename CT, bool POW2>
+static int try_cw(const uint32_t* counters, const Seeds<D>& sd, Mod wm, int64_t w, KeySrc ks, int64_t n,
+                  int64_t* out, cudaStream_t st, int optin) {
+  if (ks.kind == SFK_KEY_U32) return try_cw_k<D, CT, POW2, false>(counters, sd, wm, w, ks, n, out, st, optin);
+  if (ks.kind == SFK_KEY_U64) return try_cw_k<D, CT, POW2, true>(counters, sd, wm, w, ks, n, out, st, optin);
+  return -1;
 }
 
 // Launch the cluster kernel if this (d, w, n) suits it; returns -1 if not.

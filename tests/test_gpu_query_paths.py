@@ -124,6 +124,23 @@ def test_query_paths_misaligned_views(oracle, path):
     np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, keys[1:n + 1].astype(np.uint64)))
 
 
+@pytest.mark.parametrize("d,w,hi", [(4, 65536, 1 << 20), (4, 65536, 70000), (4, 16384, 1 << 32), (8, 50000, 1 << 17),
+                                    (2, 65536, 1 << 18)])
+@pytest.mark.parametrize("n", [1000, 100_003, 3_000_001])
+def test_warp_pipelined_cluster_u64_keys(oracle, d, w, hi, n):
+    """The reference's own key dtype (uint64) on the warp-pipelined kernel:
+    full 64-bit keys hashed with the 64-bit form of the row reduction."""
+    rng = np.random.default_rng(d * 7 + w + n)
+    c = table(rng, d, w, hi)
+    c.flat[rng.integers(0, c.size, 512)] = rng.choice(np.array([65534, 65535, 65536], np.uint32), 512)
+    seeds = seed_array(17 + d, 0, d)
+    k64 = rng.integers(0, np.iinfo(np.uint64).max, size=n, dtype=np.uint64)
+    out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    took = run_query(torch.from_numpy(c).cuda(), seeds, torch.from_numpy(k64).cuda(), _lib.KEY_U64, 0, n, out, CW)
+    assert took == CW
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.min_query(c, seeds, k64))
+
+
 @pytest.mark.parametrize("path", [L2, SMEM, CLUSTER])
 def test_query_paths_u64_and_record_keys(oracle, path):
     d, w, n = 4, 16384 if path != SMEM else 12800, 150_000
@@ -145,10 +162,11 @@ def test_auto_path_picks_warp_pipelined_cluster_for_cfg5_shape():
     d, w, n = 4, 65536, 1 << 22
     c = torch.zeros((d, w), dtype=torch.uint32, device="cuda")
     seeds = seed_array(2017, 0, d)
-    keys = torch.zeros(n, dtype=torch.uint32, device="cuda")
-    out = torch.empty(n, dtype=torch.int64, device="cuda")
-    assert run_query(c, seeds, keys, _lib.KEY_U32, 0, n, out, 0) == CW
-    assert int(out.max()) == 0
+    for dt, kind in ((torch.uint32, _lib.KEY_U32), (torch.uint64, _lib.KEY_U64)):
+        keys = torch.zeros(n, dtype=dt, device="cuda")
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        assert run_query(c, seeds, keys, kind, 0, n, out, 0) == CW
+        assert int(out.max()) == 0
 
 
 def two_phase(counters, seeds, keys_t, kind, n, out_t, stream=None, gather_stream=None):
