@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(NT, 1) min_query_cluster(const uint32_t* __res
 #define SFK_CW_KPL 16
 #endif
 #ifndef SFK_CW_NB
-#define SFK_CW_NB 2
+#define SFK_CW_NB 4
 #endif
 
 // ---- cluster path, warp-pipelined (u32 keys) ---------------------------------
