@@ -405,10 +405,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SFK_BENCH_DEVICE / SFK_BENCH_BACKEND: functional check of the N > 1 code
+    # path on a one-GPU box (every rank on one device, gloo collectives); not
+    # a measurement
+    local_dev = int(os.environ.get("SFK_BENCH_DEVICE", local))
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SFK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     L = _lib.lib()
 
     rep = replicas(args, world)
@@ -460,7 +468,7 @@ def run_ours(args):
         return [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]), eng]
 
     # nvidia-smi needs ~0.5 s to start sampling: start it before the warm-up
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     time.sleep(1.0)
     for _ in range(args.warmup):
