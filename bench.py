@@ -400,7 +400,7 @@ def run_ours(args):
 
     import paper_1701_04148_b200 as P
     from paper_1701_04148_b200 import _lib, workloads as Wl
-    from paper_1701_04148_b200.sf import query_min, query_min_host
+    from paper_1701_04148_b200.sf import query_min
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -582,7 +582,7 @@ def run_ours(args):
                 sk.apply_ops(ops_h, keys_h)  # H2D inside the API call
             if world > 1 and not rep:
                 sk.broadcast_slim_(src=0)
-            query_min_host(sk.slim.counters, sk._slim_seeds, qk_h, qo_h)
+            sk.query_many_host(qk_h, out=qo_h)  # host keys in, host int64 estimates out
             torch.cuda.synchronize()
             e = time.perf_counter() - t0
             if k >= args.warmup:
@@ -591,11 +591,20 @@ def run_ours(args):
         et = torch.tensor([sum(e_times) / len(e_times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        wire = int(L.sfk_host_query_config(_lib.HQ_LAST_WIRE, -1))
+        wb = {_lib.WIRE_C16: 2, _lib.WIRE_U32: 4}.get(wire, 8)
+        sc = sk.slim.counters.to(torch.int64)
+        dict_bytes = int(torch.unique(sc[sc >= 0xF800]).numel()) * 4 if wire == _lib.WIRE_C16 else 0
+        # per step: the apply's ops + keys and its 24-B result; the query keys,
+        # the wire dictionary's set (16 KiB + flag) back and the sorted
+        # dictionary out, and the narrowed estimates
         e2e = {"value": round(items / float(et.item()) / 1e6, 3), "unit": "Mitems/s",
-               "h2d_bytes_per_step": int(n_ops * 5 + qn * 4) if (rank == 0 or rep) else int(qn * 4),
-               "d2h_bytes_per_step": int(qn * 8 + 24),
-               "note": "apply_ops from pinned host ops/keys; queries through query_min_host (3-stream "
-                       "H2D/kernel/D2H pipeline); wall clock, max over ranks"}
+               "h2d_bytes_per_step": int((n_ops * 5 if (rank == 0 or rep) else 0) + qn * 4 + dict_bytes),
+               "d2h_bytes_per_step": int(qn * wb + (16388 if wire != _lib.WIRE_I64 else 0) + 24),
+               "wire": {_lib.WIRE_C16: "u16 codes", _lib.WIRE_U32: "u32", _lib.WIRE_I64: "int64"}.get(wire, "?"),
+               "note": "apply_ops from pinned host ops/keys; queries through SfSketch.query_many_host "
+                       "(sfk_min_query_host: chunked H2D -> query kernel -> narrowed D2H, host threads widen "
+                       "into the int64 output); wall clock, max over ranks"}
         # the estimates must equal the device-resident run's
         assert torch.equal(qo_h.to(dev), qout), "e2e estimates differ from device-resident run"
 

@@ -129,6 +129,27 @@ int sfk_min_query(const uint32_t* counters, const uint64_t* seeds, int d, int64_
                   const void* keys, int key_kind, int rec_len, int64_t n, int64_t* out,
                   void* stream);
 
+/* Host-buffer form of sfk_min_query: the reference's query_many takes and
+ * returns host arrays (sf.py:189-193, _kernels.py:229-241; its ctypes binding
+ * is INTEGRATION.md's query_many). keys_host and out_host are host pointers
+ * (pinned or pageable); counters and seeds as in sfk_min_query. Blocks until
+ * out_host holds every estimate. Work on `stream` issued before the call is
+ * complete before the slim is read. The batch flows through H2D -> query
+ * kernel -> D2H in chunks; the estimates cross PCIe narrowed (u16 codes when
+ * the slim has at most 2048 distinct counter values >= 0xF800, else u32) and
+ * host threads widen them into out_host. Bit-identical to sfk_min_query. */
+int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w,
+                       const void* keys_host, int key_kind, int rec_len, int64_t n, int64_t* out_host,
+                       void* stream);
+
+/* Tuning of sfk_min_query_host (no reference counterpart). what: 0 = keys per
+ * chunk (default 2^24), 1 = wire (0 auto, 1 int64, 2 u32, 3 u16 codes where
+ * exact, else u32), 2 = every value-th chunk returns int64 directly when
+ * out_host is pinned (0 = never, default), 3 = host threads (0 = 3/4 of the hardware threads), 4 = chunks in flight (2-16, default 4), 5 = the wire the last
+ * call used (read only). value < 0 only reads. Returns the previous value, or
+ * -1 for an unknown key or value. */
+int64_t sfk_host_query_config(int what, int64_t value);
+
 /* Query kernel selection (no reference counterpart: the reference has one
  * numba loop). mode: 0 = automatic (default), 1 = L2 gathers, 2 = whole table
  * in one SM's shared memory (only if it fits), 3 = row-partitioned cluster

@@ -20,6 +20,9 @@ KEY_U64, KEY_U32, KEY_RECORD = 0, 1, 2
 OK, PHANTOM, SATURATED, UNSUPPORTED, BAD_OPCODE = 0, 1, 2, 3, 4
 VARIANT_CODE = {"sf1": 1, "sf2": 2, "sf3": 3, "sf4": 4, "sff": 6}
 FLAG_SEQUENTIAL = 1
+# sfk_host_query_config keys and wire formats (include/sfsketch_cuda.h)
+HQ_CHUNK, HQ_WIRE, HQ_DIRECT, HQ_THREADS, HQ_RING, HQ_LAST_WIRE = 0, 1, 2, 3, 4, 5
+WIRE_AUTO, WIRE_I64, WIRE_U32, WIRE_C16 = 0, 1, 2, 3
 
 # every symbol the header declares; tests check the built library exports them
 EXPORTS = (
@@ -28,6 +31,8 @@ EXPORTS = (
     "sfk_mix_batch",
     "sfk_load_keys",
     "sfk_min_query",
+    "sfk_min_query_host",
+    "sfk_host_query_config",
     "sfk_cm_workspace_size",
     "sfk_cm_apply",
     "sfk_cm_delta",
@@ -90,6 +95,9 @@ def load_library() -> ctypes.CDLL:
     L.sfk_mix_batch.argtypes = [P, I64, P, P]
     L.sfk_load_keys.argtypes = [P, I, I, I64, P, P]
     L.sfk_min_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
+    L.sfk_min_query_host.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
+    L.sfk_host_query_config.argtypes = [I, I64]
+    L.sfk_host_query_config.restype = I64
     L.sfk_cm_workspace_size.argtypes = [I, I64, I64]
     L.sfk_cm_workspace_size.restype = SZ
     L.sfk_cu_workspace_size.argtypes = [I, I64, I64]

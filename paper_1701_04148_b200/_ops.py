@@ -107,6 +107,37 @@ def normalize_keys(keys) -> KeyBatch:
     raise ConfigurationError(f"keys must be integers, got {t.dtype}")
 
 
+def normalize_host_keys(keys):
+    """``normalize_keys`` for a batch that stays in host memory (the
+    host-buffer query path): returns (contiguous CPU tensor, key kind,
+    rec_len, n) with the same dtype rules and errors, and no device copy."""
+    if isinstance(keys, KeyBatch):
+        raise ConfigurationError("host queries take host keys, not a device KeyBatch")
+    if isinstance(keys, torch.Tensor):
+        if keys.device.type != "cpu":
+            raise ConfigurationError("host queries take keys in host memory")
+        t = keys
+    else:
+        arr = np.asarray(keys)
+        if arr.dtype == object or arr.dtype.kind not in "iub":
+            arr = np.ascontiguousarray(keys, dtype=np.uint64)
+        if arr.dtype.kind == "b":
+            arr = arr.astype(np.uint64)
+        t = _host_view(np.ascontiguousarray(arr))
+    if t.dtype == torch.uint8 and t.dim() == 2:
+        t = t.contiguous()
+        return t, _lib.KEY_RECORD, int(t.shape[1]), int(t.shape[0])
+    if t.dim() != 1:
+        raise ConfigurationError("keys must be a 1-d sequence")
+    if t.dtype == torch.uint32:
+        return t.contiguous(), _lib.KEY_U32, 0, int(t.shape[0])
+    if t.dtype in (torch.uint64, torch.int64):
+        return t.contiguous().view(torch.uint64), _lib.KEY_U64, 0, int(t.shape[0])
+    if t.dtype in (torch.int32, torch.int16, torch.int8, torch.uint8, torch.uint16, torch.bool):
+        return t.to(torch.int64).view(torch.uint64), _lib.KEY_U64, 0, int(t.shape[0])
+    raise ConfigurationError(f"keys must be integers, got {t.dtype}")
+
+
 BAD_OPCODE_MSG = "op codes must be 0 (insert) or 1 (delete)"
 
 

@@ -31,7 +31,7 @@ import math
 from .errors import ConfigurationError, UnsupportedOperationError
 from .hashing import MASK64, seed_array
 from .params import SketchParams
-from .sf import query_min
+from .sf import query_min, query_min_host
 
 
 class _CounterSketch:
@@ -82,6 +82,11 @@ class _CounterSketch:
 
     def query_many(self, keys) -> torch.Tensor:
         return query_min(self.counters, self._seeds, keys)
+
+    def query_many_host(self, keys, out=None):
+        """Host keys in, host int64 estimates out (``sfk_min_query_host``)."""
+        res = query_min_host(self.counters, self._seeds, keys, out)
+        return res if isinstance(keys, torch.Tensor) or out is not None else res.numpy()
 
 
 class CmSketch(_CounterSketch):

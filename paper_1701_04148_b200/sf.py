@@ -32,6 +32,7 @@ from ._ops import (
     OP_INSERT,
     Scratch,
     device,
+    normalize_host_keys,
     normalize_keys,
     normalize_stream,
     raise_for_status,
@@ -99,40 +100,27 @@ def query_min(counters: torch.Tensor, seeds: np.ndarray, keys) -> torch.Tensor:
     return out
 
 
-def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host: torch.Tensor, out_host: torch.Tensor,
-                   chunk: int = 1 << 25, streams: int = 3) -> torch.Tensor:
-    """Point queries for a batch that lives in (pinned) HOST memory.
-
-    The batch is cut into chunks that flow through a multi-stream pipeline
-    (H2D copy -> fused hash/gather/min kernel -> D2H copy), so PCIe transfers
-    overlap the kernel as in the paper's GPU query design.
-    ``out_host`` (int64, same length) receives the estimates; returns it after
-    the last copy completed."""
+def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_host: torch.Tensor | None = None):
+    """Point queries for a batch that lives in HOST memory (pinned or
+    pageable), the reference's ``query_many`` contract (``sf.py:189-193``):
+    host keys in, host int64 estimates out. ``sfk_min_query_host`` cuts the
+    batch into chunks that flow H2D -> fused hash/gather/min kernel -> D2H on
+    three streams, as in the paper's GPU query design,
+    with the estimates narrowed on the link and widened into ``out_host`` by
+    native host threads. ``out_host`` (int64 CPU tensor, same length) is
+    allocated when omitted; returns it."""
     L = _lib.lib()
-    dev = counters.device
-    n = int(keys_host.shape[0])
+    t, kind, rec, n = normalize_host_keys(keys_host)
+    if out_host is None:
+        out_host = torch.empty(n, dtype=torch.int64)
+    elif (out_host.device.type != "cpu" or out_host.dtype != torch.int64 or tuple(out_host.shape) != (n,)
+          or not out_host.is_contiguous()):
+        raise ConfigurationError("out_host must be a contiguous int64 CPU tensor of the batch's length")
     d, w = counters.shape
-    kind = _lib.KEY_U32 if keys_host.dtype == torch.uint32 else _lib.KEY_U64
-    esz = 4 if kind == _lib.KEY_U32 else 8
-    cur = torch.cuda.current_stream(dev)
-    ss = [torch.cuda.Stream(dev) for _ in range(streams)]
-    kbuf = [torch.empty(chunk * esz, dtype=torch.uint8, device=dev) for _ in range(streams)]
-    obuf = [torch.empty(chunk, dtype=torch.int64, device=dev) for _ in range(streams)]
-    for s in ss:
-        s.wait_stream(cur)
-    for c, a in enumerate(range(0, n, chunk)):
-        b = min(n, a + chunk)
-        s = ss[c % streams]
-        with torch.cuda.stream(s):
-            kd = kbuf[c % streams][: (b - a) * esz].view(keys_host.dtype)
-            kd.copy_(keys_host[a:b], non_blocking=True)
-            od = obuf[c % streams][: b - a]
-            rc = L.sfk_min_query(counters.data_ptr(), seeds.ctypes.data, d, w, kd.data_ptr(), kind, 0, b - a,
-                                 od.data_ptr(), int(s.cuda_stream))
-            _lib.check(rc, "sfk_min_query")
-            out_host[a:b].copy_(od, non_blocking=True)
-    for s in ss:
-        cur.wait_stream(s)
+    if n:
+        rc = L.sfk_min_query_host(counters.data_ptr(), seeds.ctypes.data, d, w, t.data_ptr(), kind, rec, n,
+                                  out_host.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "sfk_min_query_host")
     return out_host
 
 
@@ -228,6 +216,13 @@ class SfSketch:
 
     def query_many(self, keys) -> torch.Tensor:
         return query_min(self.slim.counters, self._slim_seeds, keys)
+
+    def query_many_host(self, keys, out=None):
+        """``query_many`` for host-resident keys with host-resident results
+        (the reference's numpy-in / numpy-out form): a numpy array for array or
+        list input, else the int64 CPU tensor ``out`` (allocated if omitted)."""
+        res = query_min_host(self.slim.counters, self._slim_seeds, keys, out)
+        return res if isinstance(keys, torch.Tensor) or out is not None else res.numpy()
 
     # ------------------------------------------------------------ oracle mode
     def oracle_assisted_insert(self, key: int, true_freq: int) -> None:
