@@ -167,6 +167,18 @@ int sfk_query_path(int mode);
  * round of parallel loads, one launch and no host round trip. A negative
  * value only reads. Returns the previous value. */
 int64_t sfk_warp_batch_ops(int64_t ops);
+
+/* Medium-batch engine selection (no reference counterpart). SFF / SF4 batches
+ * above sfk_warp_batch_ops() and up to `ops` ops (default 2048; at most 8192
+ * (op, row) pairs, z <= 8) run on the block engine: one 1024-thread CTA sorts,
+ * walks the fat and replays the slim updates as a dataflow in shared memory,
+ * in one launch and with no workspace. A negative value only reads. Returns
+ * the previous value. */
+int64_t sfk_block_batch_ops(int64_t ops);
+
+/* Diagnostics: globaltimer stamps (ns) at the block engine's phase boundaries
+ * in its last launch (start, sorted, scanned, fat pass, replayed, done). */
+int sfk_blk_profile(unsigned long long* out6);
 int sfk_query_last_path(void);
 
 /* Two-phase form of sfk_min_query (no reference counterpart; same

@@ -65,6 +65,8 @@ EXPORTS = (
     "sfk_query_path",
     "sfk_small_batch_ops",
     "sfk_warp_batch_ops",
+    "sfk_block_batch_ops",
+    "sfk_blk_profile",
     "sfk_query_last_path",
     "sfk_query_index",
     "sfk_min_query_idx",
@@ -142,6 +144,9 @@ def load_library() -> ctypes.CDLL:
     L.sfk_small_batch_ops.restype = I64
     L.sfk_warp_batch_ops.argtypes = [I64]
     L.sfk_warp_batch_ops.restype = I64
+    L.sfk_block_batch_ops.argtypes = [I64]
+    L.sfk_block_batch_ops.restype = I64
+    L.sfk_blk_profile.argtypes = [P]
     L.sfk_query_index.argtypes = [P, I, I64, P, I, I, I64, P, P]
     L.sfk_min_query_idx.argtypes = [P, I, I64, P, I64, P, P]
     L.sfk_gen_query_keys.argtypes = [ctypes.c_uint64, P, P, ctypes.c_uint32, P, I64, I64, P, P]

@@ -59,6 +59,11 @@ int launch_gen_query_keys(uint64_t, const uint32_t*, const uint32_t*, uint32_t, 
 int launch_seq_apply(int kind, int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, const uint64_t* s_seeds,
                      const uint64_t* f_seeds, int d, int64_t w, int64_t wp, int64_t z, const uint8_t* ops, KeySrc ks,
                      const int64_t* true_counts, int64_t n, int64_t* inc, int64_t* result, cudaStream_t st);
+int launch_blk_bucket(int variant, uint32_t* slim, uint32_t* fat, const uint64_t* s_seeds, const uint64_t* f_seeds,
+                      int d, int64_t w, int64_t z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
+                      int64_t* result, cudaStream_t st);
+bool blk_fits(int d, int64_t w, int64_t z, int64_t n);
+int blk_profile(unsigned long long* out);
 int launch_seqw_bucket(int variant, uint32_t* slim, uint32_t* fat, const uint64_t* s_seeds, const uint64_t* f_seeds,
                        int d, int64_t w, int64_t z, const uint8_t* ops, KeySrc ks, int64_t n, int64_t* inc,
                        int64_t* result, cudaStream_t st);
@@ -139,6 +144,16 @@ static bool small_batch(int64_t n) { return n > 0 && n <= small_batch_ops(); }
 #endif
 static int64_t g_warp_batch = SFK_WARP_BATCH_DEFAULT;
 static int64_t warp_batch_ops() { return __atomic_load_n(&g_warp_batch, __ATOMIC_RELAXED); }
+
+// Larger SFF / SF4 batches up to this many ops (and d x n <= 8192 (op, row)
+// pairs) run on the block engine (blk_bucket_k, sfk_blk.cu): one 1024-thread
+// CTA, sort + fat walk + dataflow replay in shared memory, one launch.
+// sfk_block_batch_ops() sets it (0: off).
+#ifndef SFK_BLOCK_BATCH_DEFAULT
+#define SFK_BLOCK_BATCH_DEFAULT 2048
+#endif
+static int64_t g_block_batch = SFK_BLOCK_BATCH_DEFAULT;
+static int64_t block_batch_ops() { return __atomic_load_n(&g_block_batch, __ATOMIC_RELAXED); }
 
 static const char* key_ptr(const void* keys, int key_kind, int rec_len, int64_t t0) {
   const char* p = static_cast<const char*>(keys);
@@ -250,6 +265,12 @@ int64_t sfk_small_batch_ops(int64_t ops) {
 
 int64_t sfk_warp_batch_ops(int64_t ops) {
   return ops < 0 ? warp_batch_ops() : __atomic_exchange_n(&g_warp_batch, ops, __ATOMIC_RELAXED);
+}
+
+int sfk_blk_profile(unsigned long long* out) { return blk_profile(out); }
+
+int64_t sfk_block_batch_ops(int64_t ops) {
+  return ops < 0 ? block_batch_ops() : __atomic_exchange_n(&g_block_batch, ops, __ATOMIC_RELAXED);
 }
 
 int sfk_mix_batch(const uint64_t* keys, int64_t n, uint64_t* out, void* stream) {
@@ -375,6 +396,9 @@ size_t sfk_sf_workspace_size(int variant, int d, int64_t w, int64_t w_prime, int
     while (Z < z) Z <<= 1;
     if ((int64_t)d * Z <= 32) return 256;
   }
+  if ((variant == SFK_VARIANT_SFF || variant == SFK_VARIANT_SF4) && n > warp_batch_ops() && n <= block_batch_ops() &&
+      blk_fits(d, w, z, n))
+    return 256;  // the block engine needs no workspace
   return parallel_workspace_size(kind, d, w, w_prime, z, std::min<int64_t>(n, chunk_ops(d, kind_z(kind, z))));
 }
 
@@ -399,6 +423,11 @@ int sfk_sf_apply(int variant, uint32_t* slim, uint32_t* fat, uint32_t* dsub, con
   if (bucketed && !(flags & SFK_FLAG_SEQUENTIAL) && n > 0 && n <= warp_batch_ops()) {
     const int rc = launch_seqw_bucket(variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, slim_seeds, fat_seeds, d, w, z,
                                       ops, all, n, inc_counts, result, st);
+    if (rc >= 0) return rc;
+  }
+  if (bucketed && !(flags & SFK_FLAG_SEQUENTIAL) && n > warp_batch_ops() && n <= block_batch_ops()) {
+    const int rc = launch_blk_bucket(variant == SFK_VARIANT_SF4 ? 0 : 1, slim, fat, slim_seeds, fat_seeds, d, w, z,
+                                     ops, all, n, inc_counts, result, st);
     if (rc >= 0) return rc;
   }
   if ((flags & SFK_FLAG_SEQUENTIAL) || kind < 0 || small_batch(n)) {

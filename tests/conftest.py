@@ -52,15 +52,18 @@ def load_baseline_fixture(name):
 
 @pytest.fixture
 def parallel_engine_only():
-    """Tiny batches normally take the one-thread engine (sfk_small_batch_ops);
-    parity tests turn that off so the parallel pipeline sees them too."""
+    """Tiny and medium batches normally take the one-thread / warp / block
+    engines (sfk_small_batch_ops, sfk_warp_batch_ops, sfk_block_batch_ops);
+    parity tests turn those off so the parallel pipeline sees them too."""
     from paper_1701_04148_b200 import _lib
 
     L = _lib.lib()
     prev = L.sfk_small_batch_ops(0)
     prev_w = L.sfk_warp_batch_ops(0)
+    prev_b = L.sfk_block_batch_ops(0)
     try:
         yield
     finally:
         L.sfk_small_batch_ops(prev)
         L.sfk_warp_batch_ops(prev_w)
+        L.sfk_block_batch_ops(prev_b)

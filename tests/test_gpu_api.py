@@ -283,11 +283,13 @@ def test_tiny_batches_both_engines_match_oracle(oracle, kind):
         ops[500], keys[500] = 1, 0xFFFFFFFF  # a phantom: never inserted
     wp = {"sf3": 4 * 16, "sf1": 64, "sf2": 64}.get(kind)
     sizes = [1, 2, 3, 5, 8, 13, 21, 31, 32, 33, 40] * 6
-    # (one-thread threshold, warp-engine threshold): the one-thread engine,
-    # the warp engine (SFF / SF4 only), the parallel pipeline
-    for small, warp in ((32, 0), (0, 2048), (0, 0)):
+    # (one-thread, warp-engine, block-engine thresholds): the one-thread
+    # engine, the warp engine and the block engine (SFF / SF4 only), the
+    # parallel pipeline
+    for small, warp, block in ((32, 0, 0), (0, 2048, 0), (0, 0, 2048), (0, 0, 0)):
         prev = L.sfk_small_batch_ops(small)
         prev_w = L.sfk_warp_batch_ops(warp)
+        prev_b = L.sfk_block_batch_ops(block)
         try:
             o = oracle.OracleSketch(kind, 3, 16, 4, wp, 5)
             sk = make_sketch(kind, 3, 16, 4, wp, 5)
@@ -297,12 +299,13 @@ def test_tiny_batches_both_engines_match_oracle(oracle, kind):
                 if a >= b:
                     break
                 st = o.apply_ops(ops[a:b], keys[a:b].astype(np.uint64))
-                assert apply_batches(sk, ops[a:b], keys[a:b]) == st[:2], (small, warp, a, b)
+                assert apply_batches(sk, ops[a:b], keys[a:b]) == st[:2], (small, warp, block, a, b)
                 assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat if kind not in ("cm", "cu") else None)
                 a = b
         finally:
             L.sfk_small_batch_ops(prev)
             L.sfk_warp_batch_ops(prev_w)
+            L.sfk_block_batch_ops(prev_b)
 
 
 def _state(sk):
@@ -401,3 +404,90 @@ def test_warp_engine_matches_oracle(oracle, seed):
                 break
     finally:
         L.sfk_warp_batch_ops(prev)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_block_engine_matches_oracle(oracle, seed):
+    """The one-CTA block engine (SFF / SF4 batches of up to 8192 (op, row)
+    pairs, z <= 8) against the oracle: random shapes (d 1-8, z 1-8, odd
+    widths), Zipf-skewed keys (long same-cell chains in the dataflow
+    replay), deletes including phantoms, fat presets near 2^32 (saturation),
+    u32 / u64 / record keys, batch splits; one launch per batch and states
+    equal after every batch."""
+    from paper_1701_04148_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(9300 + seed)
+    kind = ("sff", "sf4")[seed % 2]
+    d = int(rng.choice([1, 2, 3, 4, 4, 4, 5, 8]))
+    z = int(rng.choice([1, 2, 3, 4, 4, 5, 7, 8]))
+    w = int(rng.choice([5, 64, 1000, 12800, 65536]))
+    nmax = 8192 // d
+    n = int(rng.integers(nmax // 4, nmax + 1))
+    vocab = rng.integers(0, 1 << 62, size=int(rng.integers(1, 400)), dtype=np.uint64)
+    ranks = np.minimum(rng.zipf(rng.choice([1.1, 1.3, 2.0]), size=n) - 1, vocab.size - 1)
+    keys = vocab[ranks]
+    ops = np.zeros(n, np.uint8)
+    ops[rng.random(n) < rng.choice([0.0, 0.2, 0.45])] = 1
+    o = oracle.OracleSketch(kind, d, w, z, None, seed)
+    sk = make_sketch(kind, d, w, z, None, seed)
+    if seed % 4 == 1:  # near saturation
+        o.fat[...] = np.uint32(0xFFFFFFFF - 40)
+        sk.fat.counters.fill_(0xFFFFFFFF - 40)
+    kk = seed % 3
+    if kk == 1:
+        keys_in = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        keys_o = keys_in.astype(np.uint64)
+    elif kk == 2:
+        recs = rng.integers(0, 256, size=(vocab.size, 13), dtype=np.uint8)[ranks]
+        keys_in, keys_o = recs, oracle.keys_from_records(recs)
+    else:
+        keys_in, keys_o = keys, keys
+    prev_w, prev_b = L.sfk_warp_batch_ops(0), L.sfk_block_batch_ops(1 << 20)
+    try:
+        bounds = np.unique(np.concatenate([[0, n], rng.integers(0, n, size=2)]))
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            st = o.apply_ops(ops[a:b], keys_o[a:b])
+            l0 = L.sfk_launch_count()
+            got = apply_batches(sk, ops[a:b], keys_in[a:b])
+            assert L.sfk_launch_count() - l0 == 1  # the block engine, one launch
+            assert got == st[:2], (a, b)
+            assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+            if st[0] != 0:
+                break
+    finally:
+        L.sfk_warp_batch_ops(prev_w)
+        L.sfk_block_batch_ops(prev_b)
+
+
+def test_block_engine_bad_opcode_and_limits(oracle):
+    """A bad op code rejects the batch before anything is applied; batches past
+    8192 (op, row) pairs or z > 8 take another engine (same results)."""
+    from paper_1701_04148_b200 import _lib
+    from paper_1701_04148_b200.errors import ConfigurationError
+
+    L = _lib.lib()
+    prev_w, prev_b = L.sfk_warp_batch_ops(0), L.sfk_block_batch_ops(1 << 20)
+    try:
+        sk = make_sketch("sff", 4, 1024, 4, None, 1)
+        ops = np.zeros(1000, np.uint8)
+        ops[700] = 3
+        with pytest.raises(ConfigurationError):
+            sk.apply_ops(ops, np.arange(1000, dtype=np.uint64))
+        assert int(sk.fat.counters.sum()) == 0 and int(sk.slim.counters.sum()) == 0
+        for d, z, n in ((4, 4, 2049), (2, 12, 500), (2, 33, 500), (8, 2, 1025)):
+            rng = np.random.default_rng(d * z)
+            keys = rng.integers(0, 300, size=n).astype(np.uint64)
+            ops = (rng.random(n) < 0.1).astype(np.uint8)
+            ops[: n // 2] = 0
+            o = oracle.OracleSketch("sff", d, 4096, z, None, 2)
+            sk = make_sketch("sff", d, 4096, z, None, 2)
+            st = o.apply_ops(ops, keys)
+            l0 = L.sfk_launch_count()
+            assert apply_batches(sk, ops, keys) == st[:2]
+            if z <= 8:  # (z > 8 runs on the one-thread engine: one launch too)
+                assert L.sfk_launch_count() - l0 > 1  # not the block engine
+            assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+    finally:
+        L.sfk_warp_batch_ops(prev_w)
+        L.sfk_block_batch_ops(prev_b)
