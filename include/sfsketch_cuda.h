@@ -79,6 +79,10 @@ extern "C" {
 int sfk_abi_version(void);
 const char* sfk_last_error(void);
 
+/* cudaStreamSynchronize(stream): the Python layer's wait before it reads a
+ * result triple from pinned host memory (no torch stream object needed). */
+int sfk_stream_sync(void* stream);
+
 /* Batches of 1..ops ops (default 32) go to the exact one-thread device engine
  * (one launch, no host read-back) instead of the parallel pipeline, whose
  * fixed cost dominates tiny batches: SF, CM, CU, Count, CML and oracle-
@@ -162,7 +166,7 @@ int64_t sfk_host_query_config(int what, int64_t value);
 int sfk_query_path(int mode);
 
 /* Small-batch engine selection (no reference counterpart). SFF / SF4 batches
- * of at most `ops` ops (default 192; 0 = off) run on the warp-cooperative
+ * of at most `ops` ops (default 24; 0 = off) run on the warp-cooperative
  * exact engine: ops in stream order, each op's d x z counter reads in one
  * round of parallel loads, one launch and no host round trip. A negative
  * value only reads. Returns the previous value. */

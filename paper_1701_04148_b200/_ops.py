@@ -37,7 +37,7 @@ OP_DELETE = 1
 
 def device() -> torch.device:
     _lib.lib()  # fail loudly without CUDA / the built library
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cuda", torch._C._cuda_getDevice())
 
 
 @dataclass
@@ -141,11 +141,21 @@ def normalize_host_keys(keys):
 BAD_OPCODE_MSG = "op codes must be 0 (insert) or 1 (delete)"
 
 
-def normalize_stream(ops, keys, check_ops: bool = True):
+def normalize_stream(ops, keys, check_ops: bool = True, stage: "Scratch | None" = None):
     """``_ops.py:27-34``. ``check_ops=False``: the op codes are validated on
     the device by the apply itself (SF, CM, CU: status BAD_OPCODE, nothing
     applied, raised as the same ConfigurationError by raise_for_status), which
-    saves a reduction and a host sync per batch."""
+    saves a reduction and a host sync per batch. ``stage``: the caller's
+    Scratch, for an apply that synchronises before it returns; a small HOST
+    batch is then copied into its pinned staging area, which the kernels read
+    in place through its device mapping (no copy launches)."""
+    if stage is not None:
+        st = stage.stage_host(ops, keys)
+        if st is not None:
+            o, kb = st
+            if check_ops and kb.n and bool((o > OP_DELETE).any()):
+                raise ConfigurationError(BAD_OPCODE_MSG)
+            return o, kb
     dev = device()
     kb = normalize_keys(keys)
     if isinstance(ops, torch.Tensor):
@@ -185,33 +195,88 @@ def raise_for_status(status: int, op_index: int, keys: KeyBatch) -> None:
     raise AssertionError(f"unexpected kernel status {status}")
 
 
+STAGE_MAX_BYTES = 1 << 16  # host batches up to this many key bytes are staged in pinned memory
+
+
 class Scratch:
-    """Per-sketch scratch: the result triple and a growable device workspace.
+    """Per-sketch scratch: the result triple, a growable device workspace and
+    a pinned staging area for small host batches.
 
     The result triple lives in pinned host memory, which the kernels write
     through its (unified-address) device mapping, so reading it back costs a
-    stream synchronisation and no copy launch."""
+    stream synchronisation and no copy launch. The staging area is read the
+    same way; it is reused by the next apply, which is safe because every
+    apply that stages synchronises before it returns."""
 
     def __init__(self):
         self.result = None
+        self.result_np = None
         self.ws = None
         self._dev = None
+        self._stage = None
+        self._stage_np = None
 
     def get(self, nbytes: int):
         dev = device()
         if self.result is None or self._dev != dev:
             self.result = torch.zeros(3, dtype=torch.int64).pin_memory()
+            self.result_np = self.result.numpy()
             self.ws = None
             self._dev = dev
         if self.ws is None or self.ws.numel() < nbytes:
             self.ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
         return self.result, self.ws
 
+    def stage_host(self, ops, keys):
+        """(ops, KeyBatch) over the pinned staging area for a small host batch
+        (numpy arrays, sequences or CPU tensors), with the dtype rules of
+        normalize_keys; None when the batch is on the device or too large."""
+        if isinstance(keys, KeyBatch) or (isinstance(keys, torch.Tensor) and keys.device.type != "cpu"):
+            return None
+        if isinstance(ops, torch.Tensor) and ops.device.type != "cpu":
+            return None
+        k = keys.numpy() if isinstance(keys, torch.Tensor) else np.asarray(keys)
+        if k.dtype == object or k.dtype.kind not in "iub":
+            k = np.asarray(keys, dtype=np.uint64)
+        if k.dtype.kind == "b":
+            k = k.astype(np.uint64)
+        if k.dtype == np.uint8 and k.ndim == 2:
+            kind, rec, n = _lib.KEY_RECORD, int(k.shape[1]), int(k.shape[0])
+        elif k.ndim != 1:
+            return None  # normalize_keys raises the reference's error
+        elif k.dtype == np.uint32:
+            kind, rec, n = _lib.KEY_U32, 0, int(k.shape[0])
+        else:
+            k = k.astype(np.int64, copy=False) if k.dtype != np.uint64 else k
+            kind, rec, n = _lib.KEY_U64, 0, int(k.shape[0])
+        kbytes = n * (rec if kind == _lib.KEY_RECORD else k.dtype.itemsize)
+        if n == 0 or kbytes > STAGE_MAX_BYTES:
+            return None
+        # the reference's cast (np.ascontiguousarray(ops, dtype=np.uint8)), on the caller's object
+        o = np.ascontiguousarray(ops.numpy() if isinstance(ops, torch.Tensor) else ops, dtype=np.uint8)
+        if o.ndim != 1 or o.shape[0] != n:
+            raise ConfigurationError("ops and keys must be 1-d sequences of equal length")
+        if self._stage is None:
+            self._stage = torch.empty(2 * STAGE_MAX_BYTES + 256, dtype=torch.uint8).pin_memory()
+            self._stage_np = self._stage.numpy()
+        kb_off = ((n + 255) // 256) * 256
+        self._stage_np[:n] = o
+        self._stage_np[kb_off:kb_off + kbytes] = np.ascontiguousarray(k).reshape(-1).view(np.uint8)
+        ot = self._stage[:n]
+        if kind == _lib.KEY_RECORD:
+            kt = self._stage[kb_off:kb_off + kbytes].view(n, rec)
+        elif kind == _lib.KEY_U32:
+            kt = self._stage[kb_off:kb_off + kbytes].view(torch.uint32)
+        else:
+            kt = self._stage[kb_off:kb_off + kbytes].view(torch.uint64)
+        return ot, KeyBatch(kt, kind, rec, n)
+
     @staticmethod
-    def read(result: torch.Tensor):
+    def read(result: torch.Tensor, scratch: "Scratch | None" = None):
         if result.is_cuda:
             s, i, n = (int(v) for v in result.tolist())
         else:  # pinned, written by the device: wait for the stream, then read in place
-            torch.cuda.current_stream().synchronize()
-            s, i, n = (int(v) for v in result.tolist())
+            _lib.check(_lib.load_library().sfk_stream_sync(_lib.stream_ptr()), "sfk_stream_sync")
+            r = scratch.result_np if scratch is not None and scratch.result is result else result.numpy()
+            s, i, n = int(r[0]), int(r[1]), int(r[2])
         return s, i, n

@@ -58,9 +58,9 @@ class _CounterSketch:
 
     def apply_ops(self, ops, keys, *, sequential: bool = False) -> None:
         # CM / CU validate op codes on the device (status BAD_OPCODE)
-        ops_t, kb = normalize_stream(ops, keys, check_ops=not self._device_checks_ops)
+        ops_t, kb = normalize_stream(ops, keys, check_ops=not self._device_checks_ops, stage=self._scratch)
         result = self._submit(ops_t, kb, sequential)
-        status, bad, n_ins = Scratch.read(result)
+        status, bad, n_ins = Scratch.read(result, self._scratch)
         self.insertions_seen += n_ins
         raise_for_status(status, bad, kb)
 

@@ -140,7 +140,7 @@ static bool small_batch(int64_t n) { return n > 0 && n <= small_batch_ops(); }
 // instead of the parallel pipeline's ~140 us fixed cost. sfk_warp_batch_ops()
 // sets it (0: off).
 #ifndef SFK_WARP_BATCH_DEFAULT
-#define SFK_WARP_BATCH_DEFAULT 192
+#define SFK_WARP_BATCH_DEFAULT 24
 #endif
 static int64_t g_warp_batch = SFK_WARP_BATCH_DEFAULT;
 static int64_t warp_batch_ops() { return __atomic_load_n(&g_warp_batch, __ATOMIC_RELAXED); }
@@ -258,6 +258,15 @@ int sfk_gen_query_keys(uint64_t seed, const uint32_t* present, const uint32_t* s
 }
 
 const char* sfk_last_error(void) { return g_err; }
+
+int sfk_stream_sync(void* stream) {
+  const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    set_error("stream sync: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
 
 int64_t sfk_small_batch_ops(int64_t ops) {
   return ops < 0 ? small_batch_ops() : __atomic_exchange_n(&g_small_batch, ops, __ATOMIC_RELAXED);

@@ -180,9 +180,10 @@ class SfSketch:
             raise UnsupportedOperationError(
                 "sketch already ran in oracle-assisted mode; regular updates would break it"
             )
-        ops_t, kb = normalize_stream(ops, keys, check_ops=False)  # op codes checked on the device
+        # op codes checked on the device; small host batches read in place from pinned staging
+        ops_t, kb = normalize_stream(ops, keys, check_ops=False, stage=self._scratch)
         result = self._submit(ops_t, kb, sequential)
-        status, bad, n_ins = Scratch.read(result)
+        status, bad, n_ins = Scratch.read(result, self._scratch)
         if kb.n and status != _lib.BAD_OPCODE:  # a rejected batch leaves the sketch untouched
             self._used_normal = True
         self.slim.insertions_seen += n_ins
