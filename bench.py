@@ -571,7 +571,7 @@ def run_ours(args):
         qk_h = torch.empty(qn, dtype=torch.uint32).pin_memory()
         qk_h.copy_(qkeys)
         qo_h = torch.empty(qn, dtype=torch.int64).pin_memory()
-        e_times = []
+        e_times, e_split = [], []
         for k in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             if world > 1:
@@ -582,11 +582,14 @@ def run_ours(args):
                 sk.apply_ops(ops_h, keys_h)  # H2D inside the API call
             if world > 1 and not rep:
                 sk.broadcast_slim_(src=0)
+            t1 = time.perf_counter()
             sk.query_many_host(qk_h, out=qo_h)  # host keys in, host int64 estimates out
             torch.cuda.synchronize()
-            e = time.perf_counter() - t0
+            t2 = time.perf_counter()
+            e = t2 - t0
             if k >= args.warmup:
                 e_times.append(e)
+                e_split.append((t1 - t0, t2 - t1))
             flush.fill_(1)
         et = torch.tensor([sum(e_times) / len(e_times)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -602,6 +605,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int((n_ops * 5 if (rank == 0 or rep) else 0) + qn * 4 + dict_bytes),
                "d2h_bytes_per_step": int(qn * wb + (16388 if wire != _lib.WIRE_I64 else 0) + 24),
                "wire": {_lib.WIRE_C16: "u16 codes", _lib.WIRE_U32: "u32", _lib.WIRE_I64: "int64"}.get(wire, "?"),
+               "apply_ms": round(sum(a for a, _ in e_split) / len(e_split) * 1e3, 3),
+               "query_ms": round(sum(b for _, b in e_split) / len(e_split) * 1e3, 3),
                "note": "apply_ops from pinned host ops/keys; queries through SfSketch.query_many_host "
                        "(sfk_min_query_host: chunked H2D -> query kernel -> narrowed D2H, host threads widen "
                        "into the int64 output); wall clock, max over ranks"}
