@@ -491,3 +491,51 @@ def test_block_engine_bad_opcode_and_limits(oracle):
     finally:
         L.sfk_warp_batch_ops(prev_w)
         L.sfk_block_batch_ops(prev_b)
+
+
+@pytest.mark.parametrize("case", ["u64", "i64_neg", "u32", "i32_neg", "u16", "bool", "pylist_big", "records", "tensor_cpu"])
+def test_pinned_staging_matches_device_path(oracle, case):
+    """Small HOST batches are staged in pinned memory and read in place by
+    the kernels; every key dtype the reference accepts must give the same
+    state as the device-tensor path (normalize_keys' cast rules) and the
+    oracle."""
+    rng = np.random.default_rng(len(case))
+    n = 300
+    ops = np.zeros(n, np.uint8)
+    if case == "u64":
+        keys = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * np.uint64(2)
+    elif case == "i64_neg":
+        keys = rng.integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
+    elif case == "u32":
+        keys = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    elif case == "i32_neg":
+        keys = rng.integers(-(1 << 31), 1 << 31, size=n, dtype=np.int64).astype(np.int32)
+    elif case == "u16":
+        keys = rng.integers(0, 1 << 16, size=n).astype(np.uint16)
+    elif case == "bool":
+        keys = rng.random(n) < 0.5
+    elif case == "pylist_big":
+        keys = [int(x) for x in rng.integers(1 << 62, (1 << 63) - 1, size=n, dtype=np.int64) * 2 + 1]
+    elif case == "records":
+        keys = rng.integers(0, 256, size=(n, 13), dtype=np.uint8)
+    else:
+        keys = torch.from_numpy(rng.integers(0, 1 << 40, size=n, dtype=np.int64))
+    staged = make_sketch("sff", 4, 4096, 4, None, 3)
+    staged.apply_ops(ops, keys)  # host input: pinned staging
+    dev = make_sketch("sff", 4, 4096, 4, None, 3)
+    from paper_1701_04148_b200._ops import normalize_keys
+
+    kb = normalize_keys(keys)  # the device path's cast
+    dev.apply_ops(torch.from_numpy(ops).cuda(), kb)
+    np.testing.assert_array_equal(host(staged.slim.counters), host(dev.slim.counters))
+    np.testing.assert_array_equal(host(staged.fat.counters), host(dev.fat.counters))
+    if case == "records":
+        ko = oracle.keys_from_records(keys)
+    else:
+        ko = np.asarray(kb.tensor.cpu().numpy()).astype(np.uint64)
+    o = oracle.OracleSketch("sff", 4, 4096, 4, None, 3)
+    o.apply_ops(ops, ko)
+    np.testing.assert_array_equal(host(staged.slim.counters), o.slim)
+    # a phantom delete on a staged batch raises with the reference's message and key
+    with pytest.raises(P.PhantomDeletionError):
+        staged.apply_ops(np.ones(1, np.uint8), np.array([12345678901], np.uint64))
