@@ -215,7 +215,7 @@ static inline void split(int64_t n, int id, int T, int64_t* a, int64_t* b) {
 static int64_t g_chunk = 1 << 24;  // keys per chunk
 static int64_t g_wire = WIRE_AUTO;
 static int64_t g_direct = 0;      // every g_direct-th chunk returns int64 directly (pinned output only)
-static int64_t g_threads = 0;     // 0: 3/4 of the hardware threads (all of them contend with the DMA for host memory)
+static int64_t g_threads = 0;     // 0: 3/4 of the hardware threads / local ranks (all of them contend with the DMA for host memory)
 static int64_t g_ring = 4;        // chunks in flight
 static int64_t g_last_wire = 0;
 
@@ -304,7 +304,12 @@ static HostQ* ctx_for(int dev) {
     }
     g_ctx[dev] = q;
   }
-  const int t = std::max(1, g_threads > 0 ? (int)g_threads : (int)std::thread::hardware_concurrency() * 3 / 4);
+  // default: 3/4 of the hardware threads, shared among the node's ranks
+  // (torchrun's LOCAL_WORLD_SIZE) so N processes do not oversubscribe the host
+  int ranks = 1;
+  if (const char* lw = getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, atoi(lw));
+  const int t = std::max(1, g_threads > 0 ? (int)g_threads
+                                          : (int)std::thread::hardware_concurrency() * 3 / 4 / ranks);
   if (!g_pool || g_pool->size() != t) g_pool = new Pool(t);  // a replaced pool's threads stay parked
   return g_ctx[dev];
 }
