@@ -218,6 +218,8 @@ static int64_t g_direct = 0;      // every g_direct-th chunk returns int64 direc
 static int64_t g_threads = 0;     // 0: 3/4 of the hardware threads / local ranks (all of them contend with the DMA for host memory)
 static int64_t g_ring = 4;        // chunks in flight
 static int64_t g_last_wire = 0;
+// the knobs are read once per call and may be set from any thread
+static inline int64_t knob(const int64_t& k) { return __atomic_load_n(&k, __ATOMIC_RELAXED); }
 
 // ---------------------------------------------------------------- per-device state
 struct Slot {
@@ -308,7 +310,8 @@ static HostQ* ctx_for(int dev) {
   // (torchrun's LOCAL_WORLD_SIZE) so N processes do not oversubscribe the host
   int ranks = 1;
   if (const char* lw = getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, atoi(lw));
-  const int t = std::max(1, g_threads > 0 ? (int)g_threads
+  const int64_t gt = knob(g_threads);
+  const int t = std::max(1, gt > 0 ? (int)gt
                                           : (int)std::thread::hardware_concurrency() * 3 / 4 / ranks);
   if (!g_pool || g_pool->size() != t) g_pool = new Pool(t);  // a replaced pool's threads stay parked
   return g_ctx[dev];
@@ -358,14 +361,11 @@ int64_t sfk_host_query_config(int what, int64_t value) {
   int64_t* k = what == 0 ? &g_chunk : what == 1 ? &g_wire : what == 2 ? &g_direct : what == 3 ? &g_threads
              : what == 4 ? &g_ring : what == 5 ? &g_last_wire : nullptr;
   if (!k) return -1;
-  const int64_t prev = *k;
-  if (value >= 0 && what != 5) {
-    if (what == 0) value = std::max<int64_t>(4096, (value + 4095) & ~int64_t(4095));
-    if (what == 4) value = std::min<int64_t>(16, std::max<int64_t>(2, value));
-    if (what == 1 && value > WIRE_C16) return -1;
-    *k = value;
-  }
-  return prev;
+  if (value < 0 || what == 5) return knob(*k);
+  if (what == 0) value = std::max<int64_t>(4096, (value + 4095) & ~int64_t(4095));
+  if (what == 4) value = std::min<int64_t>(16, std::max<int64_t>(2, value));
+  if (what == 1 && value > WIRE_C16) return -1;
+  return __atomic_exchange_n(k, value, __ATOMIC_RELAXED);
 }
 
 int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const void* keys_host,
@@ -389,8 +389,8 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
   if (!q) return 1;
   std::lock_guard<std::mutex> guard(q->mu);
   const int64_t esz = key_kind == SFK_KEY_U32 ? 4 : key_kind == SFK_KEY_U64 ? 8 : rec_len;
-  const int ring = (int)g_ring;
-  const int64_t C = std::min<int64_t>(g_chunk, (n + 4095) & ~int64_t(4095));
+  const int ring = (int)knob(g_ring);
+  const int64_t C = std::min<int64_t>(knob(g_chunk), (n + 4095) & ~int64_t(4095));
   if (q->ensure(C, esz, ring)) return 1;
   const int64_t CH = C;
   const bool keys_pinned = is_pinned(keys_host), out_pinned = is_pinned(out_host);
@@ -400,7 +400,8 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
   cudaStreamWaitEvent(q->sc, q->e_start, 0);
 
   // wire format
-  int wire = (int)g_wire;
+  int wire = (int)knob(g_wire);
+  const int64_t direct_every = knob(g_direct);
   std::vector<uint32_t> dict;
   std::vector<int64_t> hi;
   if (wire == WIRE_AUTO || wire == WIRE_C16) {
@@ -418,12 +419,12 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
       wire = WIRE_U32;
     }
   }
-  g_last_wire = wire;
+  __atomic_store_n(&g_last_wire, (int64_t)wire, __ATOMIC_RELAXED);
   const int nd = (int)dict.size();
   const int64_t wb = wire == WIRE_C16 ? 2 : wire == WIRE_U32 ? 4 : 8;
   const int64_t nc = (n + CH - 1) / CH;
   auto direct = [&](int64_t j) {
-    return wire == WIRE_I64 || (out_pinned && g_direct > 0 && j % g_direct == g_direct - 1);
+    return wire == WIRE_I64 || (out_pinned && direct_every > 0 && j % direct_every == direct_every - 1);
   };
   Pool& pool = *g_pool;
   const bool avx = has_avx512();
