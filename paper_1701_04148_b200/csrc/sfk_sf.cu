@@ -121,6 +121,21 @@ struct Ctl {
   uint32_t bad_op;           // first op whose code is not 0 / 1 (NONE32: none); the batch is then a no-op
 };
 
+// One 32-B sector in a single 256-bit store (STG.E.256 on sm_100): the
+// scattered link / run records are whole sectors, and one store request per
+// sector instead of two halves the L2 store requests.
+__device__ __forceinline__ void st_sector(void* p, const uint4& a, const uint4& b) {
+#if SFK_LINKS_STREAMING
+  asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+#else
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+#endif
+}
+
 // ---------------------------------------------------------------- 1. hash_emit
 // kind: 0 bucketed (SFF/SF4: cell = bucket, slot in the low bits of val)
 //       1 flat fat (cell = fat index), 2 slim-only (cell = slim index)
@@ -437,13 +452,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
       // a sector written at another time costs L2 a DRAM fill.
       const uint32_t prev = (e > run.head) ? prev_t : NONE32;
       uint4* rec = reinterpret_cast<uint4*>(o.links) + ((size_t)t * o.D + row) * 2;
-#if SFK_LINKS_STREAMING
-      __stcs(rec, make_uint4(e - run.head, prev, rec_own, rec_oth));
-      __stcs(rec + 1, make_uint4(c, e, 0u, 0u));
-#else
-      rec[0] = make_uint4(e - run.head, prev, rec_own, rec_oth);
-      rec[1] = make_uint4(c, e, 0u, 0u);
-#endif
+      st_sector(rec, make_uint4(e - run.head, prev, rec_own, rec_oth), make_uint4(c, e, 0u, 0u));
     }
     prev_t = t;
   }
@@ -648,13 +657,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
     const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
     uint4* rec = links + ((size_t)t * D + row) * 2;
     const uint4 r0 = ign[e] ? make_uint4(0u, IGN_MARK, 0u, 0u) : make_uint4(before.cnt, before.last, 0u, 0u);
-#if SFK_LINKS_STREAMING
-    __stcs(rec, r0);
-    __stcs(rec + 1, make_uint4(c, e, 0u, 0u));
-#else
-    rec[0] = r0;
-    rec[1] = make_uint4(c, e, 0u, 0u);
-#endif
+    st_sector(rec, r0, make_uint4(c, e, 0u, 0u));
     run = op(run, el);
   }
 }
@@ -845,16 +848,13 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
         rec.O[i] = 0;
       }
     }
-#if SFK_LINKS_STREAMING
-    {  // whole sectors, streaming: read back by the engine (prefetched ahead)
+    {  // whole sectors (streaming): read back by the engine (prefetched ahead)
+      static_assert(sizeof(RunRec<D>) % 32 == 0, "run records are whole sectors");
       const uint4* src = reinterpret_cast<const uint4*>(&rec);
       uint4* dst = reinterpret_cast<uint4*>(a.recs + r);
 #pragma unroll
-      for (int q = 0; q < (int)(sizeof(RunRec<D>) / 16); ++q) __stcs(dst + q, src[q]);
+      for (int q = 0; q < (int)(sizeof(RunRec<D>) / 32); ++q) st_sector(dst + 2 * q, src[2 * q], src[2 * q + 1]);
     }
-#else
-    a.recs[r] = rec;
-#endif
   }
 }
 
