@@ -136,6 +136,13 @@ __device__ __forceinline__ void st_sector(void* p, const uint4& a, const uint4& 
 #endif
 }
 
+// and one 256-bit read-only load of a whole 32-B record
+__device__ __forceinline__ void ld_sector(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 // ---------------------------------------------------------------- 1. hash_emit
 // kind: 0 bucketed (SFF/SF4: cell = bucket, slot in the low bits of val)
 //       1 flat fat (cell = fat index), 2 slim-only (cell = slim index)
@@ -837,12 +844,15 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     const bool head_del = a.opflags[e0] & 1u;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      rec.cells[i] = a.links[((size_t)t * D + i) * 4 + 2].x;
-      rec.rank[i] = a.links[((size_t)t * D + i) * a.lstride].x;
+      // the (t, row) link record, one 256-bit load: {rank, prev, own count,
+      // max of the other slots} {cell, sorted position, 0, 0}
+      uint4 l0, l1;
+      ld_sector(a.links + ((size_t)t * D + i) * 4, l0, l1);
+      rec.cells[i] = l1.x;
+      rec.rank[i] = l0.x;
       if (a.obs2) {
-        const uint2 ob = a.obs2[((size_t)t * D + i) * a.lstride];
-        rec.A[i] = head_del ? ob.x + 1u : ob.x - 1u;
-        rec.O[i] = ob.y;
+        rec.A[i] = head_del ? l0.z + 1u : l0.z - 1u;
+        rec.O[i] = l0.w;
       } else {
         rec.A[i] = 0;
         rec.O[i] = 0;
