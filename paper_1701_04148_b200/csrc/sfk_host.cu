@@ -155,8 +155,9 @@ __attribute__((target("avx512f,avx512bw"))) static void widen32_avx512(const uin
 }
 
 // ---------------------------------------------------------------- thread pool
-// run(f) calls f(id, nthreads) on every pool thread and the caller (id 0) and
-// returns when all have finished. Workers sleep on a condition variable.
+// run(f, T) calls f(id, T) for id < T on pool threads and the caller (id 0)
+// and returns when all have finished. One pool of hardware-concurrency
+// threads lives for the process; workers sleep on a condition variable.
 class Pool {
  public:
   explicit Pool(int n) : n_(n < 1 ? 1 : n) {
@@ -164,16 +165,18 @@ class Pool {
     for (auto& t : th_) t.detach();  // never joined: lives for the process
   }
   int size() const { return n_; }
-  void run(const std::function<void(int, int)>& f) {
+  void run(const std::function<void(int, int)>& f, int T) {
+    T = std::max(1, std::min(T, n_));
     std::lock_guard<std::mutex> one(run_mu_);  // one job at a time (callers on several devices)
     {
       std::lock_guard<std::mutex> g(mu_);
       job_ = &f;
-      pending_ = n_ - 1;
+      active_ = T;
+      pending_ = T - 1;
       ++gen_;
     }
-    cv_.notify_all();
-    f(0, n_);
+    if (T > 1) cv_.notify_all();
+    f(0, T);
     std::unique_lock<std::mutex> g(mu_);
     done_.wait(g, [this] { return pending_ == 0; });
     job_ = nullptr;
@@ -184,13 +187,16 @@ class Pool {
     unsigned long long seen = 0;
     for (;;) {
       const std::function<void(int, int)>* f;
+      int T;
       {
         std::unique_lock<std::mutex> g(mu_);
         cv_.wait(g, [&] { return gen_ != seen; });
         seen = gen_;
         f = job_;
+        T = active_;
       }
-      (*f)(id, n_);
+      if (id >= T) continue;  // not part of this job
+      (*f)(id, T);
       std::lock_guard<std::mutex> g(mu_);
       if (--pending_ == 0) done_.notify_one();
     }
@@ -200,6 +206,7 @@ class Pool {
   std::mutex mu_, run_mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int, int)>* job_ = nullptr;
+  int active_ = 1;
   int pending_ = 0;
   unsigned long long gen_ = 0;
 };
@@ -270,7 +277,10 @@ struct HostQ {
   // ring of `ring` slots holding at least `ch` keys of `esz` bytes each
   int ensure(int64_t ch, int64_t esz, int ring) {
     if ((int)slots.size() == ring && chunk >= ch && kbytes >= ch * esz) return 0;
-    cudaDeviceSynchronize();
+    // the old slots may still be in use on this context's streams
+    cudaStreamSynchronize(sh);
+    cudaStreamSynchronize(sc);
+    cudaStreamSynchronize(sd);
     release_slots();
     slots.resize(ring);
     for (auto& s : slots) {
@@ -306,14 +316,7 @@ static HostQ* ctx_for(int dev) {
     }
     g_ctx[dev] = q;
   }
-  // default: 3/4 of the hardware threads, shared among the node's ranks
-  // (torchrun's LOCAL_WORLD_SIZE) so N processes do not oversubscribe the host
-  int ranks = 1;
-  if (const char* lw = getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, atoi(lw));
-  const int64_t gt = knob(g_threads);
-  const int t = std::max(1, gt > 0 ? (int)gt
-                                          : (int)std::thread::hardware_concurrency() * 3 / 4 / ranks);
-  if (!g_pool || g_pool->size() != t) g_pool = new Pool(t);  // a replaced pool's threads stay parked
+  if (!g_pool) g_pool = new Pool(std::max(1, (int)std::thread::hardware_concurrency()));
   return g_ctx[dev];
 }
 
@@ -427,6 +430,13 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
     return wire == WIRE_I64 || (out_pinned && direct_every > 0 && j % direct_every == direct_every - 1);
   };
   Pool& pool = *g_pool;
+  // threads: the knob, else 3/4 of the hardware threads shared among the
+  // node's ranks (torchrun's LOCAL_WORLD_SIZE), so N processes do not
+  // oversubscribe the host
+  int ranks = 1;
+  if (const char* lw = getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, atoi(lw));
+  const int64_t gt = knob(g_threads);
+  const int T = std::max(1, gt > 0 ? (int)gt : pool.size() * 3 / 4 / ranks);
   const bool avx = has_avx512();
   int rc = 0;
 
@@ -439,11 +449,11 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
       if (j >= ring) cudaEventSynchronize(s.e_h2d);  // pinned staging slot free
       char* dst = static_cast<char*>(s.hkeys);
       const int64_t bytes = m * esz;
-      pool.run([&](int id, int T) {
+      pool.run([&](int id, int TT) {
         int64_t x, y;
-        split(bytes, id, T, &x, &y);
+        split(bytes, id, TT, &x, &y);
         if (y > x) memcpy(dst + x, src + x, y - x);
-      });
+      }, T);
       src = dst;
     }
     cudaMemcpyAsync(s.dkeys, src, m * esz, cudaMemcpyHostToDevice, q->sh);
@@ -485,9 +495,9 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
       int64_t* o = out_host + a;
       const void* hw = s.hwire;
       const int64_t* hp = hi.data();
-      pool.run([&](int id, int T) {
+      pool.run([&](int id, int TT) {
         int64_t x, y;
-        split(m, id, T, &x, &y);
+        split(m, id, TT, &x, &y);
         if (y <= x) return;
         if (wire == WIRE_C16) {
           const uint16_t* cc = static_cast<const uint16_t*>(hw) + x;
@@ -498,7 +508,7 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
           if (avx) widen32_avx512(cc, y - x, o + x);
           else widen32_scalar(cc, y - x, o + x);
         }
-      });
+      }, T);
     }
     if (next < nc) rc = enqueue(next++);
   }
