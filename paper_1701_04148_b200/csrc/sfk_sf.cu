@@ -219,7 +219,7 @@ __device__ __forceinline__ SegState<Z> seg_combine(const SegState<Z>& a, const S
 }
 
 template <int Z>
-__device__ __forceinline__ SegState<Z> seg_identity() {
+__host__ __device__ __forceinline__ SegState<Z> seg_identity() {
   SegState<Z> r;
   r.flag = 0;
   r.head = 0;
@@ -227,6 +227,13 @@ __device__ __forceinline__ SegState<Z> seg_identity() {
   for (int k = 0; k < Z; ++k) r.v[k] = 0;
   return r;
 }
+
+template <int Z>
+struct SegStateOp {
+  __device__ __forceinline__ SegState<Z> operator()(const SegState<Z>& a, const SegState<Z>& b) const {
+    return seg_combine<Z>(a, b);
+  }
+};
 
 template <int Z>
 __device__ __forceinline__ SegState<Z> shfl_state(const SegState<Z>& s, int src_delta, bool up) {
@@ -307,41 +314,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_reduce_k(const uint32_t*
   if (threadIdx.x == 0) tile_agg[blockIdx.x] = block_tot;
 }
 
-// single block: exclusive scan of tile aggregates -> carry-in per tile
-template <int Z>
-__global__ void __launch_bounds__(1024) segscan_tiles_k(SegState<Z>* __restrict__ tile_agg, uint32_t ntiles) {
-  __shared__ SegState<Z> warp_tot[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t per = (ntiles + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = min(ntiles, threadIdx.x * per), hi = min(ntiles, lo + per);
-  SegState<Z> agg = seg_identity<Z>();
-  for (uint32_t k = lo; k < hi; ++k) agg = seg_combine<Z>(agg, tile_agg[k]);
-  SegState<Z> inc = agg;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    SegState<Z> o = shfl_state<Z>(inc, off, true);
-    if (lane >= off) inc = seg_combine<Z>(o, inc);
-  }
-  if (lane == 31) warp_tot[wid] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    SegState<Z> run = seg_identity<Z>();
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
-      SegState<Z> t = warp_tot[w];
-      warp_tot[w] = run;
-      run = seg_combine<Z>(run, t);
-    }
-  }
-  __syncthreads();
-  SegState<Z> ex = shfl_state<Z>(inc, 1, true);
-  if (lane == 0) ex = seg_identity<Z>();
-  SegState<Z> run = seg_combine<Z>(warp_tot[wid], ex);
-  for (uint32_t k = lo; k < hi; ++k) {
-    SegState<Z> t = tile_agg[k];
-    tile_agg[k] = run;  // exclusive
-    run = seg_combine<Z>(run, t);
-  }
-}
+
 
 struct ScanOut {
   const uint32_t* fat_init;  // snapshot of the fat (cell-major, Z per cell)
@@ -2271,6 +2244,15 @@ static uint64_t runrec_bytes(int d) {
   }
 }
 
+// bytes of run_scan's tile buffer for N pairs (any z <= 8)
+static size_t scan_tiles_bytes(uint64_t N) {
+  const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  size_t tbytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tbytes, (SegState<8>*)nullptr, (SegState<8>*)nullptr, SegStateOp<8>(),
+                                 seg_identity<8>(), (int)std::max<uint64_t>(ntiles, 1));
+  return 2 * ntiles * sizeof(SegState<8>) + 256 + tbytes + 256;
+}
+
 static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
   Carver cv(base, cap);
   Layout L{};
@@ -2285,7 +2267,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   if (kind == 1 || kind == 2) L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, key_sort_temp_bytes((uint32_t)n));
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
-  L.tiles = cv.take<char>(ntiles * (8 + 4 * (size_t)std::max(z, 1)) + 256);
+  L.tiles = cv.take<char>(scan_tiles_bytes(N));
   const bool bucketed = kind == 0 || kind == 4 || kind == 5;
   const bool gated = kind == 7 || kind == 8;
   const bool deletes = bucketed || kind == 6 || gated;  // runs carry delete bits (and observations)
@@ -2397,12 +2379,24 @@ template <int Z, bool HAS_FAT, int OBS, bool LINKS>
 static int run_scan(const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
                     cudaStream_t st) {
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  // tiles: [tile aggregates][their exclusive prefixes][the scan's temp storage]
   SegState<Z>* ta = static_cast<SegState<Z>*>(tiles);
+  SegState<Z>* tb = ta + ntiles;
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(tb + ntiles) + 255) & ~uintptr_t(255));
   { note_launch(); segscan_reduce_k<Z, HAS_FAT><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta); }
-  { note_launch(); segscan_tiles_k<Z><<<1, 1024, 0, st>>>(ta, ntiles); }
-  { note_launch(); segscan_apply_k<Z, HAS_FAT, OBS, LINKS><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, ta, so); }
+  // the tile carries: a multi-block decoupled look-back scan (one CTA scanning
+  // 23K 24-B states in a loop took ~0.12 ms per cfg-3 build)
+  size_t tbytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tbytes, ta, tb, SegStateOp<Z>(), seg_identity<Z>(), (int)ntiles, st);
+  cudaError_t e = cub::DeviceScan::ExclusiveScan(tmp, tbytes, ta, tb, SegStateOp<Z>(), seg_identity<Z>(), (int)ntiles, st);
+  if (e != cudaSuccess) {
+    set_error("segscan tiles: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  { note_launch(); segscan_apply_k<Z, HAS_FAT, OBS, LINKS><<<ntiles, SCAN_THREADS, 0, st>>>(keys, vals, N, kb, tb, so); }
   return check_launch("segscan");
 }
+
 
 template <bool HAS_FAT, int OBS, bool LINKS>
 static int run_scan_z(int z, const uint32_t* keys, const uint32_t* vals, uint32_t N, int kb, void* tiles, ScanOut so,
