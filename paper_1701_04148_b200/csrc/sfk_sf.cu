@@ -586,26 +586,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __
   BS(tmp).InclusiveScan(agg, inc, op, tot);
   if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
 }
-__global__ void __launch_bounds__(1024) filt_tiles_k(SegCnt* __restrict__ tile_agg, uint32_t ntiles) {
-  // one block: exclusive scan of the tile aggregates in place
-  typedef cub::BlockScan<SegCnt, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ SegCnt carry;
-  SegCntOp op;
-  if (threadIdx.x == 0) carry = SegCnt{0u, 0u, NONE32};
-  __syncthreads();
-  for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
-    const uint32_t k = b0 + threadIdx.x;
-    const SegCnt v = k < ntiles ? tile_agg[k] : SegCnt{0u, 0u, NONE32};
-    SegCnt ex, total;
-    BS(tmp).ExclusiveScan(v, ex, SegCnt{0u, 0u, NONE32}, op, total);
-    const SegCnt c0 = carry;
-    __syncthreads();
-    if (k < ntiles) tile_agg[k] = op(c0, ex);
-    if (threadIdx.x == 0) carry = op(c0, total);
-    __syncthreads();
-  }
-}
 // rewrites each element's 32-B link record: filtered rank and predecessor for
 // kept pairs; ignored pairs get prev = IGN_MARK (never a run continuation)
 constexpr uint32_t IGN_MARK = 0xFFFFFFFEu;
@@ -2253,6 +2233,15 @@ static size_t scan_tiles_bytes(uint64_t N) {
   return 2 * ntiles * sizeof(SegState<8>) + 256 + tbytes + 256;
 }
 
+// bytes of the filtered-link scan's tile buffer for N pairs
+static size_t filt_tiles_bytes(uint64_t N) {
+  const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  size_t tbytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tbytes, (SegCnt*)nullptr, (SegCnt*)nullptr, SegCntOp(),
+                                 SegCnt{0u, 0u, NONE32}, (int)std::max<uint64_t>(ntiles, 1));
+  return 2 * ntiles * sizeof(SegCnt) + 256 + tbytes + 256;
+}
+
 static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t wp, int z, int64_t n) {
   Carver cv(base, cap);
   Layout L{};
@@ -2311,7 +2300,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
     L.tb = cv.take<uint32_t>(sf1 ? n : 1);
     L.headpos = cv.take<uint32_t>(sf1 ? n : 1);
     L.ign = cv.take<uint8_t>(sf1 ? N : 1);
-    L.ftiles = cv.take<char>(sf1 ? ((N + SCAN_TILE - 1) / SCAN_TILE + 1) * 16 : 1);
+    L.ftiles = cv.take<char>(sf1 ? filt_tiles_bytes(N) : 1);
   }
   L.recs = cv.take<char>(engine ? (uint64_t)n * runrec_bytes(d) : 1);
   L.slim64 = cv.take<unsigned long long>(engine ? (uint64_t)d * w : 1);
@@ -2715,10 +2704,16 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   { note_launch(); key_count_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.headpos, L.tb, n, L.obs, cb); }
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign); }
+  // ftiles: [tile aggregates][their exclusive prefixes][scan temp storage]
   SegCnt* ft = static_cast<SegCnt*>(L.ftiles);
+  SegCnt* fc = ft + ntiles;
+  void* ftmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(fc + ntiles) + 255) & ~uintptr_t(255));
   { note_launch(); filt_reduce_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, ft); }
-  { note_launch(); filt_tiles_k<<<1, 1024, 0, st>>>(ft, ntiles); }
-  { note_launch(); filt_apply_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, ft, reinterpret_cast<uint4*>(L.links)); }
+  size_t fbytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
+  e = cub::DeviceScan::ExclusiveScan(ftmp, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
+  if (e != cudaSuccess) { set_error("filtered-link tiles: %s", cudaGetErrorString(e)); return (int)e; }
+  { note_launch(); filt_apply_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, reinterpret_cast<uint4*>(L.links)); }
   return check_launch("sf1_ignore");
 }
 
