@@ -147,12 +147,12 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
                        void* stream);
 
 /* Tuning of sfk_min_query_host (no reference counterpart). what:
- *   0 = keys per chunk (default 2^24);
+ *   0 = keys per chunk (default 2^22);
  *   1 = wire (0 auto, 1 int64, 2 u32, 3 u16 codes where exact, else u32);
  *   2 = every value-th chunk returns int64 directly when out_host is pinned
  *       (0 = never, default);
  *   3 = host threads (0 = 3/4 of the hardware threads / LOCAL_WORLD_SIZE);
- *   4 = chunks in flight (2-16, default 4);
+ *   4 = chunks in flight (2-16, default 8);
  *   5 = the wire the last call used (read only).
  * value < 0 only reads. Returns the previous value, or -1 for an unknown key
  * or value. */

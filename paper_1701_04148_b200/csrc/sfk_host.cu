@@ -219,11 +219,11 @@ static inline void split(int64_t n, int id, int T, int64_t* a, int64_t* b) {
 }
 
 // ---------------------------------------------------------------- configuration
-static int64_t g_chunk = 1 << 24;  // keys per chunk
+static int64_t g_chunk = 1 << 22;  // keys per chunk (8 MiB of u16 codes: read back while still in the LLC)
 static int64_t g_wire = WIRE_AUTO;
 static int64_t g_direct = 0;      // every g_direct-th chunk returns int64 directly (pinned output only)
 static int64_t g_threads = 0;     // 0: 3/4 of the hardware threads / local ranks (all of them contend with the DMA for host memory)
-static int64_t g_ring = 4;        // chunks in flight
+static int64_t g_ring = 8;        // chunks in flight
 static int64_t g_last_wire = 0;
 // the knobs are read once per call and may be set from any thread
 static inline int64_t knob(const int64_t& k) { return __atomic_load_n(&k, __ATOMIC_RELAXED); }
