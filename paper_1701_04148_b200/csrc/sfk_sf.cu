@@ -2061,27 +2061,68 @@ template <int D>
 __global__ void __launch_bounds__(256) cm_atomic_k(uint32_t* __restrict__ counters, Seeds<D> seeds, Mod wm, uint32_t w,
                                                    const uint8_t* __restrict__ ops, KeySrc keys, int64_t n,
                                                    const Ctl* ctl) {
+  // Two aggregation levels before a global atomic:
+  //   * warp: the lanes of a 32-op group with the same cell merge (match_any);
+  //   * block: a direct-mapped shared-memory table claims a slot for the
+  //     first cell that hashes to it and sums every later update of that
+  //     cell in shared memory; a cell whose slot is taken goes to L2 as
+  //     before. A Zipf-hot cell appears within the first ops a block sees,
+  //     so its updates (otherwise serialised on one L2 address) become one
+  //     atomic per block at the end.
+  // CM sums commute and the host precheck rules out saturation and
+  // phantoms, so the order of the updates does not matter.
+  constexpr int CM_UNR = 4;
+  constexpr int CM_SLOTS = 4096;
+  constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+  __shared__ uint32_t tag[CM_SLOTS];
+  __shared__ int32_t cnt[CM_SLOTS];
+  for (int q = threadIdx.x; q < CM_SLOTS; q += blockDim.x) tag[q] = EMPTY, cnt[q] = 0;
+  __syncthreads();
   const int64_t limit = ctl ? (ctl->fail_t == NONE32 ? n : (int64_t)ctl->fail_t) : n;
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp_id * 32; base < limit; base += nwarps * 32) {
-    const int64_t t = base + lane;
-    const bool active = t < limit;
-    const unsigned amask = __ballot_sync(0xffffffffu, active);
-    if (!active) continue;
-    const uint64_t key = load_key(keys, t);
-    const uint32_t op = ops[t];
-    const unsigned del = __ballot_sync(amask, op != 0);
+  for (int64_t base = warp_id * 32 * CM_UNR; base < limit; base += nwarps * 32 * CM_UNR) {
+    uint64_t key[CM_UNR];
+    uint32_t op[CM_UNR];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      const uint32_t cell = (uint32_t)i * w + (uint32_t)bucket(key, seeds.s[i], wm);
-      const unsigned g = __match_any_sync(amask, cell);
-      if (lane == __ffs(g) - 1) {
-        const int net = __popc(g & ~del) - __popc(g & del);
-        if (net) atomicAdd(counters + cell, (uint32_t)net);
+    for (int u = 0; u < CM_UNR; ++u) {
+      const int64_t t = base + u * 32 + lane;
+      key[u] = t < limit ? load_key(keys, t) : 0ull;
+      op[u] = t < limit ? ops[t] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < CM_UNR; ++u) {
+      const int64_t t = base + u * 32 + lane;
+      const bool active = t < limit;
+      const unsigned amask = __ballot_sync(0xffffffffu, active);
+      if (!active) continue;
+      const unsigned del = __ballot_sync(amask, op[u] != 0);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const uint32_t cell = (uint32_t)i * w + (uint32_t)bucket(key[u], seeds.s[i], wm);
+        const unsigned g = __match_any_sync(amask, cell);
+        if (lane == __ffs(g) - 1) {
+          const int net = __popc(g & ~del) - __popc(g & del);
+          if (net) {
+            const uint32_t slot = (cell * 0x9E3779B1u) >> (32 - 12);  // log2(CM_SLOTS) = 12
+            uint32_t tg = tag[slot];
+            if (tg == EMPTY) {
+              const uint32_t old = atomicCAS(&tag[slot], EMPTY, cell);
+              tg = old == EMPTY ? cell : old;
+            }
+            if (tg == cell) atomicAdd(&cnt[slot], net);
+            else atomicAdd(counters + cell, (uint32_t)net);
+          }
+        }
       }
     }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < CM_SLOTS; q += blockDim.x) {
+    const uint32_t tg = tag[q];
+    const int32_t c = cnt[q];
+    if (tg != EMPTY && c) atomicAdd(counters + tg, (uint32_t)c);
   }
 }
 
