@@ -342,34 +342,94 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
   __shared__ SegState<Z> warp_tot[SCAN_THREADS / 32];
   __shared__ SegState<Z> block_tot;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  // this thread's elements, staged in registers once: cell, value, segment
+  // head / end flags, and (fat kinds) the cell's fat snapshot; the snapshot
+  // loads are issued before the block scan so their latency overlaps it
+  uint32_t cc[SCAN_ITEMS], vv[SCAN_ITEMS];
+  if (base + SCAN_ITEMS <= N) {
+    const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
+    const uint4* vp = reinterpret_cast<const uint4*>(vals + base);
+#pragma unroll
+    for (int h = 0; h < SCAN_ITEMS / 4; ++h) {
+      const uint4 a = __ldg(kp + h), b = __ldg(vp + h);
+      cc[4 * h] = a.x, cc[4 * h + 1] = a.y, cc[4 * h + 2] = a.z, cc[4 * h + 3] = a.w;
+      vv[4 * h] = b.x, vv[4 * h + 1] = b.y, vv[4 * h + 2] = b.z, vv[4 * h + 3] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      cc[q] = base + q < N ? keys[base + q] : U32MAX;
+      vv[q] = base + q < N ? vals[base + q] : 0u;
+    }
+  }
+  const bool has_prev = base > 0 && base < N;
+  const uint32_t c_before = has_prev ? keys[base - 1] : 0u;
+  const uint32_t t_before = has_prev ? (vals[base - 1] >> (kb + 1)) : NONE32;
+  const bool has_next = base + SCAN_ITEMS < N;
+  const uint32_t c_after = has_next ? keys[base + SCAN_ITEMS] : 0u;
+  uint32_t init[HAS_FAT ? SCAN_ITEMS : 1][HAS_FAT ? Z : 1];
+  if (HAS_FAT) {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      if (base + q < N) {
+        if (Z == 4) {
+          const uint4 f = __ldg(reinterpret_cast<const uint4*>(o.fat_init) + cc[q]);
+          init[q][0] = f.x, init[q][1 % Z] = f.y, init[q][2 % Z] = f.z, init[q][3 % Z] = f.w;
+        } else {
+#pragma unroll
+          for (int q2 = 0; q2 < Z; ++q2) init[q][q2] = __ldg(o.fat_init + (size_t)cc[q] * Z + q2);
+        }
+      } else {
+#pragma unroll
+        for (int q2 = 0; q2 < Z; ++q2) init[q][q2] = 0u;
+      }
+    }
+  }
+  bool hd[SCAN_ITEMS];
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) hd[q] = (base + q == 0) || (q ? cc[q - 1] : c_before) != cc[q];
+  auto elem = [&](int q) {
+    SegState<Z> s = seg_identity<Z>();
+    s.flag = hd[q] ? 1u : 0u;
+    s.head = base + q;
+    if (HAS_FAT) {
+      const uint32_t k = vv[q] & ((1u << kb) - 1u);
+      const int32_t dl = ((vv[q] >> kb) & 1u) ? -1 : 1;
+#pragma unroll
+      for (int q2 = 0; q2 < Z; ++q2) s.v[q2] = (q2 == (int)k) ? dl : 0;
+    }
+    return s;
+  };
   SegState<Z> agg = seg_identity<Z>();
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    uint32_t e = base + q;
-    if (e < N) agg = seg_combine<Z>(agg, elem_state<Z, HAS_FAT>(keys, vals, e, kb));
-  }
+  for (int q = 0; q < SCAN_ITEMS; ++q)
+    if (base + q < N) agg = seg_combine<Z>(agg, elem(q));
   SegState<Z> run = block_exclusive<Z>(agg, warp_tot, &block_tot);
   run = seg_combine<Z>(carry[blockIdx.x], run);
   uint32_t local_fail = NONE32;
-  uint32_t prev_t = (base > 0 && base < N) ? (vals[base - 1] >> (kb + 1)) : NONE32;
-#pragma unroll 1
+  uint32_t prev_t = t_before;
+#pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t e = base + q;
     if (e >= N) break;
-    const SegState<Z> s = elem_state<Z, HAS_FAT>(keys, vals, e, kb);
-    run = seg_combine<Z>(run, s);
-    const uint32_t c = keys[e];
-    const uint32_t v = vals[e];
+    run = seg_combine<Z>(run, elem(q));
+    const uint32_t c = cc[q];
+    const uint32_t v = vv[q];
     const uint32_t t = v >> (kb + 1);
     const uint32_t op = (v >> kb) & 1u;
     const uint32_t row = c / o.row_cells;
     uint32_t rec_own = 0, rec_oth = 0;  // observations carried in the link record
     if (HAS_FAT) {
       const uint32_t k = v & ((1u << kb) - 1u);
-      uint32_t init[Z];
+      uint32_t own_init = init[q][0];
 #pragma unroll
-      for (int q2 = 0; q2 < Z; ++q2) init[q2] = __ldg(o.fat_init + (size_t)c * Z + q2);
-      const int64_t post_own = (int64_t)init[k] + (int64_t)run.v[k];
+      for (int q2 = 1; q2 < Z; ++q2)
+        if (q2 == (int)k) own_init = init[q][q2];
+      int32_t own_d = run.v[0];
+#pragma unroll
+      for (int q2 = 1; q2 < Z; ++q2)
+        if (q2 == (int)k) own_d = run.v[q2];
+      const int64_t post_own = (int64_t)own_init + (int64_t)own_d;
       const int64_t pre_own = post_own + (op ? 1 : -1);
       if (op == 0 ? (pre_own == (int64_t)U32MAX) : (pre_own == 0)) local_fail = min(local_fail, t);
       if (WRITE_OBS == 2 || WRITE_OBS == 3) {
@@ -377,12 +437,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
         if (WRITE_OBS == 2) {
 #pragma unroll
           for (int q2 = 0; q2 < Z; ++q2)
-            if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+            if (q2 != (int)k) others = max(others, (uint32_t)((int64_t)init[q][q2] + run.v[q2]));
         } else {
           uint64_t sum = 0;
 #pragma unroll
           for (int q2 = 0; q2 < Z; ++q2)
-            if (q2 != (int)k) sum += (uint64_t)((int64_t)init[q2] + run.v[q2]);
+            if (q2 != (int)k) sum += (uint64_t)((int64_t)init[q][q2] + run.v[q2]);
           others = (uint32_t)min(sum, (uint64_t)U32MAX);
         }
         if (WRITE_LINKS) {
@@ -409,14 +469,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
         } else {
           ob = 0;
 #pragma unroll
-          for (int q2 = 0; q2 < Z; ++q2) ob = max(ob, (uint32_t)((int64_t)init[q2] + run.v[q2]));
+          for (int q2 = 0; q2 < Z; ++q2) ob = max(ob, (uint32_t)((int64_t)init[q][q2] + run.v[q2]));
         }
         o.obs[(size_t)t * o.D + row] = ob;
       }
-      const bool last = (e + 1 == N) || (keys[e + 1] != c);
+      const bool last = (e + 1 == N) || ((q + 1 < SCAN_ITEMS) ? cc[q + 1 < SCAN_ITEMS ? q + 1 : q] : c_after) != c;
       if (last) {
 #pragma unroll
-        for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q2] + run.v[q2]);
+        for (int q2 = 0; q2 < Z; ++q2) o.fat_out[(size_t)c * Z + q2] = (uint32_t)((int64_t)init[q][q2] + run.v[q2]);
       }
     }
     if (WRITE_OBS == 5) {
@@ -436,6 +496,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_apply_k(const uint32_t* 
     }
     prev_t = t;
   }
+  (void)has_next;
   if (HAS_FAT && local_fail != NONE32) atomicMin(&o.ctl->fail_t, local_fail);
 }
 
@@ -562,10 +623,53 @@ struct SegCntOp {
     return SegCnt{a.flag, a.cnt + b.cnt, b.last != NONE32 ? b.last : a.last};
   }
 };
-__device__ __forceinline__ SegCnt segcnt_elem(const uint32_t* keys, const uint32_t* vals, const uint8_t* ign,
-                                              uint32_t e) {
-  const bool keep = !ign[e];
-  return SegCnt{(e == 0 || keys[e - 1] != keys[e]) ? 1u : 0u, keep ? 1u : 0u, keep ? (vals[e] >> 1) : NONE32};
+// a thread's SCAN_ITEMS consecutive elements, staged in registers once:
+// cell, op, dropped flag, and the elements' {head, kept, op} scan states
+struct FiltItems {
+  uint32_t c[SCAN_ITEMS], t[SCAN_ITEMS];
+  uint32_t ign;  // bit q: element q is dropped
+  uint32_t hd;   // bit q: element q heads its cell's segment
+};
+__device__ __forceinline__ void filt_load(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                          const uint8_t* __restrict__ ign, uint32_t N, uint32_t base, FiltItems& it) {
+  uint32_t vv[SCAN_ITEMS];
+  it.ign = 0;
+  if (base + SCAN_ITEMS <= N) {
+    const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
+    const uint4* vp = reinterpret_cast<const uint4*>(vals + base);
+#pragma unroll
+    for (int h = 0; h < SCAN_ITEMS / 4; ++h) {
+      const uint4 a = __ldg(kp + h), b = __ldg(vp + h);
+      it.c[4 * h] = a.x, it.c[4 * h + 1] = a.y, it.c[4 * h + 2] = a.z, it.c[4 * h + 3] = a.w;
+      vv[4 * h] = b.x, vv[4 * h + 1] = b.y, vv[4 * h + 2] = b.z, vv[4 * h + 3] = b.w;
+    }
+    static_assert(SCAN_ITEMS == 8, "one 8-B load of the dropped flags");
+    const uint2 g = __ldg(reinterpret_cast<const uint2*>(ign + base));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      it.ign |= ((g.x >> (8 * q)) & 1u) << q;
+      it.ign |= ((g.y >> (8 * q)) & 1u) << (q + 4);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      const bool in = base + q < N;
+      it.c[q] = in ? keys[base + q] : U32MAX;
+      vv[q] = in ? vals[base + q] : 0u;
+      if (in && ign[base + q]) it.ign |= 1u << q;
+    }
+  }
+  const uint32_t c_before = (base > 0 && base < N) ? keys[base - 1] : 0u;
+  it.hd = 0;
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    it.t[q] = vv[q] >> 1;
+    if (base + q == 0 || (q ? it.c[q - 1] : c_before) != it.c[q]) it.hd |= 1u << q;
+  }
+}
+__device__ __forceinline__ SegCnt filt_elem(const FiltItems& it, int q) {
+  const bool keep = !((it.ign >> q) & 1u);
+  return SegCnt{(it.hd >> q) & 1u, keep ? 1u : 0u, keep ? it.t[q] : NONE32};
 }
 __global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __restrict__ keys,
                                                              const uint32_t* __restrict__ vals,
@@ -574,13 +678,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __
   typedef cub::BlockScan<SegCnt, SCAN_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  FiltItems it;
+  filt_load(keys, vals, ign, N, base, it);
   SegCntOp op;
   SegCnt agg{0u, 0u, NONE32};
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const uint32_t e = base + q;
-    if (e < N) agg = op(agg, segcnt_elem(keys, vals, ign, e));
-  }
+  for (int q = 0; q < SCAN_ITEMS; ++q)
+    if (base + q < N) agg = op(agg, filt_elem(it, q));
   // ordered (non-commutative): the block's inclusive scan, last thread's value
   SegCnt inc, tot;
   BS(tmp).InclusiveScan(agg, inc, op, tot);
@@ -598,25 +702,25 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
   __shared__ typename BS::TempStorage tmp;
   SegCntOp op;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  FiltItems it;
+  filt_load(keys, vals, ign, N, base, it);
   SegCnt agg{0u, 0u, NONE32};
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const uint32_t e = base + q;
-    if (e < N) agg = op(agg, segcnt_elem(keys, vals, ign, e));
-  }
+  for (int q = 0; q < SCAN_ITEMS; ++q)
+    if (base + q < N) agg = op(agg, filt_elem(it, q));
   SegCnt run;
   BS(tmp).ExclusiveScan(agg, run, SegCnt{0u, 0u, NONE32}, op);
   if (threadIdx.x == 0) run = SegCnt{0u, 0u, NONE32};
   run = op(carry[blockIdx.x], run);
-#pragma unroll 1
+#pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t e = base + q;
     if (e >= N) break;
-    const uint32_t c = keys[e], t = vals[e] >> 1, row = c / row_cells;
-    const SegCnt el = segcnt_elem(keys, vals, ign, e);
+    const uint32_t c = it.c[q], t = it.t[q], row = c / row_cells;
+    const SegCnt el = filt_elem(it, q);
     const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
     uint4* rec = links + ((size_t)t * D + row) * 2;
-    const uint4 r0 = ign[e] ? make_uint4(0u, IGN_MARK, 0u, 0u) : make_uint4(before.cnt, before.last, 0u, 0u);
+    const uint4 r0 = ((it.ign >> q) & 1u) ? make_uint4(0u, IGN_MARK, 0u, 0u) : make_uint4(before.cnt, before.last, 0u, 0u);
     st_sector(rec, r0, make_uint4(c, e, 0u, 0u));
     run = op(run, el);
   }
