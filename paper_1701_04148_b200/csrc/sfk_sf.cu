@@ -32,6 +32,7 @@
 // Insert-only runs collapse in closed form (b_min strictly increases along
 // a same-key insert run, so once a raise happens every later op raises):
 // s raises give c_i' = max(c_i, m0 + s).
+#include <cstring>
 #include <cub/cub.cuh>
 
 #include "sfk_common.cuh"
@@ -541,16 +542,61 @@ __global__ void __launch_bounds__(512) bmin_bucket_k(const uint32_t* __restrict_
 __global__ void iota_k(uint32_t* __restrict__ t, uint32_t n) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) t[j] = j;
 }
-__global__ void key_heads_k(const uint64_t* __restrict__ ks, uint32_t n, uint32_t* __restrict__ headpos) {
+template <typename K>
+__global__ void key_heads_k(const K* __restrict__ ks, uint32_t n, uint32_t* __restrict__ headpos) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     headpos[j] = (j == 0 || ks[j] != ks[j - 1]) ? j : 0u;
 }
-// packed per op: {key count << 32 | b_min}, one 8-B gather for the ignore scan
-__global__ void key_count_k(const uint32_t* __restrict__ headpos, const uint32_t* __restrict__ ts, uint32_t n,
-                            const uint32_t* __restrict__ bmin, unsigned long long* __restrict__ cb) {
+// 64-bit keys: a group id per op from an open-addressing table (linear
+// probing, one CAS per distinct key), so the stable key grouping sorts
+// ceil(log2(cap + 1) / 8) passes of 4-B ids instead of 8 passes of 8-B keys.
+// Ids are table slots (the key ~0, the empty mark, gets the id cap); group
+// order varies between runs, grouping does not, and nothing downstream
+// depends on the order of the groups.
+constexpr unsigned long long SLOT_EMPTY = ~0ull;
+__global__ void key_slot_k(const uint64_t* __restrict__ keys, uint32_t n, unsigned long long* __restrict__ table,
+                           uint32_t cap, uint32_t* __restrict__ slot) {
+  const uint32_t mask = cap - 1u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[t];
+    uint32_t s = cap;
+    if (k != SLOT_EMPTY) {
+      s = (uint32_t)(mix64(k ^ 0x2545F4914F6CDD1Dull) >> 32) & mask;
+      while (true) {
+        const unsigned long long cur = *reinterpret_cast<volatile const unsigned long long*>(table + s);
+        if (cur == k) break;
+        if (cur == SLOT_EMPTY) {
+          const unsigned long long prev = atomicCAS(table + s, SLOT_EMPTY, k);
+          if (prev == SLOT_EMPTY || prev == k) break;
+        }
+        s = (s + 1u) & mask;
+      }
+    }
+    slot[t] = s;
+  }
+}
+static uint32_t slot_cap(uint32_t n) {  // a power of two >= 1.25 n (load <= 0.8 with every key distinct)
+  uint64_t c = 1024;
+  while (c < (uint64_t)n + n / 4) c <<= 1;
+  return (uint32_t)c;
+}
+
+// tile rule: {key count << 32 | b_min} per op, one 8-B gather for the ignore scan
+__global__ void cb_pack_k(const uint2* __restrict__ meta, const uint32_t* __restrict__ bmin, uint32_t n,
+                          unsigned long long* __restrict__ cb) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    cb[t] = ((unsigned long long)meta[t].x << 32) | bmin[t];
+}
+
+// key order -> op order: {count of the op's key up to and including it, the
+// key's previous op (NONE32 for its first)} in one 8-B store per op
+template <typename K>
+__global__ void key_meta_k(const K* __restrict__ ks, const uint32_t* __restrict__ tb,
+                           const uint32_t* __restrict__ headpos, uint32_t n, uint2* __restrict__ meta) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t t = ts[j];
-    cb[t] = ((unsigned long long)(j - headpos[j] + 1u) << 32) | bmin[t];
+    const uint32_t t = tb[j];
+    const uint32_t kp = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
+    meta[t] = make_uint2(j - headpos[j] + 1u, kp);
   }
 }
 
@@ -741,7 +787,7 @@ struct RunArgs {
   uint32_t* headflag;      // [t] (written by runs_head_k)
   int has_ign;             // SF1 / CU ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
   const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
-  const uint32_t* kprev;   // key order: the previous op of the same key (NONE32 for a key's first op)
+  const uint2* kmeta;      // key order: {key count, the previous op of the same key (NONE32 for a key's first op)}
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
   uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
@@ -783,18 +829,12 @@ __global__ void __launch_bounds__(256) runs_head_k(RunArgs<D> a) {
     if (cont) {
       // key order: p must be the key's previous op, so a run is a contiguous
       // stretch of its key's ops; row-0 order: the same key
-      cont = a.kprev ? a.kprev[t] == p : load_key(a.keys, p) == load_key(a.keys, t);
+      cont = a.kmeta ? a.kmeta[t].y == p : load_key(a.keys, p) == load_key(a.keys, t);
     }
     a.headflag[t] = (valid && !cont) ? 1u : 0u;
   }
 }
 
-// key order: the previous op of the same key, from the key-sorted op list
-__global__ void key_prev_k(const uint64_t* __restrict__ ks, const uint32_t* __restrict__ tb, uint32_t n,
-                           uint32_t* __restrict__ kprev) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    kprev[tb[j]] = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
-}
 
 // Per op in row-0 order: flags, b_min (SF1/SF2), delete bits, run boundaries.
 template <int D>
@@ -2336,8 +2376,9 @@ struct Layout {
   uint32_t *bnd, *bidx, *bpos, *isdel, *delpre;
   uint32_t* ridx;
   uint64_t *k64a, *k64b;          // SF1 ignore pass: materialised keys, sorted
+  unsigned long long* htab;       //   key -> group id table (64-bit keys)
   uint32_t *ta, *tb, *headpos;     //   op ids, sorted op ids, key segment heads
-  uint32_t* kprev;                 //   previous op of the same key
+  uint2* meta;                     //   per op: {key count, previous op of the same key}
   uint8_t* ign;                    //   dropped (op, row) flags in cell order
   void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
@@ -2438,9 +2479,10 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.ridx = cv.take<uint32_t>(engine ? n : 1);
   {
     const bool sf1 = kind == 1 || kind == 2;  // SF1 and CU: the ignore pass
-    L.kprev = cv.take<uint32_t>(sf1 ? n : 1);
+    L.meta = cv.take<uint2>(sf1 ? n : 1);
     L.k64a = cv.take<uint64_t>(sf1 ? n : 1);
     L.k64b = cv.take<uint64_t>(sf1 ? n : 1);
+    L.htab = cv.take<unsigned long long>(sf1 ? slot_cap((uint32_t)std::max<int64_t>(n, 1)) : 1);
     L.ta = cv.take<uint32_t>(sf1 ? n : 1);
     L.tb = cv.take<uint32_t>(sf1 ? n : 1);
     L.headpos = cv.take<uint32_t>(sf1 ? n : 1);
@@ -2649,7 +2691,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.isdel = L.isdel;
   ra.has_ign = has_ign ? 1 : 0;
   ra.order = has_ign ? L.tb : nullptr;
-  ra.kprev = has_ign ? L.kprev : nullptr;
+  ra.kmeta = has_ign ? L.meta : nullptr;
   ra.ctl = L.ctl;
   { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
@@ -2837,18 +2879,38 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   if (int r = launch_load_keys(ks, n, L.k64a, st)) return r;
   { note_launch(); iota_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.ta, n); }
   size_t bytes = L.cub_tmp_bytes;
-  const int kbits = ks.kind == SFK_KEY_U32 ? 32 : 64;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k64a, L.k64b, L.ta, L.tb, (int)n, 0, kbits, st);
-  if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
-  { note_launch(); key_heads_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, n, L.headpos); }
-  { note_launch(); key_prev_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, L.tb, n, L.kprev); }
-  bytes = L.cub_tmp_bytes;
-  e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
-  if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
-  unsigned long long* cb = reinterpret_cast<unsigned long long*>(L.k64a);  // free after the key sort
-  { note_launch(); key_count_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.headpos, L.tb, n, L.obs, cb); }
+  cudaError_t e;
+  static const bool key_sort = getenv("SFK_KEY_GROUP") && !strcmp(getenv("SFK_KEY_GROUP"), "sort");  // A/B knob
+  if (ks.kind != SFK_KEY_U32 && !key_sort) {
+    // 64-bit keys: group by table slot (4-B ids, see key_slot_k)
+    const uint32_t cap = slot_cap(n);
+    uint32_t* sid = reinterpret_cast<uint32_t*>(L.k64b);  // [0, n): ids in op order, [n, 2n): sorted
+    cudaMemsetAsync(L.htab, 0xFF, (size_t)cap * 8, st);
+    { note_launch(); key_slot_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(L.k64a, n, L.htab, cap, sid); }
+    e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, sid, sid + n, L.ta, L.tb, (int)n, 0,
+                                        bits_for((uint64_t)cap + 1), st);
+    if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_heads_k<uint32_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(sid + n, n, L.headpos); }
+    bytes = L.cub_tmp_bytes;
+    e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
+    if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_meta_k<uint32_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(sid + n, L.tb, L.headpos, n, L.meta); }
+  } else {
+    const int kbits = ks.kind == SFK_KEY_U32 ? 32 : 64;
+    e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k64a, L.k64b, L.ta, L.tb, (int)n, 0, kbits, st);
+    if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_heads_k<uint64_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, n, L.headpos); }
+    bytes = L.cub_tmp_bytes;
+    e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
+    if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_meta_k<uint64_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, L.tb, L.headpos, n, L.meta); }
+  }
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
-  { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign); }
+  {  // {key count, b_min} per op, gathered by the tile scan in cell order
+    unsigned long long* cb = reinterpret_cast<unsigned long long*>(L.k64a);  // free after the key grouping
+    { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.meta, L.obs, n, cb); }
+    { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign); }
+  }
   // ftiles: [tile aggregates][their exclusive prefixes][scan temp storage]
   SegCnt* ft = static_cast<SegCnt*>(L.ftiles);
   SegCnt* fc = ft + ntiles;
