@@ -2852,21 +2852,41 @@ __global__ void fold_scatter_k(const uint32_t* __restrict__ grp, uint32_t* __res
 int launch_load_keys(KeySrc ks, int64_t n, uint64_t* out, cudaStream_t st);  // sfk_query.cu
 
 // per-op b_min from the fat scan's (t, candidate) pairs in k_in / v_in (see
-// bmin_bucket_k); uses k_out / v_out (the fat-sorted pairs are dead by then)
+// bmin_bucket_k); uses k_out / v_out (the fat-sorted pairs are dead by then).
+// When t has more than 8 bits above BMIN_BITS, one 8-bit partial sort pass
+// groups the pairs into 256 ranges of consecutive ops instead of two passes
+// down to 2^BMIN_BITS, and the minima are taken with L2 atomics: CTAs walk
+// the grouped pairs in order, so the ranges they update at any time (a few
+// MB of b_min words) stay in L2 (cfg 4: one 400M-pair pass saved).
+__global__ void __launch_bounds__(256) bmin_l2_k(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ tval,
+                                                 uint32_t N, uint32_t* __restrict__ obs) {
+  const uint32_t e0 = blockIdx.x * 2048u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t e = e0 + q * 256u + threadIdx.x;
+    if (e < N) atomicMin(obs + __ldg(tkey + e), __ldg(tval + e));
+  }
+}
 static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_t st) {
   const int tbits = bits_for((uint64_t)n);
   const uint32_t* tk = L.k_in;
   const uint32_t* tv = L.v_in;
+  const bool l2 = tbits - BMIN_BITS > 8;
   if (tbits > BMIN_BITS) {
     size_t bytes = L.cub_tmp_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N,
-                                                    BMIN_BITS, tbits, st);
+                                                    l2 ? tbits - 8 : BMIN_BITS, tbits, st);
     if (e != cudaSuccess) {
       set_error("b_min sort: %s", cudaGetErrorString(e));
       return (int)e;
     }
     tk = L.k_out;
     tv = L.v_out;
+  }
+  if (l2) {
+    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
+    { note_launch(); bmin_l2_k<<<(N + 2047) / 2048, 256, 0, st>>>(tk, tv, N, L.obs); }
+    return check_launch("bmin_l2");
   }
   const uint32_t nb = (n + (1u << BMIN_BITS) - 1) >> BMIN_BITS;
   { note_launch(); bmin_bucket_k<<<nb, 512, 0, st>>>(tk, tv, n, (uint32_t)d, L.obs); }
