@@ -306,10 +306,36 @@ __global__ void __launch_bounds__(SCAN_THREADS) segscan_reduce_k(const uint32_t*
   __shared__ SegState<Z> block_tot;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   SegState<Z> agg = seg_identity<Z>();
+  if (base + SCAN_ITEMS <= N) {  // vector loads (see sf1_ignore_k)
+    uint32_t cc[SCAN_ITEMS], vv[SCAN_ITEMS];
+    const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
+    const uint4* vp = reinterpret_cast<const uint4*>(vals + base);
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    uint32_t e = base + q;
-    if (e < N) agg = seg_combine<Z>(agg, elem_state<Z, HAS_FAT>(keys, vals, e, kb));
+    for (int h = 0; h < SCAN_ITEMS / 4; ++h) {
+      const uint4 a = __ldg(kp + h), b = __ldg(vp + h);
+      cc[4 * h] = a.x, cc[4 * h + 1] = a.y, cc[4 * h + 2] = a.z, cc[4 * h + 3] = a.w;
+      vv[4 * h] = b.x, vv[4 * h + 1] = b.y, vv[4 * h + 2] = b.z, vv[4 * h + 3] = b.w;
+    }
+    const uint32_t c_before = base > 0 ? keys[base - 1] : 0u;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      SegState<Z> el = seg_identity<Z>();
+      el.flag = (base + q == 0) || (q ? cc[q - 1] : c_before) != cc[q];
+      el.head = base + q;
+      if (HAS_FAT) {
+        const uint32_t k = vv[q] & ((1u << kb) - 1u);
+        const int32_t dl = ((vv[q] >> kb) & 1u) ? -1 : 1;
+#pragma unroll
+        for (int q2 = 0; q2 < Z; ++q2) el.v[q2] = (q2 == (int)k) ? dl : 0;
+      }
+      agg = seg_combine<Z>(agg, el);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      uint32_t e = base + q;
+      if (e < N) agg = seg_combine<Z>(agg, elem_state<Z, HAS_FAT>(keys, vals, e, kb));
+    }
   }
   (void)block_exclusive<Z>(agg, warp_tot, &block_tot);
   if (threadIdx.x == 0) tile_agg[blockIdx.x] = block_tot;
@@ -622,18 +648,34 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   const uint32_t tstar = ctl->fail_t;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   // this thread's elements, loaded once: cell, head flag, op, {count, b_min}
+  // (vector loads: a warp reads 1 KB of cells and values contiguously; the
+  // scalar strided loads they replace re-requested every sector 8 times,
+  // and the gathers below evicted them from L1 and L2 in between)
   uint32_t cc[SCAN_ITEMS], tt[SCAN_ITEMS];
   unsigned long long kb[SCAN_ITEMS];
   bool hd[SCAN_ITEMS];
+  if (base + SCAN_ITEMS <= N) {
+    const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
+    const uint4* vp = reinterpret_cast<const uint4*>(vals + base);
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const uint32_t e = base + q;
-    cc[q] = e < N ? keys[e] : U32MAX;
-    tt[q] = e < N ? vals[e] >> 1 : 0u;
-    hd[q] = e < N && (e == 0 || (q ? cc[q - 1] : keys[e - 1]) != cc[q]);
+    for (int h = 0; h < SCAN_ITEMS / 4; ++h) {
+      const uint4 a = __ldg(kp + h), b = __ldg(vp + h);
+      cc[4 * h] = a.x, cc[4 * h + 1] = a.y, cc[4 * h + 2] = a.z, cc[4 * h + 3] = a.w;
+      tt[4 * h] = b.x >> 1, tt[4 * h + 1] = b.y >> 1, tt[4 * h + 2] = b.z >> 1, tt[4 * h + 3] = b.w >> 1;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      cc[q] = base + q < N ? keys[base + q] : U32MAX;
+      tt[q] = base + q < N ? vals[base + q] >> 1 : 0u;
+    }
   }
+  const uint32_t c_before = (base > 0 && base < N) ? keys[base - 1] : 0u;
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? cb[tt[q]] : 0ull;
+  for (int q = 0; q < SCAN_ITEMS; ++q)
+    hd[q] = base + q < N && (base + q == 0 || (q ? cc[q - 1] : c_before) != cc[q]);
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? __ldcg(cb + tt[q]) : 0ull;  // no L1 allocation
   SegMax agg{0u, 0u};
   SegMaxOp op;
 #pragma unroll
@@ -646,13 +688,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   SegMax run;
   BS(tmp).ExclusiveScan(agg, run, SegMax{0u, 0u}, op);
   if (threadIdx.x == 0) run = SegMax{0u, 0u};
+  uint32_t flags[2] = {0u, 0u};
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const uint32_t e = base + q;
-    if (e >= N) break;
     const uint32_t lb = hd[q] ? 0u : run.v;
-    ign[e] = (tt[q] < tstar && lb >= (uint32_t)kb[q]) ? 1u : 0u;
+    if (base + q < N && tt[q] < tstar && lb >= (uint32_t)kb[q]) flags[q >> 2] |= 1u << (8 * (q & 3));
     run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
+  }
+  static_assert(SCAN_ITEMS == 8, "one 8-B store of the flags");
+  if (base + SCAN_ITEMS <= N) {
+    *reinterpret_cast<uint2*>(ign + base) = make_uint2(flags[0], flags[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q)
+      if (base + q < N) ign[base + q] = (uint8_t)((flags[q >> 2] >> (8 * (q & 3))) & 1u);
   }
 }
 
