@@ -607,11 +607,14 @@ static uint32_t slot_cap(uint32_t n) {  // a power of two >= 1.25 n (load <= 0.8
   return (uint32_t)c;
 }
 
-// tile rule: {key count << 32 | b_min} per op, one 8-B gather for the ignore scan
+// per op, 16 B gathered once by the ignore scan: {key count, b_min, the
+// key's previous op, 0}
 __global__ void cb_pack_k(const uint2* __restrict__ meta, const uint32_t* __restrict__ bmin, uint32_t n,
-                          unsigned long long* __restrict__ cb) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-    cb[t] = ((unsigned long long)meta[t].x << 32) | bmin[t];
+                          uint4* __restrict__ cb) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint2 m = meta[t];
+    cb[t] = make_uint4(m.x, bmin[t], m.y, 0u);
+  }
 }
 
 // key order -> op order: {count of the op's key up to and including it, the
@@ -640,9 +643,9 @@ struct SegMaxOp {
 // lower bound of the cell; earlier tiles are simply not consulted)
 __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals, uint32_t N,
-                                                            uint32_t row_cells,
-                                                            const unsigned long long* __restrict__ cb,
-                                                            const Ctl* __restrict__ ctl, uint8_t* __restrict__ ign) {
+                                                            uint32_t row_cells, const uint4* __restrict__ cb,
+                                                            const Ctl* __restrict__ ctl, uint8_t* __restrict__ ign,
+                                                            uint32_t* __restrict__ kpc, uint32_t* __restrict__ dmask) {
   typedef cub::BlockScan<SegMax, SCAN_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
   const uint32_t tstar = ctl->fail_t;
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   // scalar strided loads they replace re-requested every sector 8 times,
   // and the gathers below evicted them from L1 and L2 in between)
   uint32_t cc[SCAN_ITEMS], tt[SCAN_ITEMS];
-  unsigned long long kb[SCAN_ITEMS];
+  uint4 kb[SCAN_ITEMS];
   bool hd[SCAN_ITEMS];
   if (base + SCAN_ITEMS <= N) {
     const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
@@ -675,13 +678,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   for (int q = 0; q < SCAN_ITEMS; ++q)
     hd[q] = base + q < N && (base + q == 0 || (q ? cc[q - 1] : c_before) != cc[q]);
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? __ldcg(cb + tt[q]) : 0ull;  // no L1 allocation
+  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? __ldcg(cb + tt[q]) : make_uint4(0u, 0u, 0u, 0u);
   SegMax agg{0u, 0u};
   SegMaxOp op;
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     if (base + q < N) {
-      const SegMax el{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)};
+      const SegMax el{hd[q] ? 1u : 0u, kb[q].x};
       agg = q == 0 ? el : op(agg, el);
     }
   }
@@ -692,16 +695,27 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t lb = hd[q] ? 0u : run.v;
-    if (base + q < N && tt[q] < tstar && lb >= (uint32_t)kb[q]) flags[q >> 2] |= 1u << (8 * (q & 3));
-    run = op(run, SegMax{hd[q] ? 1u : 0u, (uint32_t)(kb[q] >> 32)});
+    if (base + q < N && tt[q] < tstar && lb >= kb[q].y) {
+      flags[q >> 2] |= 1u << (8 * (q & 3));
+      // the op's dropped rows, one byte per op (D <= 8), in op order
+      const uint32_t t = tt[q], row = cc[q] / row_cells;
+      atomicOr(dmask + (t >> 2), 1u << (8 * (t & 3) + row));
+    }
+    run = op(run, SegMax{hd[q] ? 1u : 0u, kb[q].x});
   }
   static_assert(SCAN_ITEMS == 8, "one 8-B store of the flags");
   if (base + SCAN_ITEMS <= N) {
     *reinterpret_cast<uint2*>(ign + base) = make_uint2(flags[0], flags[1]);
+    uint4* kp = reinterpret_cast<uint4*>(kpc + base);
+    kp[0] = make_uint4(kb[0].z, kb[1].z, kb[2].z, kb[3].z);
+    kp[1] = make_uint4(kb[4].z, kb[5].z, kb[6].z, kb[7].z);
   } else {
 #pragma unroll
     for (int q = 0; q < SCAN_ITEMS; ++q)
-      if (base + q < N) ign[base + q] = (uint8_t)((flags[q >> 2] >> (8 * (q & 3))) & 1u);
+      if (base + q < N) {
+        ign[base + q] = (uint8_t)((flags[q >> 2] >> (8 * (q & 3))) & 1u);
+        kpc[base + q] = kb[q].z;
+      }
   }
 }
 
@@ -785,20 +799,38 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __
   BS(tmp).InclusiveScan(agg, inc, op, tot);
   if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
 }
-// rewrites each element's 32-B link record: filtered rank and predecessor for
-// kept pairs; ignored pairs get prev = IGN_MARK (never a run continuation)
+// Two passes over the filtered sequence (same scan state as filt_reduce_k):
+// filt_brk_k marks op t as a run break when one of its kept pairs follows a
+// kept op other than the key's previous op (kpc, from the ignore scan), one
+// bit per op; runs_head_ign_k decides the run heads from those bits and the
+// dropped-row bytes; filt_rec_k then writes the 32-B link record of the kept
+// pairs of run heads only (the rest of the pipeline reads no other). Every
+// (op, row) record used to be written: 400M scattered sectors at cfg 4.
 constexpr uint32_t IGN_MARK = 0xFFFFFFFEu;
+template <bool REC>
 __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals,
                                                             const uint8_t* __restrict__ ign, uint32_t N, uint32_t D,
                                                             uint32_t row_cells, const SegCnt* __restrict__ carry,
-                                                            uint4* __restrict__ links) {
+                                                            const uint32_t* __restrict__ kpc,
+                                                            uint32_t* __restrict__ bits, uint4* __restrict__ links) {
   typedef cub::BlockScan<SegCnt, SCAN_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
   SegCntOp op;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   FiltItems it;
   filt_load(keys, vals, ign, N, base, it);
+  uint32_t kp[SCAN_ITEMS];
+  if (!REC) {
+    if (base + SCAN_ITEMS <= N) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(kpc + base));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(kpc + base) + 1);
+      kp[0] = a.x, kp[1] = a.y, kp[2] = a.z, kp[3] = a.w, kp[4] = b.x, kp[5] = b.y, kp[6] = b.z, kp[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) kp[q] = base + q < N ? kpc[base + q] : NONE32;
+    }
+  }
   SegCnt agg{0u, 0u, NONE32};
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q)
@@ -811,13 +843,43 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t e = base + q;
     if (e >= N) break;
-    const uint32_t c = it.c[q], t = it.t[q], row = c / row_cells;
+    const uint32_t c = it.c[q], t = it.t[q];
     const SegCnt el = filt_elem(it, q);
     const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
-    uint4* rec = links + ((size_t)t * D + row) * 2;
-    const uint4 r0 = ((it.ign >> q) & 1u) ? make_uint4(0u, IGN_MARK, 0u, 0u) : make_uint4(before.cnt, before.last, 0u, 0u);
-    st_sector(rec, r0, make_uint4(c, e, 0u, 0u));
+    const bool kept = !((it.ign >> q) & 1u);
+    if (!REC) {
+      if (kept && before.last != kp[q]) atomicOr(bits + (t >> 5), 1u << (t & 31));
+    } else if (kept && ((__ldg(bits + (t >> 5)) >> (t & 31)) & 1u)) {
+      uint4* rec = links + ((size_t)t * D + c / row_cells) * 2;
+      st_sector(rec, make_uint4(before.cnt, before.last, 0u, 0u), make_uint4(c, e, 0u, 0u));
+    }
     run = op(run, el);
+  }
+}
+
+// run heads of the key-ordered SF1 / CU runs (the semantics of runs_head_k
+// with dropped pairs): op t continues the key's previous op p when it is
+// valid, keeps a row, drops the same rows as p, and no kept pair of t
+// follows anything but p in its cell (no break bit)
+__global__ void runs_head_ign_k(uint32_t n, const Ctl* __restrict__ ctl, const uint8_t* __restrict__ dmask,
+                                const uint32_t* __restrict__ brk, const uint2* __restrict__ kmeta, uint32_t D,
+                                uint32_t* __restrict__ headflag, uint32_t* __restrict__ headbits) {
+  const uint32_t tstar = ctl->fail_t, full = (1u << D) - 1u;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t n32 = (n + 31) & ~31u;  // whole warps, so every ballot covers one word of bits
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n32; t += stride) {
+    bool head = false;
+    if (t < n) {
+      const bool valid = t < tstar;
+      const uint32_t m = dmask[t];
+      const uint32_t p = kmeta[t].y;
+      bool cont = valid && m != full && p != NONE32 && !((__ldg(brk + (t >> 5)) >> (t & 31)) & 1u);
+      if (cont) cont = dmask[p] == m;
+      head = valid && !cont;
+      headflag[t] = head ? 1u : 0u;
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, head);
+    if ((threadIdx.x & 31) == 0) headbits[t >> 5] = hb;
   }
 }
 
@@ -948,6 +1010,7 @@ struct BuildArgs {
   uint32_t w;
   RunRec<D>* recs;
   const uint32_t* order;    // key order (see RunArgs)
+  const uint8_t* dmask;     // key order: the dropped rows of each op (link records exist for kept rows of heads only)
   Ctl* ctl;
 };
 
@@ -976,7 +1039,9 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     rec.e0 = e0;
     rec.info = L | (hasdel << 31);
     rec.bits0 = 0;
-    if (!a.delbits) {  // SF1 / CU: the rows this run's ops drop (IGN_MARK links)
+    if (a.dmask) {  // SF1 / CU: the rows this run's ops drop
+      rec.bits0 = a.dmask[t];
+    } else if (!a.delbits) {  // (SFK_NO_SF1_IGNORE: every pair is kept)
 #pragma unroll
       for (int i = 0; i < D; ++i)
         if (a.links[((size_t)t * D + i) * a.lstride].y == IGN_MARK) rec.bits0 |= 1u << i;
@@ -992,8 +1057,8 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     for (int i = 0; i < D; ++i) {
       // the (t, row) link record, one 256-bit load: {rank, prev, own count,
       // max of the other slots} {cell, sorted position, 0, 0}
-      uint4 l0, l1;
-      ld_sector(a.links + ((size_t)t * D + i) * 4, l0, l1);
+      uint4 l0 = make_uint4(0u, 0u, 0u, 0u), l1 = make_uint4(0u, 0u, 0u, 0u);
+      if (!((rec.bits0 >> i) & 1u) || !a.dmask) ld_sector(a.links + ((size_t)t * D + i) * 4, l0, l1);
       rec.cells[i] = l1.x;
       rec.rank[i] = l0.x;
       if (a.obs2) {
@@ -2428,6 +2493,8 @@ struct Layout {
   unsigned long long* htab;       //   key -> group id table (64-bit keys)
   uint32_t *ta, *tb, *headpos;     //   op ids, sorted op ids, key segment heads
   uint2* meta;                     //   per op: {key count, previous op of the same key}
+  uint32_t* dmask;                 //   per op: a byte of dropped rows (D <= 8)
+  uint32_t *rbrk, *hbits;          //   per op bits: a kept pair breaks the key's run / run head
   uint8_t* ign;                    //   dropped (op, row) flags in cell order
   void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
@@ -2529,6 +2596,9 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   {
     const bool sf1 = kind == 1 || kind == 2;  // SF1 and CU: the ignore pass
     L.meta = cv.take<uint2>(sf1 ? n : 1);
+    L.dmask = cv.take<uint32_t>(sf1 ? (uint64_t)n / 4 + 1 : 1);
+    L.rbrk = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
+    L.hbits = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
     L.k64a = cv.take<uint64_t>(sf1 ? n : 1);
     L.k64b = cv.take<uint64_t>(sf1 ? n : 1);
     L.htab = cv.take<unsigned long long>(sf1 ? slot_cap((uint32_t)std::max<int64_t>(n, 1)) : 1);
@@ -2742,7 +2812,8 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.order = has_ign ? L.tb : nullptr;
   ra.kmeta = has_ign ? L.meta : nullptr;
   ra.ctl = L.ctl;
-  { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
+  // (with dropped pairs the ignore pass has decided the run heads: runs_head_ign_k)
+  if (!has_ign) { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   { note_launch(); runs_mark_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.headflag, L.ridx, (int)n, st);
@@ -2773,6 +2844,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.w = (uint32_t)w;
   ba.recs = static_cast<RunRec<D>*>(L.recs);
   ba.order = has_ign ? L.tb : nullptr;
+  ba.dmask = has_ign ? reinterpret_cast<const uint8_t*>(L.dmask) : nullptr;
   ba.ctl = L.ctl;
   { note_launch(); runs_build_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ba); }
   const uint32_t cells = (uint32_t)(D * w);
@@ -2975,11 +3047,15 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
     { note_launch(); key_meta_k<uint64_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, L.tb, L.headpos, n, L.meta); }
   }
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
-  {  // {key count, b_min} per op, gathered by the tile scan in cell order
-    unsigned long long* cb = reinterpret_cast<unsigned long long*>(L.k64a);  // free after the key grouping
-    { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.meta, L.obs, n, cb); }
-    { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign); }
-  }
+  // {key count, b_min, previous op} per op, gathered once by the ignore scan
+  // in cell order; 16 n bytes over k64a and k64b (adjacent, dead after the
+  // key grouping)
+  uint4* cb = reinterpret_cast<uint4*>(L.k64a);
+  uint32_t* kpc = L.v_in;  // the previous op per element in cell order (v_in is dead after the slim sort)
+  cudaMemsetAsync(L.dmask, 0, ((size_t)n / 4 + 1) * 4, st);
+  cudaMemsetAsync(L.rbrk, 0, ((size_t)n / 32 + 1) * 4, st);
+  { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.meta, L.obs, n, cb); }
+  { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign, kpc, L.dmask); }
   // ftiles: [tile aggregates][their exclusive prefixes][scan temp storage]
   SegCnt* ft = static_cast<SegCnt*>(L.ftiles);
   SegCnt* fc = ft + ntiles;
@@ -2989,7 +3065,9 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   cub::DeviceScan::ExclusiveScan(nullptr, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
   e = cub::DeviceScan::ExclusiveScan(ftmp, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
   if (e != cudaSuccess) { set_error("filtered-link tiles: %s", cudaGetErrorString(e)); return (int)e; }
-  { note_launch(); filt_apply_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, reinterpret_cast<uint4*>(L.links)); }
+  { note_launch(); filt_apply_k<false><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, kpc, L.rbrk, nullptr); }
+  { note_launch(); runs_head_ign_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(n, L.ctl, reinterpret_cast<const uint8_t*>(L.dmask), L.rbrk, L.meta, D, L.headflag, L.hbits); }
+  { note_launch(); filt_apply_k<true><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, nullptr, L.hbits, reinterpret_cast<uint4*>(L.links)); }
   return check_launch("sf1_ignore");
 }
 

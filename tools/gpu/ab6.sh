@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_ab6.log 2>&1; echo rc=$? >> gpurun_out/pytest_ab6.log
+for rep in 1 2; do for v in base main; do
+  if [ $v = main ]; then lib=paper_1701_04148_b200/_lib/libsfsketch_cuda.so; else lib=paper_1701_04148_b200/_lib/$v/libsfsketch_cuda.so; fi
+  echo -n "$v "; SFK_LIB_PATH=$lib timeout 300 python tools/build_probe.py sf1 1.0 4
+  echo -n "$v "; SFK_LIB_PATH=$lib timeout 120 python tools/build_probe.py cu 1.0 2
+  echo -n "$v "; SFK_LIB_PATH=$lib timeout 120 python tools/build_probe.py sf1 1.0 1
+done; done > gpurun_out/ab6.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4_c.csv python tools/build_probe.py sf1 1.0 4 > gpurun_out/ncu_cfg4_c.log 2>&1
