@@ -899,6 +899,7 @@ struct RunArgs {
   int has_ign;             // SF1 / CU ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
   const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
   const uint2* kmeta;      // key order: {key count, the previous op of the same key (NONE32 for a key's first op)}
+  const uint32_t* hbits;   // key order: run heads as bits per op (an L2-resident copy of headflag)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
   uint32_t* isdel;         // [e]: 1 if op e is a delete (scanned into delete prefix counts)
@@ -959,7 +960,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const uint32_t t = a.order ? a.order[e] : v >> (a.kb + 1);
     const bool valid = t < tstar;
     const uint32_t op = a.order ? (valid ? 0u : 1u) : (v >> a.kb) & 1u;
-    const bool cont = valid && !a.headflag[t];
+    const bool cont = valid && !(a.hbits ? ((__ldg(a.hbits + (t >> 5)) >> (t & 31)) & 1u) : a.headflag[t]);
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
     if (a.obs) a.opdata[e] = a.obs[t];  // per-op b_min (segscan WRITE_OBS 4)
     if (a.delbits) {
@@ -1011,6 +1012,7 @@ struct BuildArgs {
   RunRec<D>* recs;
   const uint32_t* order;    // key order (see RunArgs)
   const uint8_t* dmask;     // key order: the dropped rows of each op (link records exist for kept rows of heads only)
+  const uint32_t* hbits;    // key order: run heads as bits per op
   Ctl* ctl;
 };
 
@@ -1027,7 +1029,7 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
     if (j == a.n - 1) a.ctl->n_runs = a.ridx[j] + a.headflag[j];
     const uint32_t t = a.order ? a.order[j] : j;
-    if (!a.headflag[t]) continue;
+    if (!(a.hbits ? ((__ldg(a.hbits + (t >> 5)) >> (t & 31)) & 1u) : a.headflag[t])) continue;
     const uint32_t r = a.ridx[t];
     // the head's position in the run order (row 0 or key order)
     const uint32_t e0 = a.order ? j : a.links[((size_t)t * D) * 4 + 2].y;
@@ -2811,6 +2813,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.has_ign = has_ign ? 1 : 0;
   ra.order = has_ign ? L.tb : nullptr;
   ra.kmeta = has_ign ? L.meta : nullptr;
+  ra.hbits = has_ign ? L.hbits : nullptr;
   ra.ctl = L.ctl;
   // (with dropped pairs the ignore pass has decided the run heads: runs_head_ign_k)
   if (!has_ign) { note_launch(); runs_head_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ra); }
@@ -2845,6 +2848,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ba.recs = static_cast<RunRec<D>*>(L.recs);
   ba.order = has_ign ? L.tb : nullptr;
   ba.dmask = has_ign ? reinterpret_cast<const uint8_t*>(L.dmask) : nullptr;
+  ba.hbits = has_ign ? L.hbits : nullptr;
   ba.ctl = L.ctl;
   { note_launch(); runs_build_k<D><<<grid_for(n, 256, sms * 16), 256, 0, st>>>(ba); }
   const uint32_t cells = (uint32_t)(D * w);
