@@ -619,13 +619,28 @@ __global__ void cb_pack_k(const uint2* __restrict__ meta, const uint32_t* __rest
 
 // key order -> op order: {count of the op's key up to and including it, the
 // key's previous op (NONE32 for its first)} in one 8-B store per op
+// (four positions per thread and iteration, loads first: the scattered
+// stores are partial sectors, and one position at a time left the kernel
+// latency-bound at 2 % issue)
 template <typename K>
 __global__ void key_meta_k(const K* __restrict__ ks, const uint32_t* __restrict__ tb,
                            const uint32_t* __restrict__ headpos, uint32_t n, uint2* __restrict__ meta) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t t = tb[j];
-    const uint32_t kp = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
-    meta[t] = make_uint2(j - headpos[j] + 1u, kp);
+  constexpr int U = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t j0 = blockIdx.x * blockDim.x + threadIdx.x; j0 < n; j0 += U * stride) {
+    uint32_t t[U], kp[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + u * stride;
+      if (j < n) {
+        t[u] = tb[j];
+        kp[u] = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
+        c[u] = j - headpos[j] + 1u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + u * stride < n) meta[t[u]] = make_uint2(c[u], kp[u]);
   }
 }
 
@@ -3019,9 +3034,11 @@ static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_
 }
 
 // SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
-static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st) {
+static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st,
+                           bool keys_loaded = false) {
   const int sms = sm_count();
-  if (int r = launch_load_keys(ks, n, L.k64a, st)) return r;
+  if (!keys_loaded)
+    if (int r = launch_load_keys(ks, n, L.k64a, st)) return r;
   { note_launch(); iota_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.ta, n); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e;
@@ -3096,7 +3113,14 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = run_engine<D, 2>(L, slim, slim_seeds, w, ks, n, kb, inc, st)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 1, result, nullptr, D, 0); }
   } else if (kind == 1) {  // ------------------------------------------ SF1
-    HashArgs<D> hf = make_hash<D>(ks, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
+    // record keys (FNV-1a + finalize64 over 13 B) are hashed once into k64a
+    // and read back as u64 by the hash emits and the key grouping
+    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob
+    const bool mat = ign && ks.kind == SFK_KEY_RECORD;
+    if (mat)
+      if (int r = launch_load_keys(ks, n64, L.k64a, st)) return r;
+    const KeySrc kh = mat ? KeySrc{L.k64a, SFK_KEY_U64, 8} : ks;
+    HashArgs<D> hf = make_hash<D>(kh, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
     { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
     if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
@@ -3104,12 +3128,11 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
     if (int r = bmin_from_pairs(L, n, N, D, st)) return r;
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
-    HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
+    HashArgs<D> hs = make_hash<D>(kh, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
-    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob
-    if (ign) {  // the filtered scan writes every link record itself
-      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st)) return r;
+    if (ign) {  // the filtered scan writes the run heads' link records itself
+      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st, mat)) return r;
     } else {
       ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
       if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
