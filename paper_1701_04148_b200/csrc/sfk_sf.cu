@@ -821,7 +821,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_reduce_k(const uint32_t* __
 // dropped-row bytes; filt_rec_k then writes the 32-B link record of the kept
 // pairs of run heads only (the rest of the pipeline reads no other). Every
 // (op, row) record used to be written: 400M scattered sectors at cfg 4.
-constexpr uint32_t IGN_MARK = 0xFFFFFFFEu;
 template <bool REC>
 __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals,
@@ -911,9 +910,7 @@ struct RunArgs {
   uint8_t* opflags;        // [e]: bit0 delete, bit1 continues the run, bit2 valid (t < t*)
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
   uint32_t* headflag;      // [t] (written by runs_head_k)
-  int has_ign;             // SF1 / CU ignore pass ran: dropped (op, row) pairs carry IGN_MARK links
   const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
-  const uint2* kmeta;      // key order: {key count, the previous op of the same key (NONE32 for a key's first op)}
   const uint32_t* hbits;   // key order: run heads as bits per op (an L2-resident copy of headflag)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
@@ -929,35 +926,17 @@ __global__ void __launch_bounds__(256) runs_head_k(RunArgs<D> a) {
   const uint32_t tstar = a.ctl->fail_t;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
     const bool valid = t < tstar;
-    uint32_t prev[D], mask = 0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      prev[i] = a.links[((size_t)t * D + i) * 4].y;
-      if (prev[i] == IGN_MARK) mask |= 1u << i;  // a dropped pair: not in the cell's sequence
-    }
-    // every kept row's previous op is the same op p
+    // every row's previous op is the same op p, of the same key
     uint32_t p = NONE32;
-    bool cont = valid && mask != (1u << D) - 1u;
+    bool cont = valid;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      if ((mask >> i) & 1u) continue;
-      if (prev[i] == NONE32) cont = false;
-      else if (p == NONE32) p = prev[i];
-      else if (prev[i] != p) cont = false;
+      const uint32_t prev = a.links[((size_t)t * D + i) * 4].y;
+      if (prev == NONE32) cont = false;
+      else if (p == NONE32) p = prev;
+      else if (prev != p) cont = false;
     }
-    cont = cont && p != NONE32;
-    if (cont && a.has_ign) {  // the run's ops must drop the same rows
-      uint32_t pm = 0;
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-        if (a.links[((size_t)p * D + i) * 4].y == IGN_MARK) pm |= 1u << i;
-      cont = pm == mask;
-    }
-    if (cont) {
-      // key order: p must be the key's previous op, so a run is a contiguous
-      // stretch of its key's ops; row-0 order: the same key
-      cont = a.kmeta ? a.kmeta[t].y == p : load_key(a.keys, p) == load_key(a.keys, t);
-    }
+    cont = cont && p != NONE32 && load_key(a.keys, p) == load_key(a.keys, t);
     a.headflag[t] = (valid && !cont) ? 1u : 0u;
   }
 }
@@ -1056,13 +1035,7 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     rec.e0 = e0;
     rec.info = L | (hasdel << 31);
     rec.bits0 = 0;
-    if (a.dmask) {  // SF1 / CU: the rows this run's ops drop
-      rec.bits0 = a.dmask[t];
-    } else if (!a.delbits) {  // (SFK_NO_SF1_IGNORE: every pair is kept)
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-        if (a.links[((size_t)t * D + i) * a.lstride].y == IGN_MARK) rec.bits0 |= 1u << i;
-    }
+    if (a.dmask) rec.bits0 = a.dmask[t];  // SF1 / CU: the rows this run's ops drop
     if (a.delbits && hasdel) {
       const uint32_t sh = e0 & 31u;
       uint32_t b = a.delbits[e0 >> 5] >> sh;
@@ -2825,9 +2798,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.delbits = MODE >= 2 ? L.delbits : nullptr;
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
-  ra.has_ign = has_ign ? 1 : 0;
   ra.order = has_ign ? L.tb : nullptr;
-  ra.kmeta = has_ign ? L.meta : nullptr;
   ra.hbits = has_ign ? L.hbits : nullptr;
   ra.ctl = L.ctl;
   // (with dropped pairs the ignore pass has decided the run heads: runs_head_ign_k)
