@@ -3008,13 +3008,25 @@ static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_
 static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st,
                            bool keys_loaded = false) {
   const int sms = sm_count();
-  if (!keys_loaded)
+  static const bool key_sort = getenv("SFK_KEY_GROUP") && !strcmp(getenv("SFK_KEY_GROUP"), "sort");  // A/B knob
+  // u32 keys sort as they are (4 passes of 4-B keys); wider keys are materialised
+  const bool direct32 = ks.kind == SFK_KEY_U32 && !key_sort;
+  if (!keys_loaded && !direct32)
     if (int r = launch_load_keys(ks, n, L.k64a, st)) return r;
   { note_launch(); iota_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.ta, n); }
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e;
-  static const bool key_sort = getenv("SFK_KEY_GROUP") && !strcmp(getenv("SFK_KEY_GROUP"), "sort");  // A/B knob
-  if (ks.kind != SFK_KEY_U32 && !key_sort) {
+  if (direct32) {
+    uint32_t* sk = reinterpret_cast<uint32_t*>(L.k64b);  // the sorted keys
+    e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, static_cast<const uint32_t*>(ks.p), sk, L.ta, L.tb, (int)n,
+                                        0, 32, st);
+    if (e != cudaSuccess) { set_error("key sort: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_heads_k<uint32_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(sk, n, L.headpos); }
+    bytes = L.cub_tmp_bytes;
+    e = cub::DeviceScan::InclusiveScan(L.cub_tmp, bytes, L.headpos, L.headpos, cub::Max(), (int)n, st);
+    if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
+    { note_launch(); key_meta_k<uint32_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(sk, L.tb, L.headpos, n, L.meta); }
+  } else if (ks.kind != SFK_KEY_U32 && !key_sort) {
     // 64-bit keys: group by table slot (4-B ids, see key_slot_k)
     const uint32_t cap = slot_cap(n);
     uint32_t* sid = reinterpret_cast<uint32_t*>(L.k64b);  // [0, n): ids in op order, [n, 2n): sorted
