@@ -3054,6 +3054,11 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   // {key count, b_min, previous op} per op, gathered once by the ignore scan
   // in cell order; 16 n bytes over k64a and k64b (adjacent, dead after the
   // key grouping)
+  if (reinterpret_cast<char*>(L.k64b) < reinterpret_cast<char*>(L.k64a) ||
+      reinterpret_cast<char*>(L.k64a) + 16ull * n > reinterpret_cast<char*>(L.k64b) + 8ull * n) {
+    set_error("workspace layout: k64a and k64b must be adjacent");  // (carve() keeps them so)
+    return 1;
+  }
   uint4* cb = reinterpret_cast<uint4*>(L.k64a);
   uint32_t* kpc = L.v_in;  // the previous op per element in cell order (v_in is dead after the slim sort)
   cudaMemsetAsync(L.dmask, 0, ((size_t)n / 4 + 1) * 4, st);
