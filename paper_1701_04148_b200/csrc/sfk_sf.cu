@@ -2485,6 +2485,9 @@ struct Layout {
   uint2* meta;                     //   per op: {key count, previous op of the same key}
   uint32_t* dmask;                 //   per op: a byte of dropped rows (D <= 8)
   uint32_t *rbrk, *hbits;          //   per op bits: a kept pair breaks the key's run / run head
+  uint32_t* owner;                 // SF1 shared-cell fat phase: first claimant per fat cell
+  uint8_t* shared;                 //   fat cells claimed by two or more keys
+  uint32_t *ncnt, *noff;           //   per op: rows on shared cells, their exclusive prefix sums
   uint8_t* ign;                    //   dropped (op, row) flags in cell order
   void* ftiles;                    //   filtered-link scan tile carries
   void* recs;
@@ -2589,6 +2592,11 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
     L.dmask = cv.take<uint32_t>(sf1 ? (uint64_t)n / 4 + 1 : 1);
     L.rbrk = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
     L.hbits = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
+    const bool f1 = kind == 1;
+    L.owner = cv.take<uint32_t>(f1 ? (uint64_t)d * wp : 1);
+    L.shared = cv.take<uint8_t>(f1 ? (uint64_t)d * wp : 1);
+    L.ncnt = cv.take<uint32_t>(f1 ? (uint64_t)n + 1 : 1);
+    L.noff = cv.take<uint32_t>(f1 ? (uint64_t)n + 1 : 1);
     L.k64a = cv.take<uint64_t>(sf1 ? n : 1);
     L.k64b = cv.take<uint64_t>(sf1 ? n : 1);
     L.htab = cv.take<unsigned long long>(sf1 ? slot_cap((uint32_t)std::max<int64_t>(n, 1)) : 1);
@@ -2960,6 +2968,116 @@ __global__ void fold_scatter_k(const uint32_t* __restrict__ grp, uint32_t* __res
 }
 
 
+// ---------------------------------------------------------------- SF1 fat phase over shared cells
+// An SF1 op's post-op count on a fat cell that no other key of the batch
+// touches is its fat value before the batch plus the key's count so far, so
+// only the pairs on cells that two or more keys share (56 % at cfg 4) need
+// the cell sort and the segmented scan. fat_owner_k lets every key's head
+// claim its d cells (a second key's claim marks the cell shared),
+// fat_count_k / fat_emit_k write the shared pairs compacted in op order (a
+// stable cell sort keeps each cell's ops in stream order) and each op's
+// minimum over its exclusive rows into b_min, and fat_excl_final_k writes
+// the exclusive cells' final values. The batch must be insert-only and
+// free of saturation on exclusive cells (checked on the device, read once by
+// the host; otherwise the batch takes the full sort).
+template <int D>
+struct FatArgs {
+  KeySrc keys;
+  const uint8_t* ops;
+  uint32_t n;
+  Seeds<D> seeds;
+  Mod wm;
+  uint32_t wp;
+  const uint32_t* tb;       // key-sorted op list
+  const uint32_t* headpos;  // [j]: position of j's key segment head
+  const uint2* meta;        // [t]: {key count, previous op}
+  uint32_t* owner;          // [cell]: the first key head that claimed it
+  uint8_t* shared;          // [cell]: claimed by two or more keys
+  const uint32_t* fat_init;
+  uint32_t* fat;
+  uint32_t* ncnt;           // [t]: the op's rows on shared cells (then their exclusive prefix sum)
+  uint32_t* key_out;
+  uint32_t* val_out;
+  uint32_t* obs;            // [t]: min over the op's exclusive rows of its post-op count
+  Ctl* ctl;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) fat_owner_k(FatArgs<D> a) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
+    if (a.headpos[j] != j) continue;
+    const uint64_t key = load_key(a.keys, a.tb[j]);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint32_t f = (uint32_t)i * a.wp + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+      const uint32_t prev = atomicCAS(a.owner + f, NONE32, j);
+      if (prev != NONE32 && prev != j) a.shared[f] = 1;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) fat_count_k(FatArgs<D> a) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
+    const uint64_t key = load_key(a.keys, t);
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) c += a.shared[(uint32_t)i * a.wp + (uint32_t)bucket(key, a.seeds.s[i], a.wm)];
+    a.ncnt[t] = c;
+  }
+}
+
+// (ncnt holds the exclusive prefix sums here: op t's first output slot)
+template <int D>
+__global__ void __launch_bounds__(256) fat_emit_k(FatArgs<D> a) {
+  uint32_t local_fail = NONE32, local_bad = NONE32;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.n; t += gridDim.x * blockDim.x) {
+    const uint64_t key = load_key(a.keys, t);
+    const uint32_t code = a.ops[t];
+    const uint32_t op = code != 0;
+    if (code > 1 && local_bad == NONE32) local_bad = t;
+    if (op && local_fail == NONE32) local_fail = t;  // SF1: a delete is the failing op
+    const uint64_t cnt = a.meta[t].x;
+    uint32_t o = a.ncnt[t];
+    uint64_t ex = ~0ull;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint32_t f = (uint32_t)i * a.wp + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+      if (a.shared[f]) {
+        a.key_out[o] = f;
+        a.val_out[o] = (t << 1) | op;
+        ++o;
+      } else {
+        const uint64_t post = (uint64_t)__ldg(a.fat_init + f) + cnt;
+        if (post - 1 >= (uint64_t)U32MAX) local_fail = min(local_fail, t);  // a saturated counter before the op
+        ex = min(ex, post);
+      }
+    }
+    a.obs[t] = (uint32_t)min(ex, (uint64_t)U32MAX);
+  }
+  if (local_fail != NONE32) atomicMin(&a.ctl->fail_t, local_fail);
+  if (local_bad != NONE32) {
+    atomicMin(&a.ctl->bad_op, local_bad);
+    atomicMin(&a.ctl->fail_t, 0u);
+  }
+}
+
+// exclusive cells: the final value is the value before the batch plus the
+// key's op count (the last op of a key segment carries it)
+template <int D>
+__global__ void __launch_bounds__(256) fat_excl_final_k(FatArgs<D> a) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
+    if (j + 1 < a.n && a.headpos[j + 1] == a.headpos[j]) continue;  // not the segment's last op
+    const uint32_t tot = j - a.headpos[j] + 1u;
+    const uint64_t key = load_key(a.keys, a.tb[j]);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const uint32_t f = (uint32_t)i * a.wp + (uint32_t)bucket(key, a.seeds.s[i], a.wm);
+      if (!a.shared[f]) a.fat[f] = a.fat_init[f] + tot;
+    }
+  }
+}
+
 int launch_load_keys(KeySrc ks, int64_t n, uint64_t* out, cudaStream_t st);  // sfk_query.cu
 
 // per-op b_min from the fat scan's (t, candidate) pairs in k_in / v_in (see
@@ -2978,15 +3096,17 @@ __global__ void __launch_bounds__(256) bmin_l2_k(const uint32_t* __restrict__ tk
     if (e < N) atomicMin(obs + __ldg(tkey + e), __ldg(tval + e));
   }
 }
-static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_t st) {
+// compacted: the pairs cover only some of each op's rows (the shared-cell
+// fat phase), and obs already holds the other rows' minimum
+static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_t st, bool compacted = false) {
   const int tbits = bits_for((uint64_t)n);
   const uint32_t* tk = L.k_in;
   const uint32_t* tv = L.v_in;
-  const bool l2 = tbits - BMIN_BITS > 8;
+  const bool l2 = compacted || tbits - BMIN_BITS > 8;
   if (tbits > BMIN_BITS) {
     size_t bytes = L.cub_tmp_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)N,
-                                                    l2 ? tbits - 8 : BMIN_BITS, tbits, st);
+                                                    l2 ? std::max(tbits - 8, 0) : BMIN_BITS, tbits, st);
     if (e != cudaSuccess) {
       set_error("b_min sort: %s", cudaGetErrorString(e));
       return (int)e;
@@ -2995,7 +3115,7 @@ static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_
     tv = L.v_out;
   }
   if (l2) {
-    cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
+    if (!compacted) cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
     { note_launch(); bmin_l2_k<<<(N + 2047) / 2048, 256, 0, st>>>(tk, tv, N, L.obs); }
     return check_launch("bmin_l2");
   }
@@ -3004,9 +3124,9 @@ static int bmin_from_pairs(Layout& L, uint32_t n, uint32_t N, int d, cudaStream_
   return check_launch("bmin_bucket");
 }
 
-// SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
-static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st,
-                           bool keys_loaded = false) {
+// SF1 / CU key grouping: the key-sorted op list (tb), segment heads
+// (headpos) and, per op, {key count, previous op of the key} (meta)
+static int key_group(Layout& L, KeySrc ks, uint32_t n, cudaStream_t st, bool keys_loaded) {
   const int sms = sm_count();
   static const bool key_sort = getenv("SFK_KEY_GROUP") && !strcmp(getenv("SFK_KEY_GROUP"), "sort");  // A/B knob
   // u32 keys sort as they are (4 passes of 4-B keys); wider keys are materialised
@@ -3050,6 +3170,16 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
     if (e != cudaSuccess) { set_error("key heads: %s", cudaGetErrorString(e)); return (int)e; }
     { note_launch(); key_meta_k<uint64_t><<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.k64b, L.tb, L.headpos, n, L.meta); }
   }
+  return 0;
+}
+
+// SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
+static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st,
+                           bool keys_loaded = false, bool grouped = false) {
+  const int sms = sm_count();
+  cudaError_t e;
+  if (!grouped)
+    if (int r = key_group(L, ks, n, st, keys_loaded)) return r;
   const uint32_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   // {key count, b_min, previous op} per op, gathered once by the ignore scan
   // in cell order; 16 n bytes over k64a and k64b (adjacent, dead after the
@@ -3109,18 +3239,87 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
       if (int r = launch_load_keys(ks, n64, L.k64a, st)) return r;
     const KeySrc kh = mat ? KeySrc{L.k64a, SFK_KEY_U64, 8} : ks;
     HashArgs<D> hf = make_hash<D>(kh, ops, n64, fat_seeds, nullptr, (uint64_t)wp, 1, 0, L, 1);
-    { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
-    if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
     cudaMemcpyAsync(L.fat_snap, fat, (size_t)D * wp * 4, cudaMemcpyDeviceToDevice, st);
-    ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl, L.k_in, L.v_in};
-    if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
-    if (int r = bmin_from_pairs(L, n, N, D, st)) return r;
+    // large batches: the fat sort and scan only over pairs on shared cells
+    // (fat_owner_k ...); one host read of {pairs, t*}. Not while the stream
+    // is being captured into a graph (no host read there), and not for
+    // batches that fail (deletes, saturation): those take the full sort.
+    static const bool fat_sort = getenv("SFK_SF1_FAT") && !strcmp(getenv("SFK_SF1_FAT"), "sort");  // A/B knob
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    const char* fmin = getenv("SFK_SF1_FAT_MIN");  // tests: smallest batch for this path (default 2^20 ops)
+    const uint32_t excl_min = fmin ? (uint32_t)strtoul(fmin, nullptr, 10) : (1u << 20);
+    bool grouped = false, excl = ign && !fat_sort && n >= excl_min && cap == cudaStreamCaptureStatusNone;
+    if (excl) {
+      if (int r = key_group(L, kh, n, st, mat)) return r;
+      grouped = true;
+      FatArgs<D> fa;
+      fa.keys = kh;
+      fa.ops = ops;
+      fa.n = n;
+      for (int i = 0; i < D; ++i) fa.seeds.s[i] = fat_seeds[i];
+      fa.wm = make_mod((uint64_t)wp);
+      fa.wp = (uint32_t)wp;
+      fa.tb = L.tb;
+      fa.headpos = L.headpos;
+      fa.meta = L.meta;
+      fa.owner = L.owner;
+      fa.shared = L.shared;
+      fa.fat_init = L.fat_snap;
+      fa.fat = fat;
+      fa.ncnt = L.ncnt;
+      fa.key_out = L.k_in;
+      fa.val_out = L.v_in;
+      fa.obs = L.obs;
+      fa.ctl = L.ctl;
+      cudaMemsetAsync(L.owner, 0xFF, (size_t)D * wp * 4, st);
+      cudaMemsetAsync(L.shared, 0, (size_t)D * wp, st);
+      cudaMemsetAsync(L.ncnt + n, 0, 4, st);
+      { note_launch(); fat_owner_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(fa); }
+      { note_launch(); fat_count_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(fa); }
+      size_t bytes = L.cub_tmp_bytes;
+      if (cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.ncnt, L.noff, (int)n + 1, st) != cudaSuccess) {
+        set_error("shared-pair offsets: scan failed");
+        return 1;
+      }
+      fa.ncnt = L.noff;
+      { note_launch(); fat_emit_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(fa); }
+      uint32_t hv[2];
+      cudaMemcpyAsync(hv, L.noff + n, 4, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hv + 1, &L.ctl->fail_t, 4, cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("shared-pair count");
+      if (hv[1] != NONE32) {  // a delete, a bad op code or a saturated exclusive cell: the full sort
+        excl = false;
+        { note_launch(); ctl_init_k<<<1, 1, 0, st>>>(L.ctl); }
+      } else {
+        const uint32_t Ns = hv[0];
+        { note_launch(); fat_excl_final_k<D><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(fa); }
+        if (Ns) {
+          bytes = L.cub_tmp_bytes;
+          if (cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)Ns, 0,
+                                              std::max(bits_for((uint64_t)D * wp), 1), st) != cudaSuccess) {
+            set_error("shared-pair sort failed");
+            return 1;
+          }
+          ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl, L.k_in, L.v_in};
+          if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, Ns, 0, L.tiles, sf, st)) return r;
+          if (int r = bmin_from_pairs(L, n, Ns, D, st, true)) return r;
+        }
+      }
+    }
+    if (!excl) {
+      { note_launch(); hash_emit_k<D, 1><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hf); }
+      if (int r = sort_pairs(L, N, D, (uint64_t)wp, st)) return r;
+      ScanOut sf{L.fat_snap, fat, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)wp, L.ctl, L.k_in, L.v_in};
+      if (int r = run_scan_z<true, 6, false>(1, L.k_out, L.v_out, N, 0, L.tiles, sf, st)) return r;
+      if (int r = bmin_from_pairs(L, n, N, D, st)) return r;
+    }
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(kh, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     if (ign) {  // the filtered scan writes the run heads' link records itself
-      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st, mat)) return r;
+      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st, mat, grouped)) return r;
     } else {
       ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
       if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;

@@ -67,3 +67,49 @@ def test_sf1_record_keys_midsize(oracle, seed):
     o = oracle.OracleSketch("sf1", 4, 1280, 1, 16384 + seed, seed)
     assert o.apply_ops(ops, keys)[0] == 0
     assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
+
+
+@pytest.fixture
+def shared_cell_fat_path(monkeypatch):
+    """Route every SF1 batch through the shared-cell fat phase (normally
+    batches of >= 2^20 ops only; DESIGN.md §8 item 3)."""
+    monkeypatch.setenv("SFK_SF1_FAT_MIN", "1")
+    yield
+
+
+@pytest.mark.usefixtures("shared_cell_fat_path")
+@pytest.mark.parametrize("seed", range(40))
+def test_sf1_shared_cell_fat_phase(oracle, seed):
+    """Random shapes (tiny fat widths: most cells shared; wide ones: most
+    exclusive), warm sketches, saturation presets on the fat and mid-batch
+    deletes (both fall back to the full sort), several batches."""
+    rng = np.random.default_rng(900 + seed)
+    d = int(rng.integers(2, 9))
+    w = int(rng.choice([16, 100, 1024]))
+    wp = int(rng.choice([w, 4 * w + 1, 64 * w + 7]))
+    v, n = int(rng.integers(5, 5000)), int(rng.integers(100, 60_000))
+    keys = _stream(rng, n, v, np.array([EMPTY], dtype=np.uint64))
+    ops = np.zeros(n, np.uint8)
+    if rng.random() < 0.25:
+        ops[int(rng.integers(0, n))] = 1
+    o = oracle.OracleSketch("sf1", d, w, 1, wp, seed)
+    sk = make_sketch("sf1", d, w, 1, wp, seed)
+    r = rng.random()
+    if r < 0.2:  # near saturation
+        o.fat[...] = np.uint32(0xFFFFFFFF - int(rng.integers(0, 60)))
+        sk.fat.counters.copy_(torch.from_numpy(o.fat.copy()))
+    elif r < 0.5:  # warm: fat and slim from an earlier batch
+        pre = _stream(rng, 5000, v, np.array([], dtype=np.uint64))
+        o.apply_ops(np.zeros(pre.size, np.uint8), pre)
+        sk.apply_ops(np.zeros(pre.size, np.uint8), pre)
+    batches = int(rng.integers(1, 3))
+    bounds = np.linspace(0, n, batches + 1).astype(int)
+    want = (0, -1)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        st, oi, _ = o.apply_ops(ops[a:b], keys[a:b])
+        if st:
+            want = (st, a + oi)
+            break
+    got = apply_batches(sk, ops, keys, batches=batches)
+    assert got == want
+    assert_state_equal(sk, o.slim, o.inc, o.seen, o.fat)
