@@ -163,6 +163,7 @@ struct HashArgs {
   uint32_t* key_out;
   uint32_t* val_out;
   int unsupported_deletes;  // SF1 / CU: a delete is the failing op
+  const uint2* pos;         // SF1 / CU slim pairs: name op t by its key-order position (pos[t].y)
   Ctl* ctl;
 };
 
@@ -177,7 +178,8 @@ __global__ void __launch_bounds__(256) hash_emit_k(HashArgs<D> a) {
     if (a.unsupported_deletes && op != 0 && local_fail == NONE32) local_fail = (uint32_t)t;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      uint32_t cell, v = ((uint32_t)t << (a.kb + 1)) | (op << a.kb);
+      const uint32_t name = (KIND == 2 && a.pos) ? a.pos[t].y : (uint32_t)t;
+      uint32_t cell, v = (name << (a.kb + 1)) | (op << a.kb);
       if (KIND == 3) {
         const uint32_t g = (uint32_t)bucket(key, a.cell_seeds.s[i], a.cm);
         cell = (uint32_t)i * a.fold_w + g % a.fold_w;
@@ -607,18 +609,22 @@ static uint32_t slot_cap(uint32_t n) {  // a power of two >= 1.25 n (load <= 0.8
   return (uint32_t)c;
 }
 
-// per op, 16 B gathered once by the ignore scan: {key count, b_min, the
-// key's previous op, 0}
-__global__ void cb_pack_k(const uint2* __restrict__ meta, const uint32_t* __restrict__ bmin, uint32_t n,
-                          uint4* __restrict__ cb) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const uint2 m = meta[t];
-    cb[t] = make_uint4(m.x, bmin[t], m.y, 0u);
+// per op in key order, 16 B gathered once by the ignore scan: {key count,
+// b_min, the key's previous op (j - 1, or NONE32), the op t}; b_min is laid
+// out by t (SF1: the fat phase) or already by j (CU: the upper-bound scan)
+__global__ void cb_pack_k(const uint32_t* __restrict__ tb, const uint32_t* __restrict__ headpos,
+                          const uint32_t* __restrict__ bmin, int bmin_by_j, uint32_t n, uint4* __restrict__ cb) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t t = tb[j], h = headpos[j];
+    cb[j] = make_uint4(j - h + 1u, bmin[bmin_by_j ? j : t], h == j ? NONE32 : j - 1u, t);
   }
 }
 
 // key order -> op order: {count of the op's key up to and including it, the
-// key's previous op (NONE32 for its first)} in one 8-B store per op
+// op's position j in the key-sorted list} in one 8-B store per op. The
+// dropped-pair pipeline names ops by j: a key's ops are consecutive there,
+// so its previous op is j - 1 and per-op data laid out by j is read with
+// locality wherever a cell's sequence follows one key.
 // (four positions per thread and iteration, loads first: the scattered
 // stores are partial sectors, and one position at a time left the kernel
 // latency-bound at 2 % issue)
@@ -628,19 +634,18 @@ __global__ void key_meta_k(const K* __restrict__ ks, const uint32_t* __restrict_
   constexpr int U = 4;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t j0 = blockIdx.x * blockDim.x + threadIdx.x; j0 < n; j0 += U * stride) {
-    uint32_t t[U], kp[U], c[U];
+    uint32_t t[U], c[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t j = j0 + u * stride;
       if (j < n) {
         t[u] = tb[j];
-        kp[u] = (j > 0 && ks[j - 1] == ks[j]) ? tb[j - 1] : NONE32;
         c[u] = j - headpos[j] + 1u;
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j0 + u * stride < n) meta[t[u]] = make_uint2(c[u], kp[u]);
+      if (j0 + u * stride < n) meta[t[u]] = make_uint2(c[u], j0 + u * stride);
   }
 }
 
@@ -665,7 +670,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   __shared__ typename BS::TempStorage tmp;
   const uint32_t tstar = ctl->fail_t;
   const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
-  // this thread's elements, loaded once: cell, head flag, op, {count, b_min}
+  // this thread's elements, loaded once: cell, head flag, the op's key-order
+  // position j, and {count, b_min, previous op (j space), t} gathered by j
   // (vector loads: a warp reads 1 KB of cells and values contiguously; the
   // scalar strided loads they replace re-requested every sector 8 times,
   // and the gathers below evicted them from L1 and L2 in between)
@@ -693,7 +699,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
   for (int q = 0; q < SCAN_ITEMS; ++q)
     hd[q] = base + q < N && (base + q == 0 || (q ? cc[q - 1] : c_before) != cc[q]);
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? __ldcg(cb + tt[q]) : make_uint4(0u, 0u, 0u, 0u);
+  for (int q = 0; q < SCAN_ITEMS; ++q) kb[q] = base + q < N ? __ldg(cb + tt[q]) : make_uint4(0u, 0u, 0u, 0u);
   SegMax agg{0u, 0u};
   SegMaxOp op;
 #pragma unroll
@@ -710,11 +716,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) sf1_ignore_k(const uint32_t* __r
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t lb = hd[q] ? 0u : run.v;
-    if (base + q < N && tt[q] < tstar && lb >= kb[q].y) {
+    if (base + q < N && kb[q].w < tstar && lb >= kb[q].y) {
       flags[q >> 2] |= 1u << (8 * (q & 3));
-      // the op's dropped rows, one byte per op (D <= 8), in op order
-      const uint32_t t = tt[q], row = cc[q] / row_cells;
-      atomicOr(dmask + (t >> 2), 1u << (8 * (t & 3) + row));
+      // the op's dropped rows, one byte per op (D <= 8), by key-order position
+      const uint32_t j = tt[q], row = cc[q] / row_cells;
+      atomicOr(dmask + (j >> 2), 1u << (8 * (j & 3) + row));
     }
     run = op(run, SegMax{hd[q] ? 1u : 0u, kb[q].x});
   }
@@ -827,6 +833,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
                                                             const uint8_t* __restrict__ ign, uint32_t N, uint32_t D,
                                                             uint32_t row_cells, const SegCnt* __restrict__ carry,
                                                             const uint32_t* __restrict__ kpc,
+                                                            const uint32_t* __restrict__ tb,
                                                             uint32_t* __restrict__ bits, uint4* __restrict__ links) {
   typedef cub::BlockScan<SegCnt, SCAN_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
@@ -857,24 +864,28 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     const uint32_t e = base + q;
     if (e >= N) break;
-    const uint32_t c = it.c[q], t = it.t[q];
+    const uint32_t c = it.c[q], j = it.t[q];  // ops named by key-order position j (see key_meta_k)
     const SegCnt el = filt_elem(it, q);
     const SegCnt before = el.flag ? SegCnt{1u, 0u, NONE32} : run;
     const bool kept = !((it.ign >> q) & 1u);
     if (!REC) {
-      if (kept && before.last != kp[q]) atomicOr(bits + (t >> 5), 1u << (t & 31));
-    } else if (kept && ((__ldg(bits + (t >> 5)) >> (t & 31)) & 1u)) {
-      uint4* rec = links + ((size_t)t * D + c / row_cells) * 2;
-      st_sector(rec, make_uint4(before.cnt, before.last, 0u, 0u), make_uint4(c, e, 0u, 0u));
+      if (kept && before.last != kp[q]) atomicOr(bits + (j >> 5), 1u << (j & 31));
+    } else if (kept) {
+      const uint32_t t = __ldg(tb + j);
+      if ((__ldg(bits + (t >> 5)) >> (t & 31)) & 1u) {
+        uint4* rec = links + ((size_t)t * D + c / row_cells) * 2;
+        st_sector(rec, make_uint4(before.cnt, before.last, 0u, 0u), make_uint4(c, e, 0u, 0u));
+      }
     }
     run = op(run, el);
   }
 }
 
 // run heads of the key-ordered SF1 / CU runs (the semantics of runs_head_k
-// with dropped pairs): op t continues the key's previous op p when it is
-// valid, keeps a row, drops the same rows as p, and no kept pair of t
-// follows anything but p in its cell (no break bit)
+// with dropped pairs): op t (key-order position j) continues the key's
+// previous op j - 1 when it is valid, keeps a row, drops the same rows as
+// j - 1, and no kept pair of t follows anything but j - 1 in its cell (no
+// break bit at j). Heads are written by t: run ids follow stream order.
 __global__ void runs_head_ign_k(uint32_t n, const Ctl* __restrict__ ctl, const uint8_t* __restrict__ dmask,
                                 const uint32_t* __restrict__ brk, const uint2* __restrict__ kmeta, uint32_t D,
                                 uint32_t* __restrict__ headflag, uint32_t* __restrict__ headbits) {
@@ -885,10 +896,11 @@ __global__ void runs_head_ign_k(uint32_t n, const Ctl* __restrict__ ctl, const u
     bool head = false;
     if (t < n) {
       const bool valid = t < tstar;
-      const uint32_t m = dmask[t];
-      const uint32_t p = kmeta[t].y;
-      bool cont = valid && m != full && p != NONE32 && !((__ldg(brk + (t >> 5)) >> (t & 31)) & 1u);
-      if (cont) cont = dmask[p] == m;
+      const uint2 km = kmeta[t];  // {key count, j}: a count above 1 means j - 1 is the key's previous op
+      const uint32_t j = km.y;
+      const uint32_t m = dmask[j];
+      bool cont = valid && m != full && km.x > 1u && !((__ldg(brk + (j >> 5)) >> (j & 31)) & 1u);
+      if (cont) cont = dmask[j - 1] == m;
       head = valid && !cont;
       headflag[t] = head ? 1u : 0u;
     }
@@ -911,6 +923,7 @@ struct RunArgs {
   uint32_t* opdata;        // SF1: b_min per op, row-0 order
   uint32_t* headflag;      // [t] (written by runs_head_k)
   const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
+  int obs_by_pos;          // obs is laid out by key-order position (CU's upper bounds), not by op
   const uint32_t* hbits;   // key order: run heads as bits per op (an L2-resident copy of headflag)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
@@ -956,7 +969,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const uint32_t op = a.order ? (valid ? 0u : 1u) : (v >> a.kb) & 1u;
     const bool cont = valid && !(a.hbits ? ((__ldg(a.hbits + (t >> 5)) >> (t & 31)) & 1u) : a.headflag[t]);
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
-    if (a.obs) a.opdata[e] = a.obs[t];  // per-op b_min (segscan WRITE_OBS 4)
+    if (a.obs) a.opdata[e] = a.obs[a.obs_by_pos ? e : t];  // per-op b_min / cap
     if (a.delbits) {
       // e advances in warp-aligned strides, so the ballot covers one word
       const unsigned bits = __ballot_sync(__activemask(), op != 0);
@@ -1035,7 +1048,7 @@ __global__ void __launch_bounds__(256) runs_build_k(BuildArgs<D> a) {
     rec.e0 = e0;
     rec.info = L | (hasdel << 31);
     rec.bits0 = 0;
-    if (a.dmask) rec.bits0 = a.dmask[t];  // SF1 / CU: the rows this run's ops drop
+    if (a.dmask) rec.bits0 = a.dmask[j];  // SF1 / CU: the rows this run's ops drop (by key-order position)
     if (a.delbits && hasdel) {
       const uint32_t sh = e0 & 31u;
       uint32_t b = a.delbits[e0 >> 5] >> sh;
@@ -2756,6 +2769,7 @@ static HashArgs<D> make_hash(KeySrc ks, const uint8_t* ops, int64_t n, const uin
   h.key_out = L.k_in;
   h.val_out = L.v_in;
   h.unsupported_deletes = unsupported_deletes;
+  h.pos = nullptr;
   h.ctl = L.ctl;
   return h;
 }
@@ -2807,6 +2821,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.bnd = L.bnd;
   ra.isdel = L.isdel;
   ra.order = has_ign ? L.tb : nullptr;
+  ra.obs_by_pos = 0;
   ra.hbits = has_ign ? L.hbits : nullptr;
   ra.ctl = L.ctl;
   // (with dropped pairs the ignore pass has decided the run heads: runs_head_ign_k)
@@ -3175,7 +3190,7 @@ static int key_group(Layout& L, KeySrc ks, uint32_t n, cudaStream_t st, bool key
 
 // SF1: per-op key counts (sort by key), dropped (op, row) flags, filtered links
 static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_t w, uint32_t D, cudaStream_t st,
-                           bool keys_loaded = false, bool grouped = false) {
+                           bool keys_loaded = false, bool grouped = false, bool bmin_by_pos = false) {
   const int sms = sm_count();
   cudaError_t e;
   if (!grouped)
@@ -3193,7 +3208,7 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   uint32_t* kpc = L.v_in;  // the previous op per element in cell order (v_in is dead after the slim sort)
   cudaMemsetAsync(L.dmask, 0, ((size_t)n / 4 + 1) * 4, st);
   cudaMemsetAsync(L.rbrk, 0, ((size_t)n / 32 + 1) * 4, st);
-  { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.meta, L.obs, n, cb); }
+  { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.tb, L.headpos, L.obs, bmin_by_pos ? 1 : 0, n, cb); }
   { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign, kpc, L.dmask); }
   // ftiles: [tile aggregates][their exclusive prefixes][scan temp storage]
   SegCnt* ft = static_cast<SegCnt*>(L.ftiles);
@@ -3204,9 +3219,9 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   cub::DeviceScan::ExclusiveScan(nullptr, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
   e = cub::DeviceScan::ExclusiveScan(ftmp, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
   if (e != cudaSuccess) { set_error("filtered-link tiles: %s", cudaGetErrorString(e)); return (int)e; }
-  { note_launch(); filt_apply_k<false><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, kpc, L.rbrk, nullptr); }
+  { note_launch(); filt_apply_k<false><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, kpc, L.tb, L.rbrk, nullptr); }
   { note_launch(); runs_head_ign_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(n, L.ctl, reinterpret_cast<const uint8_t*>(L.dmask), L.rbrk, L.meta, D, L.headflag, L.hbits); }
-  { note_launch(); filt_apply_k<true><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, nullptr, L.hbits, reinterpret_cast<uint4*>(L.links)); }
+  { note_launch(); filt_apply_k<true><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, nullptr, L.tb, L.hbits, reinterpret_cast<uint4*>(L.links)); }
   return check_launch("sf1_ignore");
 }
 
@@ -3316,6 +3331,12 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     }
     { note_launch(); fat_undo_k<D, 1><<<grid_for(n64, 256, sms * 8), 256, 0, st>>>(hf, fat, 1u); }
     HashArgs<D> hs = make_hash<D>(kh, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 0);
+    if (ign) {  // slim pairs name their ops by key-order position (key_meta_k)
+      if (!grouped)
+        if (int r = key_group(L, kh, n, st, mat)) return r;
+      grouped = true;
+      hs.pos = L.meta;
+    }
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
     if (ign) {  // the filtered scan writes the run heads' link records itself
@@ -3409,9 +3430,13 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, opk, 0, result, nullptr, D, 0); }
   } else if (kind == 2) {  // ------------------------------------------ CU
     HashArgs<D> hs = make_hash<D>(ks, ops, n64, slim_seeds, nullptr, (uint64_t)w, 1, 0, L, 1);
+    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob (shared with SF1)
+    if (ign) {  // slim pairs name their ops by key-order position (key_meta_k)
+      if (int r = key_group(L, ks, n, st, false)) return r;
+      hs.pos = L.meta;
+    }
     { note_launch(); hash_emit_k<D, 2><<<grid_for(n64, 256, sms * 16), 256, 0, st>>>(hs); }
     if (int r = sort_pairs(L, N, D, (uint64_t)w, st)) return r;
-    const bool ign = D > 1 && !getenv("SFK_NO_SF1_IGNORE");  // diagnostics knob (shared with SF1)
     if (!ign) {
       ScanOut ss{nullptr, nullptr, nullptr, nullptr, L.links, n, (uint32_t)D, (uint32_t)w, L.ctl};
       if (int r = run_scan_z<false, 0, true>(1, L.k_out, L.v_out, N, 0, L.tiles, ss, st)) return r;
@@ -3422,7 +3447,7 @@ static int sf_parallel_d(int kind, uint32_t* slim, uint32_t* fat, uint32_t* dsub
       ScanOut su{slim, nullptr, L.obs, nullptr, nullptr, n, (uint32_t)D, (uint32_t)w, L.ctl};
       cudaMemsetAsync(L.obs, 0xFF, (size_t)n * 4, st);
       if (int r = run_scan<1, false, 5, false>(L.k_out, L.v_out, N, 0, L.tiles, su, st)) return r;
-      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st)) return r;
+      if (int r = sf1_ignore_pass(L, ks, n, N, (uint32_t)w, (uint32_t)D, st, false, true, true)) return r;
     }
     if (int r = run_engine<D, 1>(L, slim, slim_seeds, w, ks, n, 0, inc, st, false, ign)) return r;
     { note_launch(); finalize_k<<<1, 1, 0, st>>>(L.ctl, ops, 0, result, nullptr, D, 0); }
