@@ -924,6 +924,7 @@ struct RunArgs {
   uint32_t* headflag;      // [t] (written by runs_head_k)
   const uint32_t* order;   // key order (ignore pass): run extents are positions in the key-sorted op list
   int obs_by_pos;          // obs is laid out by key-order position (CU's upper bounds), not by op
+  const uint4* cbk;        // key order: the ignore pass's {count, b_min, prev, t} per position (b_min read coalesced)
   const uint32_t* hbits;   // key order: run heads as bits per op (an L2-resident copy of headflag)
   uint32_t* delbits;       // [e / 32] bit e % 32: op e (row-0 order) is a delete; may be null
   uint32_t* bnd;           // [e]: 1 if op e does not continue the run before it (run start or invalid)
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(256) runs_mark_k(RunArgs<D> a) {
     const uint32_t op = a.order ? (valid ? 0u : 1u) : (v >> a.kb) & 1u;
     const bool cont = valid && !(a.hbits ? ((__ldg(a.hbits + (t >> 5)) >> (t & 31)) & 1u) : a.headflag[t]);
     a.opflags[e] = (uint8_t)(op | (cont ? 2u : 0u) | (valid ? 4u : 0u));
-    if (a.obs) a.opdata[e] = a.obs[a.obs_by_pos ? e : t];  // per-op b_min / cap
+    if (a.obs) a.opdata[e] = a.cbk ? a.cbk[e].y : a.obs[a.obs_by_pos ? e : t];  // per-op b_min / cap
     if (a.delbits) {
       // e advances in warp-aligned strides, so the ballot covers one word
       const unsigned bits = __ballot_sync(__activemask(), op != 0);
@@ -2822,6 +2823,7 @@ static int run_engine(Layout& L, uint32_t* slim, const uint64_t* slim_seeds, int
   ra.isdel = L.isdel;
   ra.order = has_ign ? L.tb : nullptr;
   ra.obs_by_pos = 0;
+  ra.cbk = (MODE == 0 && has_ign) ? reinterpret_cast<const uint4*>(L.k64a) : nullptr;  // (sf1_ignore_pass's cb)
   ra.hbits = has_ign ? L.hbits : nullptr;
   ra.ctl = L.ctl;
   // (with dropped pairs the ignore pass has decided the run heads: runs_head_ign_k)
