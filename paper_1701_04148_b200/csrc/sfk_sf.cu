@@ -870,12 +870,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
     const bool kept = !((it.ign >> q) & 1u);
     if (!REC) {
       if (kept && before.last != kp[q]) atomicOr(bits + (j >> 5), 1u << (j & 31));
-    } else if (kept) {
+    } else if (kept && ((__ldg(bits + (j >> 5)) >> (j & 31)) & 1u)) {  // run heads, by j
       const uint32_t t = __ldg(tb + j);
-      if ((__ldg(bits + (t >> 5)) >> (t & 31)) & 1u) {
-        uint4* rec = links + ((size_t)t * D + c / row_cells) * 2;
-        st_sector(rec, make_uint4(before.cnt, before.last, 0u, 0u), make_uint4(c, e, 0u, 0u));
-      }
+      uint4* rec = links + ((size_t)t * D + c / row_cells) * 2;
+      st_sector(rec, make_uint4(before.cnt, before.last, 0u, 0u), make_uint4(c, e, 0u, 0u));
     }
     run = op(run, el);
   }
@@ -888,7 +886,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) filt_apply_k(const uint32_t* __r
 // break bit at j). Heads are written by t: run ids follow stream order.
 __global__ void runs_head_ign_k(uint32_t n, const Ctl* __restrict__ ctl, const uint8_t* __restrict__ dmask,
                                 const uint32_t* __restrict__ brk, const uint2* __restrict__ kmeta, uint32_t D,
-                                uint32_t* __restrict__ headflag, uint32_t* __restrict__ headbits) {
+                                uint32_t* __restrict__ headflag, uint32_t* __restrict__ headbits,
+                                uint32_t* __restrict__ headbits_j) {
   const uint32_t tstar = ctl->fail_t, full = (1u << D) - 1u;
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t n32 = (n + 31) & ~31u;  // whole warps, so every ballot covers one word of bits
@@ -903,6 +902,7 @@ __global__ void runs_head_ign_k(uint32_t n, const Ctl* __restrict__ ctl, const u
       if (cont) cont = dmask[j - 1] == m;
       head = valid && !cont;
       headflag[t] = head ? 1u : 0u;
+      if (head) atomicOr(headbits_j + (j >> 5), 1u << (j & 31));  // (heads are few)
     }
     const unsigned hb = __ballot_sync(0xffffffffu, head);
     if ((threadIdx.x & 31) == 0) headbits[t >> 5] = hb;
@@ -2499,6 +2499,7 @@ struct Layout {
   uint2* meta;                     //   per op: {key count, previous op of the same key}
   uint32_t* dmask;                 //   per op: a byte of dropped rows (D <= 8)
   uint32_t *rbrk, *hbits;          //   per op bits: a kept pair breaks the key's run / run head
+  uint32_t* hbitsj;                //   run heads as bits by key-order position
   uint32_t* owner;                 // SF1 shared-cell fat phase: first claimant per fat cell
   uint8_t* shared;                 //   fat cells claimed by two or more keys
   uint32_t *ncnt, *noff;           //   per op: rows on shared cells, their exclusive prefix sums
@@ -2606,6 +2607,7 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
     L.dmask = cv.take<uint32_t>(sf1 ? (uint64_t)n / 4 + 1 : 1);
     L.rbrk = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
     L.hbits = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
+    L.hbitsj = cv.take<uint32_t>(sf1 ? (uint64_t)n / 32 + 1 : 1);
     const bool f1 = kind == 1;
     L.owner = cv.take<uint32_t>(f1 ? (uint64_t)d * wp : 1);
     L.shared = cv.take<uint8_t>(f1 ? (uint64_t)d * wp : 1);
@@ -3210,6 +3212,7 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   uint32_t* kpc = L.v_in;  // the previous op per element in cell order (v_in is dead after the slim sort)
   cudaMemsetAsync(L.dmask, 0, ((size_t)n / 4 + 1) * 4, st);
   cudaMemsetAsync(L.rbrk, 0, ((size_t)n / 32 + 1) * 4, st);
+  cudaMemsetAsync(L.hbitsj, 0, ((size_t)n / 32 + 1) * 4, st);
   { note_launch(); cb_pack_k<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(L.tb, L.headpos, L.obs, bmin_by_pos ? 1 : 0, n, cb); }
   { note_launch(); sf1_ignore_k<<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, N, w, cb, L.ctl, L.ign, kpc, L.dmask); }
   // ftiles: [tile aggregates][their exclusive prefixes][scan temp storage]
@@ -3222,8 +3225,8 @@ static int sf1_ignore_pass(Layout& L, KeySrc ks, uint32_t n, uint32_t N, uint32_
   e = cub::DeviceScan::ExclusiveScan(ftmp, fbytes, ft, fc, SegCntOp(), SegCnt{0u, 0u, NONE32}, (int)ntiles, st);
   if (e != cudaSuccess) { set_error("filtered-link tiles: %s", cudaGetErrorString(e)); return (int)e; }
   { note_launch(); filt_apply_k<false><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, kpc, L.tb, L.rbrk, nullptr); }
-  { note_launch(); runs_head_ign_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(n, L.ctl, reinterpret_cast<const uint8_t*>(L.dmask), L.rbrk, L.meta, D, L.headflag, L.hbits); }
-  { note_launch(); filt_apply_k<true><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, nullptr, L.tb, L.hbits, reinterpret_cast<uint4*>(L.links)); }
+  { note_launch(); runs_head_ign_k<<<grid_for(n, 256, sms * 16), 256, 0, st>>>(n, L.ctl, reinterpret_cast<const uint8_t*>(L.dmask), L.rbrk, L.meta, D, L.headflag, L.hbits, L.hbitsj); }
+  { note_launch(); filt_apply_k<true><<<ntiles, SCAN_THREADS, 0, st>>>(L.k_out, L.v_out, L.ign, N, D, w, fc, nullptr, L.tb, L.hbitsj, reinterpret_cast<uint4*>(L.links)); }
   return check_launch("sf1_ignore");
 }
 
