@@ -2437,6 +2437,8 @@ __global__ void stats_counters_k(const uint32_t* __restrict__ c, int64_t cells, 
 }
 
 // ================================================================ host side
+constexpr uint32_t SORT_FORK_MAX_ROWS = 8;  // sort_pairs: rows sorted concurrently
+
 struct Plan {
   // sizes
   uint32_t n, N;  // ops, pairs (D*n)
@@ -2564,6 +2566,9 @@ static Layout carve(void* base, size_t cap, int kind, int d, int64_t w, int64_t 
   L.v_out = cv.take<uint32_t>(N);
   L.cub_tmp_bytes = std::max(sort_temp_bytes((uint32_t)N), scan_temp_bytes((uint32_t)n + 1));
   if (kind == 1 || kind == 2) L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, key_sort_temp_bytes((uint32_t)n));
+  // room for the d concurrent per-row sorts of sort_pairs (a few KB over one sort of all pairs)
+  if (d > 1 && d <= (int)SORT_FORK_MAX_ROWS)
+    L.cub_tmp_bytes = std::max(L.cub_tmp_bytes, (size_t)d * ((sort_temp_bytes((uint32_t)n) + 255) & ~(size_t)255));
   L.cub_tmp = cv.take<char>(L.cub_tmp_bytes);
   const uint64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
   L.tiles = cv.take<char>(scan_tiles_bytes(N));
@@ -2729,6 +2734,43 @@ static int run_scan_z(int z, const uint32_t* keys, const uint32_t* vals, uint32_
 // cells per row), so when R is a power of two each row sorts on its own over
 // log2(R) bits: for cfg 3 two 8-bit onesweep passes instead of three for the
 // 18-bit cells of all rows together.
+//
+// A row's sort alone leaves most of HBM idle (onesweep over 12M pairs: ~1.7
+// TB/s per pass, its tiles chained by the decoupled look-back), so large rows
+// sort concurrently, one side stream and one slice of the CUB workspace per
+// row, forked from and joined back into `st` with events. The side streams
+// and events are per host thread and device, so concurrent callers never
+// share an event.
+constexpr uint32_t SORT_FORK_MIN_PAIRS = 1u << 20;  // per row
+struct SortFork {
+  cudaStream_t s[SORT_FORK_MAX_ROWS] = {};
+  cudaEvent_t ev[SORT_FORK_MAX_ROWS + 1] = {};
+  bool ok = false, tried = false;
+};
+static SortFork* sort_fork() {
+  thread_local SortFork forks[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  SortFork& f = forks[dev];
+  if (!f.tried) {
+    f.tried = true;
+    f.ok = true;
+    for (uint32_t i = 0; i < SORT_FORK_MAX_ROWS && f.ok; ++i)
+      f.ok = cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking) == cudaSuccess;
+    for (uint32_t i = 0; i <= SORT_FORK_MAX_ROWS && f.ok; ++i)
+      f.ok = cudaEventCreateWithFlags(&f.ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!f.ok) cudaGetLastError();
+  }
+  return f.ok ? &f : nullptr;
+}
+static bool sort_fork_enabled() {
+  static const int v = [] {
+    const char* s = getenv("SFK_SORT_FORK");
+    return s ? atoi(s) : 1;
+  }();
+  return v != 0;
+}
+
 static int sort_pairs(Layout& L, uint32_t N, uint32_t rows, uint64_t row_cells, cudaStream_t st) {
   size_t bytes = L.cub_tmp_bytes;
   cudaError_t e = cudaSuccess;
@@ -2737,6 +2779,33 @@ static int sort_pairs(Layout& L, uint32_t N, uint32_t rows, uint64_t row_cells, 
   const bool per_row = rows > 1 && (row_cells & (row_cells - 1)) == 0 && (row_bits + 7) / 8 < (all_bits + 7) / 8;
   if (per_row) {
     const uint32_t n = N / rows;
+    size_t row_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, row_bytes, L.k_in, L.k_out, L.v_in, L.v_out, (int)n, 0,
+                                    std::max(row_bits, 1), st);
+    row_bytes = (row_bytes + 255) & ~(size_t)255;
+    SortFork* f = (sort_fork_enabled() && rows <= SORT_FORK_MAX_ROWS && n >= SORT_FORK_MIN_PAIRS &&
+                   row_bytes * rows <= L.cub_tmp_bytes)
+                      ? sort_fork()
+                      : nullptr;
+    if (f) {
+      e = cudaEventRecord(f->ev[SORT_FORK_MAX_ROWS], st);
+      for (uint32_t i = 0; i < rows && e == cudaSuccess; ++i) {
+        const size_t o = (size_t)i * n;
+        size_t b = row_bytes;
+        e = cudaStreamWaitEvent(f->s[i], f->ev[SORT_FORK_MAX_ROWS], 0);
+        if (e == cudaSuccess)
+          e = cub::DeviceRadixSort::SortPairs(static_cast<char*>(L.cub_tmp) + i * row_bytes, b, L.k_in + o,
+                                              L.k_out + o, L.v_in + o, L.v_out + o, (int)n, 0,
+                                              std::max(row_bits, 1), f->s[i]);
+        if (e == cudaSuccess) e = cudaEventRecord(f->ev[i], f->s[i]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev[i], 0);
+      }
+      if (e != cudaSuccess) {
+        set_error("radix sort (forked rows): %s", cudaGetErrorString(e));
+        return (int)e;
+      }
+      return 0;
+    }
     for (uint32_t i = 0; i < rows && e == cudaSuccess; ++i) {
       const size_t o = (size_t)i * n;
       e = cub::DeviceRadixSort::SortPairs(L.cub_tmp, bytes, L.k_in + o, L.k_out + o, L.v_in + o, L.v_out + o, (int)n, 0,
