@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--alpha", type=float, default=1.0, help="build stream skew (cfg 3)")
     ap.add_argument("--alpha-q", type=float, default=1.0, help="query rank skew (cfg 5)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-stage", type=int, default=0,
+                    help="e2e: query keys uploaded (SfSketch.stage_query_keys) before the build; 0 = none "
+                         "(measured slower: the staging copy delays the build's own upload, DESIGN.md §5.1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cm", action="store_true", help="skip the cfg-2 CM merge leg")
     ap.add_argument("--replicas", action="store_true",
@@ -577,13 +580,16 @@ def run_ours(args):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
+            # optionally, the first query keys upload on a side stream before the build
+            staged = sk.stage_query_keys(qk_h, args.e2e_stage) if args.e2e_stage > 0 else None
             if rank == 0 or rep:
                 reset()
                 sk.apply_ops(ops_h, keys_h)  # H2D inside the API call
             if world > 1 and not rep:
                 sk.broadcast_slim_(src=0)
             t1 = time.perf_counter()
-            sk.query_many_host(qk_h, out=qo_h)  # host keys in, host int64 estimates out
+            sk.query_many_host(qk_h, out=qo_h, staged=staged)  # host keys in, host int64 estimates out
+            del staged
             torch.cuda.synchronize()
             t2 = time.perf_counter()
             e = t2 - t0
@@ -607,7 +613,10 @@ def run_ours(args):
                "wire": {_lib.WIRE_C16: "u16 codes", _lib.WIRE_U32: "u32", _lib.WIRE_I64: "int64"}.get(wire, "?"),
                "apply_ms": round(sum(a for a, _ in e_split) / len(e_split) * 1e3, 3),
                "query_ms": round(sum(b for _, b in e_split) / len(e_split) * 1e3, 3),
-               "note": "apply_ops from pinned host ops/keys; queries through SfSketch.query_many_host "
+               "staged_query_keys": int(min(args.e2e_stage, qn)) if args.e2e_stage > 0 else 0,
+               "note": "apply_ops from pinned host ops/keys (staged_query_keys > 0: that many query keys upload "
+                       "on a side stream from before the build, SfSketch.stage_query_keys); queries through "
+                       "SfSketch.query_many_host "
                        "(sfk_min_query_host: chunked H2D -> query kernel -> narrowed D2H, host threads widen "
                        "into the int64 output); wall clock, max over ranks"}
         # the estimates must equal the device-resident run's

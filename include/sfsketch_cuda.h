@@ -146,6 +146,18 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
                        const void* keys_host, int key_kind, int rec_len, int64_t n, int64_t* out_host,
                        void* stream);
 
+/* sfk_min_query_host for a batch whose first n_dev keys the caller has
+ * already copied to the device (keys_dev, the same bytes as keys_host's
+ * prefix, the copy ordered before `stream`'s work): chunks wholly inside the
+ * prefix are queried in place without an H2D, so the caller can upload them
+ * while the sketch is still being built (SfSketch.stage_query_keys). No
+ * reference counterpart (the reference's query_many, sf.py:189-193, takes one
+ * host array); keys_host must still hold all n keys. n_dev = 0 is
+ * sfk_min_query_host. */
+int sfk_min_query_host_staged(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w,
+                              const void* keys_host, int key_kind, int rec_len, int64_t n, int64_t* out_host,
+                              const void* keys_dev, int64_t n_dev, void* stream);
+
 /* Tuning of sfk_min_query_host (no reference counterpart). what:
  *   0 = keys per chunk (default 2^22);
  *   1 = wire (0 auto, 1 int64, 2 u32, 3 u16 codes where exact, else u32);

@@ -33,6 +33,7 @@ EXPORTS = (
     "sfk_load_keys",
     "sfk_min_query",
     "sfk_min_query_host",
+    "sfk_min_query_host_staged",
     "sfk_host_query_config",
     "sfk_cm_workspace_size",
     "sfk_cm_apply",
@@ -100,6 +101,7 @@ def load_library() -> ctypes.CDLL:
     L.sfk_load_keys.argtypes = [P, I, I, I64, P, P]
     L.sfk_min_query.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
     L.sfk_min_query_host.argtypes = [P, P, I, I64, P, I, I, I64, P, P]
+    L.sfk_min_query_host_staged.argtypes = [P, P, I, I64, P, I, I, I64, P, P, I64, P]
     L.sfk_host_query_config.argtypes = [I, I64]
     L.sfk_host_query_config.restype = I64
     L.sfk_cm_workspace_size.argtypes = [I, I64, I64]

@@ -371,8 +371,21 @@ int64_t sfk_host_query_config(int what, int64_t value) {
   return __atomic_exchange_n(k, value, __ATOMIC_RELAXED);
 }
 
+int sfk_min_query_host_staged(const uint32_t*, const uint64_t*, int, int64_t, const void*, int, int, int64_t, int64_t*,
+                              const void*, int64_t, void*);
+
 int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w, const void* keys_host,
                        int key_kind, int rec_len, int64_t n, int64_t* out_host, void* stream) {
+  return sfk_min_query_host_staged(counters, seeds, d, w, keys_host, key_kind, rec_len, n, out_host, nullptr, 0,
+                                   stream);
+}
+
+// keys_dev: the batch's first n_dev keys already resident on the device (a
+// copy of keys_host's prefix, ordered before `stream`'s work): chunks that lie
+// wholly inside it are queried in place, with no H2D.
+int sfk_min_query_host_staged(const uint32_t* counters, const uint64_t* seeds, int d, int64_t w,
+                              const void* keys_host, int key_kind, int rec_len, int64_t n, int64_t* out_host,
+                              const void* keys_dev, int64_t n_dev, void* stream) {
   if (d < 1 || d > MAXSEEDS || w < 1 || (uint64_t)d * (uint64_t)w >= (1ull << 32)) {
     set_error("sfk_min_query_host: bad sketch shape d=%d w=%lld", d, (long long)w);
     return 1;
@@ -385,7 +398,12 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
     set_error("sfk_min_query_host: bad arguments");
     return 1;
   }
+  if (n_dev < 0 || (n_dev > 0 && !keys_dev)) {
+    set_error("sfk_min_query_host: bad staged keys");
+    return 1;
+  }
   if (n == 0) return 0;
+  n_dev = std::min(n_dev, n);
   int dev = 0;
   cudaGetDevice(&dev);
   HostQ* q = ctx_for(dev);
@@ -444,6 +462,11 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
     Slot& s = q->slots[j % ring];
     const int64_t a = j * CH, m = std::min(CH, n - a);
     const char* src = static_cast<const char*>(keys_host) + a * esz;
+    const bool staged = a + m <= n_dev;
+    const void* kdev = staged ? static_cast<const char*>(keys_dev) + a * esz : s.dkeys;
+    if (staged) {
+      // already resident: no copy; the query still waits for the slot's last D2H
+    } else {
     if (j >= ring) cudaStreamWaitEvent(q->sh, s.e_comp, 0);  // key slot free
     if (!keys_pinned) {
       if (j >= ring) cudaEventSynchronize(s.e_h2d);  // pinned staging slot free
@@ -459,8 +482,9 @@ int sfk_min_query_host(const uint32_t* counters, const uint64_t* seeds, int d, i
     cudaMemcpyAsync(s.dkeys, src, m * esz, cudaMemcpyHostToDevice, q->sh);
     cudaEventRecord(s.e_h2d, q->sh);
     cudaStreamWaitEvent(q->sc, s.e_h2d, 0);
+    }
     if (j >= ring) cudaStreamWaitEvent(q->sc, s.e_d2h, 0);  // dest / wire slot free
-    if (int r = launch_min_query(counters, seeds, d, w, KeySrc{s.dkeys, key_kind, rec_len}, m, s.dest, q->sc))
+    if (int r = launch_min_query(counters, seeds, d, w, KeySrc{kdev, key_kind, rec_len}, m, s.dest, q->sc))
       return r;
     if (!direct(j)) {
       note_launch();

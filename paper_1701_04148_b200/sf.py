@@ -100,7 +100,47 @@ def query_min(counters: torch.Tensor, seeds: np.ndarray, keys) -> torch.Tensor:
     return out
 
 
-def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_host: torch.Tensor | None = None):
+class StagedKeys:
+    """A device copy of a host key batch's first ``n`` keys, uploaded on a
+    side stream (``stage_query_keys``) so the copy can overlap a build."""
+
+    __slots__ = ("buf", "n", "kind", "rec_len", "event")
+
+    def __init__(self, buf, n, kind, rec_len, event):
+        self.buf, self.n, self.kind, self.rec_len, self.event = buf, n, kind, rec_len, event
+
+
+_stage_streams: dict = {}
+
+
+def stage_query_keys(keys_host, count: int | None = None) -> StagedKeys:
+    """Start copying the first ``count`` keys (default: all) of a host batch
+    to the device on a side stream and return at once. Pass the handle with
+    the SAME host batch to ``query_min_host(..., staged=...)``: its chunks
+    inside the staged prefix are then queried in place, with no H2D on the
+    query's critical path (``sfk_min_query_host_staged``). Pinned host keys
+    make the copy asynchronous."""
+    t, kind, rec, n = normalize_host_keys(keys_host)
+    m = n if count is None else max(0, min(int(count), n))
+    dev = device()
+    flat = t.view(torch.uint8).reshape(-1)
+    esz = flat.numel() // n if n else 1
+    cur = torch.cuda.current_stream(dev)
+    buf = torch.empty(m * esz, dtype=torch.uint8, device=dev)
+    side = _stage_streams.get(dev.index)
+    if side is None:
+        side = _stage_streams[dev.index] = torch.cuda.Stream(dev)
+    side.wait_stream(cur)  # the buffer's allocation is ordered on the current stream
+    with torch.cuda.stream(side):
+        buf.copy_(flat[: m * esz], non_blocking=True)
+    buf.record_stream(side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    return StagedKeys(buf, m, kind, rec, ev)
+
+
+def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_host: torch.Tensor | None = None,
+                   staged: StagedKeys | None = None):
     """Point queries for a batch that lives in HOST memory (pinned or
     pageable), the reference's ``query_many`` contract (``sf.py:189-193``):
     host keys in, host int64 estimates out. ``sfk_min_query_host`` cuts the
@@ -117,9 +157,17 @@ def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_hos
           or not out_host.is_contiguous()):
         raise ConfigurationError("out_host must be a contiguous int64 CPU tensor of the batch's length")
     d, w = counters.shape
+    if staged is not None and (staged.kind != kind or staged.rec_len != rec or staged.n > n):
+        raise ConfigurationError("staged keys do not match this batch's key type or length")
     if n:
-        rc = L.sfk_min_query_host(counters.data_ptr(), seeds.ctypes.data, d, w, t.data_ptr(), kind, rec, n,
-                                  out_host.data_ptr(), _lib.stream_ptr())
+        if staged is not None and staged.n:
+            torch.cuda.current_stream(device()).wait_event(staged.event)
+            rc = L.sfk_min_query_host_staged(counters.data_ptr(), seeds.ctypes.data, d, w, t.data_ptr(), kind, rec,
+                                             n, out_host.data_ptr(), staged.buf.data_ptr(), staged.n,
+                                             _lib.stream_ptr())
+        else:
+            rc = L.sfk_min_query_host(counters.data_ptr(), seeds.ctypes.data, d, w, t.data_ptr(), kind, rec, n,
+                                      out_host.data_ptr(), _lib.stream_ptr())
         _lib.check(rc, "sfk_min_query_host")
     return out_host
 
@@ -218,11 +266,18 @@ class SfSketch:
     def query_many(self, keys) -> torch.Tensor:
         return query_min(self.slim.counters, self._slim_seeds, keys)
 
-    def query_many_host(self, keys, out=None):
+    @staticmethod
+    def stage_query_keys(keys, count: int | None = None) -> StagedKeys:
+        """Upload a prefix of a host query batch before the sketch is final
+        (e.g. while ``apply_ops`` runs); see ``stage_query_keys``."""
+        return stage_query_keys(keys, count)
+
+    def query_many_host(self, keys, out=None, staged: StagedKeys | None = None):
         """``query_many`` for host-resident keys with host-resident results
         (the reference's numpy-in / numpy-out form): a numpy array for array or
-        list input, else the int64 CPU tensor ``out`` (allocated if omitted)."""
-        res = query_min_host(self.slim.counters, self._slim_seeds, keys, out)
+        list input, else the int64 CPU tensor ``out`` (allocated if omitted).
+        ``staged``: a ``stage_query_keys`` handle for a prefix of ``keys``."""
+        res = query_min_host(self.slim.counters, self._slim_seeds, keys, out, staged)
         return res if isinstance(keys, torch.Tensor) or out is not None else res.numpy()
 
     # ------------------------------------------------------------ oracle mode

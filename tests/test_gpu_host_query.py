@@ -159,3 +159,58 @@ def test_host_query_empty_and_errors(hq):
         sk.query_many_host(torch.zeros(4, dtype=torch.uint32, device="cuda"))
     with pytest.raises(ConfigurationError):
         sk.query_many_host(np.zeros((2, 2), np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["u32", "u64", "rec"])
+@pytest.mark.parametrize("staged_n", [0, 1, 65536, 2 * 65536 + 5, 3 * 65536 + 4097])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_query_staged_prefix(oracle, hq, kind, staged_n, pinned):
+    """stage_query_keys + query_min_host(staged=...): chunks wholly inside the
+    device-resident prefix are queried in place, the partly staged chunk and
+    the rest through the H2D ring; same estimates as the unstaged path."""
+    rng = np.random.default_rng(staged_n + len(kind) + 100 * pinned)
+    d, w = 4, 65536
+    c = slim_with_large(rng, d, w, 300)
+    seeds = seed_array(11, 0, d)
+    n = 3 * 65536 + 4097
+    keys = keys_for(rng, kind, n)
+    hq.sfk_host_query_config(_lib.HQ_CHUNK, 65536)
+    hq.sfk_host_query_config(_lib.HQ_RING, 2)
+    kt = torch.from_numpy(keys)
+    out = torch.full((n,), -5, dtype=torch.int64)
+    if pinned:
+        kt, out = kt.pin_memory(), out.pin_memory()
+    counters = torch.from_numpy(c).cuda()
+    st = P.sf.stage_query_keys(kt, staged_n)
+    assert st.n == staged_n
+    query_min_host(counters, seeds, kt, out, staged=st)
+    want = oracle.min_query(c, seeds, oracle_keys(oracle, kind, keys), threads=oracle.max_threads())
+    np.testing.assert_array_equal(out.numpy(), want)
+
+
+def test_host_query_staged_mismatch(hq):
+    rng = np.random.default_rng(1)
+    c = torch.from_numpy(slim_with_large(rng, 4, 4096, 0)).cuda()
+    seeds = seed_array(1, 0, 4)
+    k32 = keys_for(rng, "u32", 1000)
+    st = P.sf.stage_query_keys(k32)
+    with pytest.raises(ConfigurationError):
+        query_min_host(c, seeds, keys_for(rng, "u64", 1000), staged=st)  # other key type
+    with pytest.raises(ConfigurationError):
+        query_min_host(c, seeds, k32[:500], staged=st)  # prefix longer than the batch
+
+
+def test_query_many_host_staged_during_build(hq):
+    """The bench's e2e order: stage the query keys, build, then query."""
+    from paper_1701_04148_b200 import workloads as W
+
+    c = W.cfg3(seed=2017, n_ins=400_000, v=50_000, alpha=1.0)
+    q = np.random.default_rng(3).integers(0, 1 << 32, size=1_000_000, dtype=np.uint64).astype(np.uint32)
+    qh = torch.from_numpy(q).pin_memory()
+    hq.sfk_host_query_config(_lib.HQ_CHUNK, 1 << 16)
+    sk = P.SfSketch(P.SketchParams(d=4, w=65536, z=4, master_seed=2017), "sff")
+    st = sk.stage_query_keys(qh, 600_000)
+    sk.apply_ops(c["ops"], c["keys"])
+    got = sk.query_many_host(qh, staged=st)
+    want = sk.query_many(torch.from_numpy(q).cuda()).cpu()
+    assert torch.equal(got, want)
