@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--alpha", type=float, default=1.0, help="build stream skew (cfg 3)")
     ap.add_argument("--alpha-q", type=float, default=1.0, help="query rank skew (cfg 5)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-stage-first", action="store_true",
+                    help="e2e: start the staging copy before apply_ops instead of behind its upload")
     ap.add_argument("--e2e-stage", type=int, default=0,
                     help="e2e: query keys uploaded (SfSketch.stage_query_keys) before the build; 0 = none "
                          "(measured slower: the staging copy delays the build's own upload, DESIGN.md §5.1)")
@@ -581,7 +583,8 @@ def run_ours(args):
                 dist.barrier()
             t0 = time.perf_counter()
             # optionally, the first query keys upload on a side stream before the build
-            staged = sk.stage_query_keys(qk_h, args.e2e_stage) if args.e2e_stage > 0 else None
+            staged = (sk.stage_query_keys(qk_h, args.e2e_stage, with_next_apply=not args.e2e_stage_first)
+                      if args.e2e_stage > 0 else None)
             if rank == 0 or rep:
                 reset()
                 sk.apply_ops(ops_h, keys_h)  # H2D inside the API call

@@ -104,39 +104,51 @@ class StagedKeys:
     """A device copy of a host key batch's first ``n`` keys, uploaded on a
     side stream (``stage_query_keys``) so the copy can overlap a build."""
 
-    __slots__ = ("buf", "n", "kind", "rec_len", "event")
+    __slots__ = ("buf", "n", "kind", "rec_len", "event", "_src", "_alloc")
 
-    def __init__(self, buf, n, kind, rec_len, event):
-        self.buf, self.n, self.kind, self.rec_len, self.event = buf, n, kind, rec_len, event
+    def __init__(self, buf, n, kind, rec_len, src):
+        self.buf, self.n, self.kind, self.rec_len, self.event, self._src = buf, n, kind, rec_len, None, src
+        self._alloc = torch.cuda.Event()  # the buffer's allocation is ordered on the current stream
+        self._alloc.record(torch.cuda.current_stream(buf.device))
+
+    def issue(self) -> None:
+        """Enqueue the copy on the side stream (once)."""
+        if self.event is not None:
+            return
+        dev = self.buf.device
+        side = _stage_streams.get(dev.index)
+        if side is None:
+            side = _stage_streams[dev.index] = torch.cuda.Stream(dev)
+        side.wait_event(self._alloc)  # not on later work of the current stream (the build it overlaps)
+        with torch.cuda.stream(side):
+            self.buf.copy_(self._src, non_blocking=True)
+        self.buf.record_stream(side)
+        self.event = torch.cuda.Event()
+        self.event.record(side)
+        self._src = None
 
 
 _stage_streams: dict = {}
 
 
-def stage_query_keys(keys_host, count: int | None = None) -> StagedKeys:
+def stage_query_keys(keys_host, count: int | None = None, *, defer: bool = False) -> StagedKeys:
     """Start copying the first ``count`` keys (default: all) of a host batch
     to the device on a side stream and return at once. Pass the handle with
     the SAME host batch to ``query_min_host(..., staged=...)``: its chunks
     inside the staged prefix are then queried in place, with no H2D on the
     query's critical path (``sfk_min_query_host_staged``). Pinned host keys
-    make the copy asynchronous."""
+    make the copy asynchronous. ``defer=True`` only prepares the handle: the
+    copy starts at ``handle.issue()`` (``SfSketch.stage_query_keys`` issues it
+    inside the next ``apply_ops``, after that batch's own upload), or at the
+    query at the latest."""
     t, kind, rec, n = normalize_host_keys(keys_host)
     m = n if count is None else max(0, min(int(count), n))
-    dev = device()
     flat = t.view(torch.uint8).reshape(-1)
     esz = flat.numel() // n if n else 1
-    cur = torch.cuda.current_stream(dev)
-    buf = torch.empty(m * esz, dtype=torch.uint8, device=dev)
-    side = _stage_streams.get(dev.index)
-    if side is None:
-        side = _stage_streams[dev.index] = torch.cuda.Stream(dev)
-    side.wait_stream(cur)  # the buffer's allocation is ordered on the current stream
-    with torch.cuda.stream(side):
-        buf.copy_(flat[: m * esz], non_blocking=True)
-    buf.record_stream(side)
-    ev = torch.cuda.Event()
-    ev.record(side)
-    return StagedKeys(buf, m, kind, rec, ev)
+    h = StagedKeys(torch.empty(m * esz, dtype=torch.uint8, device=device()), m, kind, rec, flat[: m * esz])
+    if not defer:
+        h.issue()
+    return h
 
 
 def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_host: torch.Tensor | None = None,
@@ -161,6 +173,7 @@ def query_min_host(counters: torch.Tensor, seeds: np.ndarray, keys_host, out_hos
         raise ConfigurationError("staged keys do not match this batch's key type or length")
     if n:
         if staged is not None and staged.n:
+            staged.issue()
             torch.cuda.current_stream(device()).wait_event(staged.event)
             rc = L.sfk_min_query_host_staged(counters.data_ptr(), seeds.ctypes.data, d, w, t.data_ptr(), kind, rec,
                                              n, out_host.data_ptr(), staged.buf.data_ptr(), staged.n,
@@ -205,6 +218,7 @@ class SfSketch:
         self._used_normal = False
         self._used_oracle = False
         self._scratch = Scratch()
+        self._deferred_stage: list = []
 
     @property
     def kind(self) -> str:
@@ -231,6 +245,8 @@ class SfSketch:
         # op codes checked on the device; small host batches read in place from pinned staging
         ops_t, kb = normalize_stream(ops, keys, check_ops=False, stage=self._scratch)
         result = self._submit(ops_t, kb, sequential)
+        while self._deferred_stage:  # query keys staged to upload behind this batch's own
+            self._deferred_stage.pop().issue()
         status, bad, n_ins = Scratch.read(result, self._scratch)
         if kb.n and status != _lib.BAD_OPCODE:  # a rejected batch leaves the sketch untouched
             self._used_normal = True
@@ -266,11 +282,15 @@ class SfSketch:
     def query_many(self, keys) -> torch.Tensor:
         return query_min(self.slim.counters, self._slim_seeds, keys)
 
-    @staticmethod
-    def stage_query_keys(keys, count: int | None = None) -> StagedKeys:
-        """Upload a prefix of a host query batch before the sketch is final
-        (e.g. while ``apply_ops`` runs); see ``stage_query_keys``."""
-        return stage_query_keys(keys, count)
+    def stage_query_keys(self, keys, count: int | None = None, *, with_next_apply: bool = False) -> StagedKeys:
+        """Upload a prefix of a host query batch before the sketch is final;
+        see ``stage_query_keys``. ``with_next_apply=True`` starts the copy
+        inside the next ``apply_ops``, right after that batch's upload, so it
+        overlaps the build instead of delaying it."""
+        h = stage_query_keys(keys, count, defer=with_next_apply)
+        if with_next_apply:
+            self._deferred_stage.append(h)
+        return h
 
     def query_many_host(self, keys, out=None, staged: StagedKeys | None = None):
         """``query_many`` for host-resident keys with host-resident results

@@ -214,3 +214,23 @@ def test_query_many_host_staged_during_build(hq):
     got = sk.query_many_host(qh, staged=st)
     want = sk.query_many(torch.from_numpy(q).cuda()).cpu()
     assert torch.equal(got, want)
+
+
+def test_query_many_host_staged_with_next_apply(hq):
+    """with_next_apply: the copy starts inside apply_ops, behind the batch's upload."""
+    from paper_1701_04148_b200 import workloads as W
+
+    c = W.cfg3(seed=2018, n_ins=300_000, v=40_000, alpha=1.2)
+    q = np.random.default_rng(4).integers(0, 1 << 32, size=700_001, dtype=np.uint64).astype(np.uint32)
+    qh = torch.from_numpy(q).pin_memory()
+    hq.sfk_host_query_config(_lib.HQ_CHUNK, 1 << 16)
+    sk = P.SfSketch(P.SketchParams(d=4, w=65536, z=4, master_seed=2018), "sff")
+    st = sk.stage_query_keys(qh, 500_000, with_next_apply=True)
+    assert st.event is None  # not yet issued
+    sk.apply_ops(torch.from_numpy(c["ops"]).pin_memory(), torch.from_numpy(c["keys"]).pin_memory())
+    assert st.event is not None
+    got = sk.query_many_host(qh, staged=st)
+    assert torch.equal(got, sk.query_many(torch.from_numpy(q).cuda()).cpu())
+    # a deferred handle that no apply issued is issued by the query itself
+    st2 = sk.stage_query_keys(qh, 300_000, with_next_apply=True)
+    assert torch.equal(sk.query_many_host(qh, staged=st2), got)
